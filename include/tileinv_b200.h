@@ -1,0 +1,151 @@
+/*
+ * tileinv_b200.h -- C-ABI of the B200-native SPD tile inversion engine.
+ *
+ * Drop-in boundary for the reference package `tileinv`
+ * (arxiv/paper_1002_4057, /root/reference/pkg/src/tileinv). The reference is
+ * pure Python over numpy; its "FFI" for this path is the Python call surface
+ * below, which the ctypes shim `paper_1002_4057_b200/_native.py` binds 1:1:
+ *
+ *   reference interface                                  replaced by
+ *   -----------------------------------------------------------------------
+ *   tile_matrix.from_dense(m, b)       tile_matrix.py:84-99   tinv_create + tinv_put_dense
+ *   tile_matrix.to_dense(tm)           tile_matrix.py:102-114 tinv_get_dense(mode=LOWER)
+ *   symmetrize_lower(to_dense(tm))     tile_matrix.py:117-119 tinv_get_dense(mode=SYMMETRIZE)
+ *   tm.tile(i,j) / tm.set_tile(...)    tile_matrix.py:53-57   tinv_get_tile / tinv_put_tile
+ *   taskgen.gen_step1/2/3, gen_inversion taskgen.py:230-269   tinv_gen_stream
+ *   scheduler.build_dag                scheduler.py:101-153   tinv_dag_edges
+ *   scheduler.execute(stream, a, w)    scheduler.py:261-351   tinv_plan_create + tinv_plan_exec
+ *   scheduler.run_in_order(stream, a)  scheduler.py:248-258   same, flags |= TINV_SERIAL
+ *   scheduler.run_task -> kernels.*    scheduler.py:206-235   executed on device per task kind
+ *   ExecutionError(task, cause)        scheduler.py:185-190   tinv_err {task, kind, code, index}
+ *
+ * All arithmetic is IEEE FP64. Plain pointers and sizes only; no torch types.
+ * Every call blocks until the device work it issued has finished.
+ * A context is not thread-safe; use one context per host thread.
+ */
+#ifndef TILEINV_B200_H
+#define TILEINV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TINV_ABI_VERSION 1
+
+/* status codes */
+#define TINV_OK 0
+#define TINV_ERR_NOT_SPD 1     /* kernels.py:38-43  NotPositiveDefiniteError */
+#define TINV_ERR_SINGULAR 2    /* kernels.py:46-51  SingularTileError        */
+#define TINV_ERR_BAD_ARG 3     /* ValueError / InvalidSizeError               */
+#define TINV_ERR_CUDA 4        /* CUDA runtime/driver failure                 */
+#define TINV_ERR_STREAM 5      /* malformed stream (scheduler.py:274-276 and store KeyError) */
+#define TINV_ERR_NO_DEVICE 6   /* no usable sm_100 device                     */
+#define TINV_ERR_INTERNAL 7    /* executor watchdog / invariant violation     */
+
+/* kernel kinds; COPY = taskgen.py:164-170, the rest = kernels.py:23-35 */
+#define TINV_COPY 0
+#define TINV_POTRF 1
+#define TINV_TRSM 2
+#define TINV_SYRK_SUB 3
+#define TINV_SYRK_ADD_T 4
+#define TINV_GEMM 5
+#define TINV_TRTRI 6
+#define TINV_TRMM_LEFT 7
+#define TINV_TRMM_RIGHT_NEG 8
+#define TINV_TRMM_LEFT_T 9
+#define TINV_LAUUM 10
+
+/* steps (taskgen.py:37-41); select the GEMM shape (scheduler.py:198-203) */
+#define TINV_STEP_COPY 0
+#define TINV_STEP_CHOLESKY 1
+#define TINV_STEP_TRINV 2
+#define TINV_STEP_PRODUCT 3
+
+/* One task = TINV_TASK_FIELDS int32 (Task, taskgen.py:55-87):
+ * kind, step, i, j, k, out_label, out_row, out_col, out_mode, nreads,
+ * r0_label, r0_row, r0_col, r1_label, r1_row, r1_col.
+ * Labels are small ints: 0 = the matrix being executed on (its TileMatrix
+ * label), 1.. = working arrays (B, C, ...). out_mode: 1 = RW, 2 = W (COPY).
+ * Unused index / read fields are -1. */
+#define TINV_TASK_FIELDS 16
+
+/* execution flags */
+#define TINV_SERIAL 1u          /* chain tasks in stream order (run_in_order) */
+#define TINV_TRACE 2u           /* record per-task device timestamps          */
+#define TINV_KEEP_ON_FAILURE 4u /* snapshot the matrix; restore it if a task fails */
+
+/* tinv_get_dense modes */
+#define TINV_DENSE_LOWER_TILES 0 /* write only the lower tiles (to_dense on them) */
+#define TINV_DENSE_SYMMETRIZE 1  /* full matrix: lower + mirrored upper          */
+
+typedef struct tinv_err {
+  int32_t task_id;  /* reference task id of the stream-order-first failure, -1 if none */
+  int32_t kind;     /* its kernel kind                                             */
+  int32_t code;     /* TINV_ERR_*                                                  */
+  int32_t index;    /* tile-local index (pivot / zero diagonal), -1 if n/a         */
+} tinv_err;
+
+typedef struct tinv_ctx tinv_ctx;
+typedef struct tinv_plan tinv_plan;
+
+int tinv_abi_version(void);
+/* number of usable devices (sm_100), or a negative TINV_ERR_* */
+int tinv_device_count(void);
+/* last error message of a context (or the global one when ctx == NULL) */
+const char* tinv_last_error(const tinv_ctx* ctx);
+
+/* TileMatrix (tile_matrix.py:35-66): order n, tile order b, on `device`. */
+int tinv_create(tinv_ctx** ctx, int64_t n, int64_t b, int device);
+int tinv_destroy(tinv_ctx* ctx);
+int tinv_shape(const tinv_ctx* ctx, int64_t* n, int64_t* b, int64_t* t, int64_t* padded_b);
+
+/* dense row-major matrices (leading dimension lda >= n). `host` variants take
+ * host pointers (pinned memory is faster, pageable works); `device` variants
+ * take device pointers on the context's device. put copies only the lower
+ * tiles (the authoritative ones, tile_matrix.py:62-66). */
+int tinv_put_dense(tinv_ctx* ctx, const double* host, int64_t lda);
+int tinv_get_dense(tinv_ctx* ctx, double* host, int64_t lda, int mode);
+int tinv_put_dense_device(tinv_ctx* ctx, const double* dev, int64_t lda);
+int tinv_get_dense_device(tinv_ctx* ctx, double* dev, int64_t lda, int mode);
+/* one lower tile (i >= j) of the matrix, b*b row-major */
+int tinv_put_tile(tinv_ctx* ctx, int64_t i, int64_t j, const double* host);
+int tinv_get_tile(tinv_ctx* ctx, int64_t i, int64_t j, double* host);
+
+/* Native stream generation (taskgen.py:178-269). steps: bit mask 1|2|4 for
+ * steps 1,2,3; loops: 3 chars of 'U'/'D' (for a single-step stream only the
+ * first char is used); out_of_place: Placement.OUT_OF_PLACE; pipelined: no
+ * barriers between steps. If table is NULL only the counts are returned. */
+int tinv_gen_stream(int32_t t, int32_t steps, const char* loops, int32_t out_of_place,
+                    int32_t pipelined, int32_t* table, int64_t cap_tasks, int64_t* ntasks,
+                    int64_t* barriers, int64_t cap_barriers, int64_t* nbarriers);
+
+/* Hazard DAG of a stream (scheduler.py:101-153): edges (src, dst, kind) with
+ * kind 0 RAW, 1 WAR, 2 WAW, 3 barrier; same multiset as the reference. */
+int tinv_dag_edges(const int32_t* table, int64_t ntasks, const int64_t* barriers, int64_t nbar,
+                   int32_t* src, int32_t* dst, int8_t* kind, int64_t cap, int64_t* nedges);
+
+/* Plan = the device-resident executable form of a stream on a context
+ * (hazard DAG, renaming slots, priorities, ready queues). Reusable. */
+int tinv_plan_create(tinv_ctx* ctx, const int32_t* table, int64_t ntasks, int32_t stream_t,
+                     const int64_t* barriers, int64_t nbar, uint32_t flags, tinv_plan** plan,
+                     tinv_err* err);
+/* run the plan on the context's matrix; blocks. ms (optional) = device time
+ * of the executor launch measured with CUDA events. */
+int tinv_plan_exec(tinv_plan* plan, tinv_err* err, double* ms);
+int tinv_plan_destroy(tinv_plan* plan);
+/* plan statistics: exec tasks (incl. hidden INV tasks), work items, edges */
+int tinv_plan_stats(const tinv_plan* plan, int64_t* exec_tasks, int64_t* items, int64_t* edges);
+/* per reference task: device start/end (ns since launch) and SM id; TRACE only */
+int tinv_plan_trace(const tinv_plan* plan, int64_t* start_ns, int64_t* end_ns, int32_t* sm,
+                    int64_t ntasks);
+
+/* convenience: plan_create + plan_exec + plan_destroy */
+int tinv_run(tinv_ctx* ctx, const int32_t* table, int64_t ntasks, int32_t stream_t,
+             const int64_t* barriers, int64_t nbar, uint32_t flags, tinv_err* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TILEINV_B200_H */

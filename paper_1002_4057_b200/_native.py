@@ -1,0 +1,249 @@
+"""ctypes binding of libtileinv_b200.so (include/tileinv_b200.h).
+
+The library is the product: every numeric operation of the package runs
+through it on the B200. There is no CPU fallback -- if the library is missing
+or no sm_100 device is present, calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libtileinv_b200.so")
+
+TASK_FIELDS = 16
+OK, ERR_NOT_SPD, ERR_SINGULAR, ERR_BAD_ARG, ERR_CUDA, ERR_STREAM, ERR_NO_DEVICE, ERR_INTERNAL = range(8)
+SERIAL, TRACE, KEEP_ON_FAILURE = 1, 2, 4
+DENSE_LOWER, DENSE_SYMMETRIZE = 0, 1
+
+# every symbol include/tileinv_b200.h declares
+EXPORTS = (
+    "tinv_abi_version", "tinv_device_count", "tinv_last_error", "tinv_create", "tinv_destroy",
+    "tinv_shape", "tinv_put_dense", "tinv_get_dense", "tinv_put_dense_device", "tinv_get_dense_device",
+    "tinv_put_tile", "tinv_get_tile", "tinv_gen_stream", "tinv_dag_edges", "tinv_plan_create",
+    "tinv_plan_exec", "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
+)
+
+
+class TinvErr(ctypes.Structure):
+    _fields_ = [("task_id", ctypes.c_int32), ("kind", ctypes.c_int32), ("code", ctypes.c_int32),
+                ("index", ctypes.c_int32)]
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code, msg):
+        self.code = code
+        super().__init__(f"libtileinv_b200 error {code}: {msg}")
+
+
+_lib = None
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_U32 = ctypes.c_uint32
+_DP = ctypes.POINTER(ctypes.c_double)
+_I32P = ctypes.POINTER(ctypes.c_int32)
+_I64P = ctypes.POINTER(ctypes.c_int64)
+
+
+def lib():
+    """Load the native library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `python __graft_entry__.py build` "
+                           "(nvcc, sm_100a); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    sig = {
+        "tinv_abi_version": ([], ctypes.c_int),
+        "tinv_device_count": ([], ctypes.c_int),
+        "tinv_last_error": ([_P], ctypes.c_char_p),
+        "tinv_create": ([ctypes.POINTER(_P), _I64, _I64, ctypes.c_int], ctypes.c_int),
+        "tinv_destroy": ([_P], ctypes.c_int),
+        "tinv_shape": ([_P, _I64P, _I64P, _I64P, _I64P], ctypes.c_int),
+        "tinv_put_dense": ([_P, _DP, _I64], ctypes.c_int),
+        "tinv_get_dense": ([_P, _DP, _I64, ctypes.c_int], ctypes.c_int),
+        "tinv_put_dense_device": ([_P, _P, _I64], ctypes.c_int),
+        "tinv_get_dense_device": ([_P, _P, _I64, ctypes.c_int], ctypes.c_int),
+        "tinv_put_tile": ([_P, _I64, _I64, _DP], ctypes.c_int),
+        "tinv_get_tile": ([_P, _I64, _I64, _DP], ctypes.c_int),
+        "tinv_gen_stream": ([_I32, _I32, ctypes.c_char_p, _I32, _I32, _I32P, _I64, _I64P, _I64P, _I64, _I64P],
+                            ctypes.c_int),
+        "tinv_dag_edges": ([_I32P, _I64, _I64P, _I64, _I32P, _I32P, ctypes.POINTER(ctypes.c_int8), _I64, _I64P],
+                           ctypes.c_int),
+        "tinv_plan_create": ([_P, _I32P, _I64, _I32, _I64P, _I64, _U32, ctypes.POINTER(_P),
+                              ctypes.POINTER(TinvErr)], ctypes.c_int),
+        "tinv_plan_exec": ([_P, ctypes.POINTER(TinvErr), ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+        "tinv_plan_destroy": ([_P], ctypes.c_int),
+        "tinv_plan_stats": ([_P, _I64P, _I64P, _I64P], ctypes.c_int),
+        "tinv_plan_trace": ([_P, _I64P, _I64P, _I32P, _I64], ctypes.c_int),
+        "tinv_run": ([_P, _I32P, _I64, _I32, _I64P, _I64, _U32, ctypes.POINTER(TinvErr)], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    if L.tinv_abi_version() != 1:
+        raise RuntimeError("libtileinv_b200.so ABI mismatch")
+    _lib = L
+    return L
+
+
+def _dp(a):
+    return a.ctypes.data_as(_DP)
+
+
+def _ip(a):
+    return a.ctypes.data_as(_I32P) if a is not None else None
+
+
+def _lp(a):
+    return a.ctypes.data_as(_I64P) if a is not None and len(a) else None
+
+
+def last_error(ctx=None):
+    m = lib().tinv_last_error(ctx)
+    return m.decode() if m else ""
+
+
+def check(rc, ctx=None):
+    if rc != OK:
+        raise NativeError(rc, last_error(ctx))
+
+
+def device_count():
+    return lib().tinv_device_count()
+
+
+def gen_stream(t, steps_mask, loops, out_of_place, pipelined):
+    """Native task-stream generation -> (table int32[n,16], barriers int64[k])."""
+    L = lib()
+    n = ctypes.c_int64()
+    nb = ctypes.c_int64()
+    lp = loops.encode()
+    check(L.tinv_gen_stream(t, steps_mask, lp, int(out_of_place), int(pipelined), None, 0, ctypes.byref(n),
+                            None, 0, ctypes.byref(nb)))
+    table = np.empty((n.value, TASK_FIELDS), dtype=np.int32)
+    bars = np.empty(max(nb.value, 1), dtype=np.int64)
+    check(L.tinv_gen_stream(t, steps_mask, lp, int(out_of_place), int(pipelined), _ip(table), n.value,
+                            ctypes.byref(n), bars.ctypes.data_as(_I64P), len(bars), ctypes.byref(nb)))
+    return table, bars[:nb.value].copy()
+
+
+def dag_edges(table, barriers):
+    """Native hazard scoreboard: (src, dst, kind) arrays, kind 0 RAW 1 WAR 2 WAW 3 barrier."""
+    L = lib()
+    table = np.ascontiguousarray(table, dtype=np.int32)
+    bars = np.ascontiguousarray(barriers, dtype=np.int64)
+    ne = ctypes.c_int64()
+    check(L.tinv_dag_edges(_ip(table), len(table), _lp(bars), len(bars), None, None, None, 0, ctypes.byref(ne)))
+    src = np.empty(ne.value, dtype=np.int32)
+    dst = np.empty(ne.value, dtype=np.int32)
+    kind = np.empty(ne.value, dtype=np.int8)
+    check(L.tinv_dag_edges(_ip(table), len(table), _lp(bars), len(bars), _ip(src), _ip(dst),
+                           kind.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)), ne.value, ctypes.byref(ne)))
+    return src, dst, kind
+
+
+class Context:
+    """One device tile store (tinv_ctx) for an order-n matrix with tile order b."""
+
+    def __init__(self, n, b, device=0):
+        L = lib()
+        h = _P()
+        rc = L.tinv_create(ctypes.byref(h), n, b, device)
+        if rc != OK:
+            raise NativeError(rc, last_error(None))
+        self.h = h
+        self.n, self.b = n, b
+        self.t = n // b
+
+    def close(self):
+        if self.h:
+            lib().tinv_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+    def put_dense(self, m):
+        m = np.ascontiguousarray(m, dtype=np.float64)
+        check(lib().tinv_put_dense(self.h, _dp(m), m.shape[1]), self.h)
+
+    def get_dense(self, out, mode=DENSE_LOWER):
+        assert out.dtype == np.float64 and out.flags["C_CONTIGUOUS"]
+        check(lib().tinv_get_dense(self.h, _dp(out), out.shape[1], mode), self.h)
+        return out
+
+    def put_dense_device(self, ptr, lda):
+        check(lib().tinv_put_dense_device(self.h, ctypes.c_void_p(ptr), lda), self.h)
+
+    def get_dense_device(self, ptr, lda, mode=DENSE_SYMMETRIZE):
+        check(lib().tinv_get_dense_device(self.h, ctypes.c_void_p(ptr), lda, mode), self.h)
+
+    def put_tile(self, i, j, tile):
+        tile = np.ascontiguousarray(tile, dtype=np.float64)
+        check(lib().tinv_put_tile(self.h, i, j, _dp(tile)), self.h)
+
+    def get_tile(self, i, j):
+        out = np.empty((self.b, self.b))
+        check(lib().tinv_get_tile(self.h, i, j, _dp(out)), self.h)
+        return out
+
+
+class Plan:
+    """A stream compiled for the device executor on one Context (reusable)."""
+
+    def __init__(self, ctx, table, t, barriers, flags=0):
+        L = lib()
+        self.ctx = ctx
+        self.table = np.ascontiguousarray(table, dtype=np.int32)
+        self.barriers = np.ascontiguousarray(barriers, dtype=np.int64)
+        self.h = _P()
+        self.err = TinvErr()
+        rc = L.tinv_plan_create(ctx.h, _ip(self.table), len(self.table), t, _lp(self.barriers),
+                                len(self.barriers), flags, ctypes.byref(self.h), ctypes.byref(self.err))
+        self.rc = rc
+        self.msg = last_error(ctx.h) if rc != OK else ""
+
+    def run(self):
+        """-> (rc, TinvErr, device ms)."""
+        if self.rc != OK:
+            return self.rc, self.err, 0.0
+        ms = ctypes.c_double()
+        rc = lib().tinv_plan_exec(self.h, ctypes.byref(self.err), ctypes.byref(ms))
+        self.msg = last_error(self.ctx.h) if rc != OK else ""
+        return rc, self.err, ms.value
+
+    def stats(self):
+        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(lib().tinv_plan_stats(self.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return {"exec_tasks": a.value, "items": b.value, "edges": c.value}
+
+    def trace(self):
+        n = len(self.table)
+        s = np.empty(n, np.int64)
+        e = np.empty(n, np.int64)
+        sm = np.empty(n, np.int32)
+        check(lib().tinv_plan_trace(self.h, s.ctypes.data_as(_I64P), e.ctypes.data_as(_I64P), _ip(sm), n))
+        return s, e, sm
+
+    def close(self):
+        if self.h:
+            lib().tinv_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

@@ -1,0 +1,1037 @@
+// C-ABI of the B200 SPD tile-inversion engine (include/tileinv_b200.h):
+// device tile store, layout conversion, native stream generation
+// (taskgen.py), the hazard scoreboard (scheduler.py:101-153), the planner
+// that turns a stream into a device-resident DAG, and the executor launch.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "tinv_internal.h"
+
+namespace tinv {
+cudaError_t launch_exec(const CUtensorMap& tmK, const CUtensorMap& tmM, const ExecParams& P, int b, int grid,
+                        cudaStream_t stream);
+cudaError_t launch_put(const double* src, int64_t lda, int64_t row0, double* pool, int64_t slot_elems,
+                       const int32_t* slot_of, int b, int bp, int64_t tri_lo, int64_t ntiles, cudaStream_t st);
+cudaError_t launch_get(double* dst, int64_t ldd, int64_t row0, const double* pool, int64_t slot_elems,
+                       const int32_t* slot_of, int b, int bp, int t, int panel_i, int64_t tile_lo,
+                       int64_t ntiles, int symmetrize, cudaStream_t st);
+cudaError_t launch_copy_slots(double* pool, int64_t slot_elems, const int32_t* from, const int32_t* to,
+                              int64_t n, cudaStream_t st);
+}  // namespace tinv
+
+using namespace tinv;
+
+static std::string g_err;
+
+struct tinv_ctx {
+  int64_t n = 0, b = 0, t = 0, bp = 0, R = 0, T = 0;
+  int device = 0, nsm = 0;
+  cudaStream_t st = nullptr, st2 = nullptr;
+  double* pool = nullptr;
+  int64_t pool_slots = 0, slot_elems = 0;
+  std::vector<int32_t> a_slot;  // current slot of each lower tile (home k or shadow T+k)
+  int32_t* d_a_slot = nullptr;
+  double* staging[2] = {nullptr, nullptr};
+  size_t staging_bytes = 0;
+  CUtensorMap tmK, tmM;
+  std::string err;
+};
+
+#define CK(ctx, call)                                                                               \
+  do {                                                                                              \
+    cudaError_t e_ = (call);                                                                        \
+    if (e_ != cudaSuccess) {                                                                        \
+      std::string m_ = std::string(#call) + ": " + cudaGetErrorString(e_);                          \
+      if (ctx) (ctx)->err = m_;                                                                     \
+      g_err = m_;                                                                                   \
+      return TINV_ERR_CUDA;                                                                         \
+    }                                                                                               \
+  } while (0)
+
+static int fail(tinv_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  g_err = msg;
+  return code;
+}
+
+// ------------------------------------------------------------------ tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static int make_maps(tinv_ctx* c) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    CK(c, cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) return fail(c, TINV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = (EncodeTiledFn)p;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)c->bp, (cuuint64_t)c->bp, (cuuint64_t)c->pool_slots};
+  cuuint64_t strides[2] = {(cuuint64_t)c->bp * 8, (cuuint64_t)c->bp * c->bp * 8};
+  cuuint32_t estr[3] = {1, 1, 1};
+  cuuint32_t boxK[3] = {KCH, BLK, 1};  // 16 doubles (128 B) x 128 rows
+  cuuint32_t boxM[3] = {16, KCH, 1};   // 16 doubles x 16 rows
+  CUresult r1 = fn(&c->tmK, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->pool, dims, strides, boxK, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r2 = fn(&c->tmM, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->pool, dims, strides, boxM, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS)
+    return fail(c, TINV_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r1) + "/" + std::to_string(r2));
+  return TINV_OK;
+}
+
+// grow the slot pool to at least `slots`, keeping the matrix region [0, 2T)
+static int ensure_pool(tinv_ctx* c, int64_t slots) {
+  if (slots <= c->pool_slots) return TINV_OK;
+  CK(c, cudaSetDevice(c->device));
+  double* np = nullptr;
+  CK(c, cudaMalloc(&np, (size_t)slots * c->slot_elems * 8));
+  if (c->pool) {
+    CK(c, cudaMemcpyAsync(np, c->pool, (size_t)std::min<int64_t>(c->pool_slots, 2 * c->T) * c->slot_elems * 8,
+                          cudaMemcpyDeviceToDevice, c->st));
+    CK(c, cudaStreamSynchronize(c->st));
+    CK(c, cudaFree(c->pool));
+  }
+  c->pool = np;
+  c->pool_slots = slots;
+  return make_maps(c);
+}
+
+// ------------------------------------------------------------------ C-ABI: context
+extern "C" {
+
+int tinv_abi_version(void) { return TINV_ABI_VERSION; }
+
+const char* tinv_last_error(const tinv_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+int tinv_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int ok = 0;
+  for (int d = 0; d < n; ++d) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++ok;
+  }
+  return ok;
+}
+
+int tinv_create(tinv_ctx** out, int64_t n, int64_t b, int device) {
+  if (!out) return fail(nullptr, TINV_ERR_BAD_ARG, "null ctx pointer");
+  *out = nullptr;
+  if (n < 1 || b < 1 || n % b) return fail(nullptr, TINV_ERR_BAD_ARG, "matrix order not divisible by tile order");
+  int nd = 0;
+  if (cudaGetDeviceCount(&nd) != cudaSuccess || device < 0 || device >= nd) {
+    cudaGetLastError();
+    return fail(nullptr, TINV_ERR_NO_DEVICE, "no CUDA device");
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10)
+    return fail(nullptr, TINV_ERR_NO_DEVICE, "device is not sm_100 (B200)");
+  tinv_ctx* c = new tinv_ctx();
+  c->n = n;
+  c->b = b;
+  c->t = n / b;
+  c->bp = (b + BLK - 1) / BLK * BLK;
+  c->R = c->bp / BLK;
+  c->T = c->t * (c->t + 1) / 2;
+  c->device = device;
+  c->nsm = prop.multiProcessorCount;
+  c->slot_elems = c->bp * c->bp;
+  int rc = TINV_OK;
+  auto bail = [&](int code) {
+    tinv_destroy(c);
+    return code;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return bail(fail(nullptr, TINV_ERR_CUDA, "cudaSetDevice failed"));
+  if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(nullptr, TINV_ERR_CUDA, "stream create failed"));
+  c->a_slot.resize(c->T);
+  for (int64_t k = 0; k < c->T; ++k) c->a_slot[k] = (int32_t)k;
+  if (cudaMalloc(&c->d_a_slot, c->T * sizeof(int32_t)) != cudaSuccess)
+    return bail(fail(nullptr, TINV_ERR_CUDA, "cudaMalloc failed"));
+  cudaMemcpy(c->d_a_slot, c->a_slot.data(), c->T * sizeof(int32_t), cudaMemcpyHostToDevice);
+  rc = ensure_pool(c, 2 * c->T + c->nsm);
+  if (rc != TINV_OK) {
+    g_err = c->err;
+    return bail(rc);
+  }
+  *out = c;
+  return TINV_OK;
+}
+
+int tinv_destroy(tinv_ctx* c) {
+  if (!c) return TINV_OK;
+  cudaSetDevice(c->device);
+  if (c->pool) cudaFree(c->pool);
+  if (c->d_a_slot) cudaFree(c->d_a_slot);
+  for (auto& s : c->staging)
+    if (s) cudaFree(s);
+  if (c->st) cudaStreamDestroy(c->st);
+  if (c->st2) cudaStreamDestroy(c->st2);
+  delete c;
+  return TINV_OK;
+}
+
+int tinv_shape(const tinv_ctx* c, int64_t* n, int64_t* b, int64_t* t, int64_t* bp) {
+  if (!c) return TINV_ERR_BAD_ARG;
+  if (n) *n = c->n;
+  if (b) *b = c->b;
+  if (t) *t = c->t;
+  if (bp) *bp = c->bp;
+  return TINV_OK;
+}
+
+static int ensure_staging(tinv_ctx* c) {
+  const size_t need = (size_t)c->b * c->n * 8;
+  if (c->staging_bytes >= need) return TINV_OK;
+  for (auto& s : c->staging) {
+    if (s) cudaFree(s);
+    s = nullptr;
+    CK(c, cudaMalloc(&s, need));
+  }
+  c->staging_bytes = need;
+  return TINV_OK;
+}
+
+static int sync_slots(tinv_ctx* c) {
+  CK(c, cudaMemcpyAsync(c->d_a_slot, c->a_slot.data(), c->T * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+  return TINV_OK;
+}
+
+int tinv_put_dense_device(tinv_ctx* c, const double* dev, int64_t lda) {
+  if (!c || !dev || lda < c->n) return fail(c, TINV_ERR_BAD_ARG, "bad put_dense_device arguments");
+  CK(c, cudaSetDevice(c->device));
+  int rc = sync_slots(c);
+  if (rc) return rc;
+  CK(c, launch_put(dev, lda, 0, c->pool, c->slot_elems, c->d_a_slot, (int)c->b, (int)c->bp, 0, c->T, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  return TINV_OK;
+}
+
+int tinv_get_dense_device(tinv_ctx* c, double* dev, int64_t lda, int mode) {
+  if (!c || !dev || lda < c->n) return fail(c, TINV_ERR_BAD_ARG, "bad get_dense_device arguments");
+  CK(c, cudaSetDevice(c->device));
+  int rc = sync_slots(c);
+  if (rc) return rc;
+  const int sym = mode == TINV_DENSE_SYMMETRIZE;
+  CK(c, launch_get(dev, lda, 0, c->pool, c->slot_elems, c->d_a_slot, (int)c->b, (int)c->bp, (int)c->t, -1, 0,
+                   sym ? c->t * c->t : c->T, sym, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  return TINV_OK;
+}
+
+// Host transfers go by tile-row panels through two device staging buffers:
+// H2D of panel i+1 (copy stream) overlaps the conversion of panel i.
+int tinv_put_dense(tinv_ctx* c, const double* host, int64_t lda) {
+  if (!c || !host || lda < c->n) return fail(c, TINV_ERR_BAD_ARG, "bad put_dense arguments");
+  CK(c, cudaSetDevice(c->device));
+  int rc = ensure_staging(c);
+  if (rc) return rc;
+  rc = sync_slots(c);
+  if (rc) return rc;
+  cudaEvent_t copied[2], freed[2];
+  for (int k = 0; k < 2; ++k) {
+    CK(c, cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming));
+    CK(c, cudaEventRecord(freed[k], c->st));
+  }
+  const int64_t b = c->b, n = c->n;
+  for (int64_t i = 0; i < c->t; ++i) {
+    const int k = (int)(i & 1);
+    CK(c, cudaStreamWaitEvent(c->st2, freed[k], 0));
+    CK(c, cudaMemcpy2DAsync(c->staging[k], n * 8, host + i * b * lda, lda * 8, (size_t)(i + 1) * b * 8, b,
+                            cudaMemcpyHostToDevice, c->st2));
+    CK(c, cudaEventRecord(copied[k], c->st2));
+    CK(c, cudaStreamWaitEvent(c->st, copied[k], 0));
+    CK(c, launch_put(c->staging[k], n, i * b, c->pool, c->slot_elems, c->d_a_slot, (int)b, (int)c->bp,
+                     tri_index(i, 0), i + 1, c->st));
+    CK(c, cudaEventRecord(freed[k], c->st));
+  }
+  CK(c, cudaStreamSynchronize(c->st));
+  CK(c, cudaStreamSynchronize(c->st2));
+  for (int k = 0; k < 2; ++k) {
+    cudaEventDestroy(copied[k]);
+    cudaEventDestroy(freed[k]);
+  }
+  return TINV_OK;
+}
+
+int tinv_get_dense(tinv_ctx* c, double* host, int64_t lda, int mode) {
+  if (!c || !host || lda < c->n) return fail(c, TINV_ERR_BAD_ARG, "bad get_dense arguments");
+  CK(c, cudaSetDevice(c->device));
+  int rc = ensure_staging(c);
+  if (rc) return rc;
+  rc = sync_slots(c);
+  if (rc) return rc;
+  const int sym = mode == TINV_DENSE_SYMMETRIZE;
+  cudaEvent_t built[2], freed[2];
+  for (int k = 0; k < 2; ++k) {
+    CK(c, cudaEventCreateWithFlags(&built[k], cudaEventDisableTiming));
+    CK(c, cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming));
+    CK(c, cudaEventRecord(freed[k], c->st2));
+  }
+  const int64_t b = c->b, n = c->n;
+  for (int64_t i = 0; i < c->t; ++i) {
+    const int k = (int)(i & 1);
+    const int64_t ntile = sym ? c->t : i + 1;
+    CK(c, cudaStreamWaitEvent(c->st, freed[k], 0));
+    CK(c, launch_get(c->staging[k], n, i * b, c->pool, c->slot_elems, c->d_a_slot, (int)b, (int)c->bp,
+                     (int)c->t, (int)i, 0, ntile, sym, c->st));
+    CK(c, cudaEventRecord(built[k], c->st));
+    CK(c, cudaStreamWaitEvent(c->st2, built[k], 0));
+    CK(c, cudaMemcpy2DAsync(host + i * b * lda, lda * 8, c->staging[k], n * 8, (size_t)ntile * b * 8, b,
+                            cudaMemcpyDeviceToHost, c->st2));
+    CK(c, cudaEventRecord(freed[k], c->st2));
+  }
+  CK(c, cudaStreamSynchronize(c->st));
+  CK(c, cudaStreamSynchronize(c->st2));
+  for (int k = 0; k < 2; ++k) {
+    cudaEventDestroy(built[k]);
+    cudaEventDestroy(freed[k]);
+  }
+  return TINV_OK;
+}
+
+int tinv_put_tile(tinv_ctx* c, int64_t i, int64_t j, const double* host) {
+  if (!c || !host || i < 0 || j < 0 || j > i || i >= c->t) return fail(c, TINV_ERR_BAD_ARG, "bad tile index");
+  CK(c, cudaSetDevice(c->device));
+  int rc = sync_slots(c);
+  if (rc) return rc;
+  double* tmp = nullptr;
+  CK(c, cudaMalloc(&tmp, (size_t)c->b * c->b * 8));
+  CK(c, cudaMemcpyAsync(tmp, host, (size_t)c->b * c->b * 8, cudaMemcpyHostToDevice, c->st));
+  const int64_t x = tri_index(i, j);
+  CK(c, launch_put(tmp - i * c->b * c->b - j * c->b, c->b, 0, c->pool, c->slot_elems, c->d_a_slot, (int)c->b,
+                   (int)c->bp, x, 1, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  cudaFree(tmp);
+  return TINV_OK;
+}
+
+int tinv_get_tile(tinv_ctx* c, int64_t i, int64_t j, double* host) {
+  if (!c || !host || i < 0 || j < 0 || j > i || i >= c->t) return fail(c, TINV_ERR_BAD_ARG, "bad tile index");
+  CK(c, cudaSetDevice(c->device));
+  const int64_t b = c->b;
+  CK(c, cudaMemcpy2D(host, b * 8, c->pool + (int64_t)c->a_slot[tri_index(i, j)] * c->slot_elems, c->bp * 8, b * 8,
+                     b, cudaMemcpyDeviceToHost));
+  return TINV_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ streams and DAGs
+namespace {
+
+struct Tk {
+  int32_t f[TINV_TASK_FIELDS];
+};
+
+enum { F_KIND, F_STEP, F_I, F_J, F_K, F_OL, F_OR, F_OC, F_OM, F_NR, F_R0L, F_R0R, F_R0C, F_R1L, F_R1R, F_R1C };
+
+struct Gen {
+  std::vector<Tk> tasks;
+  void add(int kind, int step, int i, int j, int k, int ol, int orr, int oc, int mode, int nr, int r0l = -1,
+           int r0r = -1, int r0c = -1, int r1l = -1, int r1r = -1, int r1c = -1) {
+    Tk t = {{kind, step, i, j, k, ol, orr, oc, mode, nr, r0l, r0r, r0c, r1l, r1r, r1c}};
+    tasks.push_back(t);
+  }
+  // taskgen.py:164-170
+  void copies(int t, int src, int dst) {
+    for (int r = 0; r < t; ++r)
+      for (int c = 0; c <= r; ++c) add(TINV_COPY, TINV_STEP_COPY, r, c, -1, dst, r, c, 2, 1, src, r, c);
+  }
+  // taskgen.py:178-189
+  void step1(int t, char d) {
+    for (int j = 0; j < t; ++j) {
+      for (int k = 0; k < j; ++k) add(TINV_SYRK_SUB, 1, j, k, -1, 0, j, j, 1, 1, 0, j, k);
+      add(TINV_POTRF, 1, j, -1, -1, 0, j, j, 1, 0);
+      for (int i = j + 1; i < t; ++i)
+        for (int s = 0; s < j; ++s) {
+          const int k = d == 'U' ? s : j - 1 - s;
+          add(TINV_GEMM, 1, i, j, k, 0, i, j, 1, 2, 0, i, k, 0, j, k);
+        }
+      for (int i = j + 1; i < t; ++i) add(TINV_TRSM, 1, i, j, -1, 0, i, j, 1, 1, 0, j, j);
+    }
+  }
+  // taskgen.py:192-205
+  void step2(int t, char d, bool oop) {
+    if (oop && t > 1) copies(t, 0, 1);
+    const int col = oop ? 1 : 0;
+    for (int j = t - 1; j >= 0; --j) {
+      add(TINV_TRTRI, 2, j, -1, -1, 0, j, j, 1, 0);
+      for (int i = t - 1; i > j; --i) {
+        add(TINV_TRMM_LEFT, 2, i, j, -1, 0, i, j, 1, 1, 0, i, i);
+        const int lo = j + 1, hi = i;
+        for (int s = 0; s < hi - lo; ++s) {
+          const int k = d == 'U' ? lo + s : hi - 1 - s;
+          add(TINV_GEMM, 2, i, j, k, 0, i, j, 1, 2, 0, i, k, col, k, j);
+        }
+        add(TINV_TRMM_RIGHT_NEG, 2, i, j, -1, 0, i, j, 1, 1, 0, j, j);
+      }
+    }
+  }
+  // taskgen.py:208-223
+  void step3(int t, char d, bool oop) {
+    if (oop && t > 1) copies(t, 0, 2);
+    const int src = oop ? 2 : 0;
+    for (int i = 0; i < t; ++i) {
+      for (int j = 0; j < i; ++j) add(TINV_TRMM_LEFT_T, 3, i, j, -1, 0, i, j, 1, 1, src, i, i);
+      add(TINV_LAUUM, 3, i, -1, -1, 0, i, i, 1, 0);
+      for (int j = 0; j < i; ++j) {
+        const int lo = i + 1, hi = t;
+        for (int s = 0; s < hi - lo; ++s) {
+          const int k = d == 'U' ? lo + s : hi - 1 - s;
+          add(TINV_GEMM, 3, i, j, k, 0, i, j, 1, 2, src, k, i, src, k, j);
+        }
+      }
+      for (int k = i + 1; k < t; ++k) add(TINV_SYRK_ADD_T, 3, i, k, -1, 0, i, i, 1, 1, src, k, i);
+    }
+  }
+};
+
+// accesses of a task: reads (operand order) then the output
+struct Acc {
+  int64_t tile;
+  int mode;  // 0 R, 1 RW, 2 W
+};
+
+struct Edge {
+  int32_t u, v;
+  int8_t kind;  // 0 RAW 1 WAR 2 WAW 3 barrier
+};
+
+// Scoreboard of scheduler.py:101-140 over abstract tile keys + barrier edges
+// (scheduler.py:143-153: prefix sinks -> suffix sources).
+void scoreboard(int64_t n, const std::vector<std::vector<Acc>>& acc, const std::vector<int64_t>& barriers,
+                std::vector<Edge>& edges) {
+  std::unordered_map<int64_t, int32_t> last_writer;
+  std::unordered_map<int64_t, std::vector<int32_t>> readers;
+  last_writer.reserve(n * 2);
+  readers.reserve(n * 2);
+  std::vector<std::pair<int32_t, int64_t>> raw;
+  for (int64_t v = 0; v < n; ++v) {
+    raw.clear();
+    for (const Acc& a : acc[v])
+      if (a.mode == 0 || a.mode == 1) {
+        auto it = last_writer.find(a.tile);
+        if (it != last_writer.end()) {
+          edges.push_back({it->second, (int32_t)v, 0});
+          raw.push_back({it->second, a.tile});
+        }
+      }
+    for (const Acc& a : acc[v])
+      if (a.mode == 1 || a.mode == 2) {
+        auto rit = readers.find(a.tile);
+        if (rit != readers.end())
+          for (int32_t r : rit->second) edges.push_back({r, (int32_t)v, 1});
+        auto it = last_writer.find(a.tile);
+        if (it != last_writer.end()) {
+          bool has = false;
+          for (auto& p : raw)
+            if (p.first == it->second && p.second == a.tile) has = true;
+          if (!has) edges.push_back({it->second, (int32_t)v, 2});
+        }
+      }
+    for (const Acc& a : acc[v])
+      if (a.mode == 0 || a.mode == 1) readers[a.tile].push_back((int32_t)v);
+    for (const Acc& a : acc[v])
+      if (a.mode == 1 || a.mode == 2) {
+        last_writer[a.tile] = (int32_t)v;
+        readers[a.tile].clear();
+      }
+  }
+  std::vector<int64_t> bs(barriers);
+  std::sort(bs.begin(), bs.end());
+  for (int64_t pos : bs) {
+    std::vector<char> has_out(n, 0), has_in(n, 0);
+    for (const Edge& e : edges) {
+      if (e.u < pos && e.v < pos) has_out[e.u] = 1;
+      if (e.u >= pos && e.v >= pos) has_in[e.v] = 1;
+    }
+    std::vector<int32_t> sinks, sources;
+    for (int64_t u = 0; u < std::min<int64_t>(pos, n); ++u)
+      if (!has_out[u]) sinks.push_back((int32_t)u);
+    for (int64_t v = std::max<int64_t>(pos, 0); v < n; ++v)
+      if (!has_in[v]) sources.push_back((int32_t)v);
+    for (int32_t u : sinks)
+      for (int32_t v : sources) edges.push_back({u, v, 3});
+  }
+}
+
+int64_t tile_key(int label, int r, int c) { return ((int64_t)label << 40) | ((int64_t)r << 20) | (int64_t)c; }
+
+void ref_accesses(const int32_t* table, int64_t n, std::vector<std::vector<Acc>>& acc) {
+  acc.resize(n);
+  for (int64_t v = 0; v < n; ++v) {
+    const int32_t* f = table + v * TINV_TASK_FIELDS;
+    acc[v].clear();
+    if (f[F_NR] >= 1) acc[v].push_back({tile_key(f[F_R0L], f[F_R0R], f[F_R0C]), 0});
+    if (f[F_NR] >= 2) acc[v].push_back({tile_key(f[F_R1L], f[F_R1R], f[F_R1C]), 0});
+    acc[v].push_back({tile_key(f[F_OL], f[F_OR], f[F_OC]), f[F_OM] == 2 ? 2 : 1});
+  }
+}
+
+int expected_reads(int kind) {
+  switch (kind) {
+    case TINV_POTRF:
+    case TINV_TRTRI:
+    case TINV_LAUUM:
+      return 0;
+    case TINV_GEMM:
+      return 2;
+    default:
+      return 1;
+  }
+}
+
+int items_of(int kind, int R) {
+  switch (kind) {
+    case TINV_SYRK_SUB:
+    case TINV_SYRK_ADD_T:
+    case TINV_LAUUM:
+      return R * (R + 1) / 2;
+    case TINV_POTRF:
+    case TINV_TRTRI:
+    case KIND_INV:
+      return 1;
+    case TINV_COPY:
+      return R;
+    default:
+      return R * R;
+  }
+}
+
+double weight_of(int kind) {  // flops in units of b^3 (SURVEY.md §7 hard part 2)
+  switch (kind) {
+    case TINV_POTRF:
+    case TINV_TRTRI:
+    case TINV_LAUUM:
+    case KIND_INV:
+      return 1.0 / 3.0;
+    case TINV_GEMM:
+      return 2.0;
+    case TINV_COPY:
+      return 0.05;
+    default:
+      return 1.0;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ plans
+struct tinv_plan {
+  tinv_ctx* ctx = nullptr;
+  uint32_t flags = 0;
+  int64_t nref = 0, nexec = 0, items = 0, nedges = 0;
+  std::vector<TaskDev> tasks;
+  std::vector<int32_t> succ, indeg0, ref_kind, exec_ref;
+  int64_t nlogical = 0;
+  std::vector<int32_t> cur0, alt0;  // non-matrix logical tiles (matrix tiles filled at exec)
+  int64_t dyn_slots = 0;
+  int64_t q_off[NLEV + 1];
+  std::vector<unsigned long long> q_init;
+  std::vector<int32_t> tail0;
+  // device state
+  TaskDev* d_tasks = nullptr;
+  int32_t *d_succ = nullptr, *d_indeg = nullptr, *d_done = nullptr, *d_cur = nullptr, *d_alt = nullptr;
+  unsigned long long* d_queue = nullptr;
+  int32_t *d_head = nullptr, *d_tail = nullptr, *d_ctr = nullptr;  // ctr: remaining, abort
+  unsigned long long* d_err = nullptr;
+  unsigned* d_progress = nullptr;
+  unsigned long long *d_ts = nullptr, *d_te = nullptr;
+  int32_t* d_tsm = nullptr;
+  int32_t *d_snap_from = nullptr, *d_snap_to = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<unsigned long long> h_ts, h_te;
+  std::vector<int32_t> h_tsm;
+};
+
+extern "C" {
+
+int tinv_gen_stream(int32_t t, int32_t steps, const char* loops, int32_t out_of_place, int32_t pipelined,
+                    int32_t* table, int64_t cap, int64_t* ntasks, int64_t* barriers, int64_t capb, int64_t* nbar) {
+  if (t < 1 || steps < 1 || steps > 7 || !loops) return fail(nullptr, TINV_ERR_BAD_ARG, "bad gen_stream arguments");
+  const size_t nl = strlen(loops);
+  for (size_t x = 0; x < nl; ++x)
+    if (loops[x] != 'U' && loops[x] != 'D') return fail(nullptr, TINV_ERR_BAD_ARG, "loop order must be [UD]");
+  Gen g;
+  std::vector<int64_t> bars;
+  int nsteps = 0;
+  for (int s = 0; s < 3; ++s) nsteps += (steps >> s) & 1;
+  int which = 0;
+  for (int s = 0; s < 3; ++s) {
+    if (!((steps >> s) & 1)) continue;
+    const char d = nsteps > 1 ? loops[std::min<size_t>(s, nl - 1)] : loops[0];
+    if (which > 0 && !pipelined) bars.push_back((int64_t)g.tasks.size());
+    if (s == 0) g.step1(t, d);
+    if (s == 1) g.step2(t, d, out_of_place != 0);
+    if (s == 2) g.step3(t, d, out_of_place != 0);
+    ++which;
+  }
+  if (ntasks) *ntasks = (int64_t)g.tasks.size();
+  if (nbar) *nbar = (int64_t)bars.size();
+  if (table) {
+    if (cap < (int64_t)g.tasks.size()) return fail(nullptr, TINV_ERR_BAD_ARG, "table capacity too small");
+    memcpy(table, g.tasks.data(), g.tasks.size() * sizeof(Tk));
+  }
+  if (barriers) {
+    if (capb < (int64_t)bars.size()) return fail(nullptr, TINV_ERR_BAD_ARG, "barrier capacity too small");
+    for (size_t x = 0; x < bars.size(); ++x) barriers[x] = bars[x];
+  }
+  return TINV_OK;
+}
+
+int tinv_dag_edges(const int32_t* table, int64_t n, const int64_t* barriers, int64_t nbar, int32_t* src,
+                   int32_t* dst, int8_t* kind, int64_t cap, int64_t* nedges) {
+  if (!table && n > 0) return fail(nullptr, TINV_ERR_BAD_ARG, "null table");
+  std::vector<std::vector<Acc>> acc;
+  ref_accesses(table, n, acc);
+  std::vector<int64_t> bars(barriers, barriers + (barriers ? nbar : 0));
+  std::vector<Edge> edges;
+  scoreboard(n, acc, bars, edges);
+  if (nedges) *nedges = (int64_t)edges.size();
+  if (src) {
+    if (cap < (int64_t)edges.size()) return fail(nullptr, TINV_ERR_BAD_ARG, "edge capacity too small");
+    for (size_t x = 0; x < edges.size(); ++x) {
+      src[x] = edges[x].u;
+      dst[x] = edges[x].v;
+      kind[x] = edges[x].kind;
+    }
+  }
+  return TINV_OK;
+}
+
+int tinv_plan_destroy(tinv_plan* p) {
+  if (!p) return TINV_OK;
+  cudaSetDevice(p->ctx->device);
+  void* ptrs[] = {p->d_tasks, p->d_succ, p->d_indeg, p->d_done, p->d_cur,      p->d_alt,       p->d_queue, p->d_head,
+                  p->d_tail,  p->d_ctr,  p->d_err,   p->d_progress, p->d_ts, p->d_te, p->d_tsm, p->d_snap_from,
+                  p->d_snap_to};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  if (p->ev0) cudaEventDestroy(p->ev0);
+  if (p->ev1) cudaEventDestroy(p->ev1);
+  delete p;
+  return TINV_OK;
+}
+
+static void set_err(tinv_err* err, int32_t task, int32_t kind, int32_t code, int32_t index) {
+  if (!err) return;
+  err->task_id = task;
+  err->kind = kind;
+  err->code = code;
+  err->index = index;
+}
+
+int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, const int64_t* barriers,
+                     int64_t nbar, uint32_t flags, tinv_plan** out, tinv_err* err) {
+  set_err(err, -1, -1, TINV_OK, -1);
+  if (!c || !out || (!table && n > 0)) return fail(c, TINV_ERR_BAD_ARG, "bad plan arguments");
+  *out = nullptr;
+  // scheduler.py:274-276
+  if (stream_t != c->t) {
+    set_err(err, -1, -1, TINV_ERR_STREAM, -1);
+    return fail(c, TINV_ERR_STREAM, "stream generated for t=" + std::to_string(stream_t) +
+                                        " cannot run on a t=" + std::to_string(c->t) + " matrix");
+  }
+  const int R = (int)c->R, t = (int)c->t;
+  const int64_t T = c->T;
+  tinv_plan* p = new tinv_plan();
+  p->ctx = c;
+  p->flags = flags;
+  p->nref = n;
+  p->ref_kind.resize(n);
+
+  // ---- logical tiles, validation, INV insertion for TRSM (renamed inverse)
+  std::unordered_map<int64_t, int32_t> logical;  // key -> logical id (non-matrix tiles)
+  std::vector<char> written_dyn;                 // per non-matrix logical: written so far
+  int64_t next_logical = T;
+  auto get_logical = [&](int label, int r, int cc, bool is_read, int64_t task, int32_t& id) -> bool {
+    if (label == 0) {
+      if (r < 0 || r >= t || cc < 0 || cc > r) return false;
+      id = (int32_t)tri_index(r, cc);
+      return true;
+    }
+    if (label < 0 || r < 0 || r >= t || cc < 0 || cc >= t) return false;
+    const int64_t key = tile_key(label, r, cc);
+    auto it = logical.find(key);
+    if (it == logical.end()) {
+      if (is_read) return false;  // reference: store KeyError (never written)
+      id = (int32_t)next_logical++;
+      logical[key] = id;
+      written_dyn.push_back(0);
+    } else {
+      id = it->second;
+    }
+    (void)task;
+    return true;
+  };
+  std::vector<int32_t> last_writer_exec;  // per logical tile: exec index of last writer (-1 initial)
+  last_writer_exec.assign(T, -1);
+  std::unordered_map<int64_t, int32_t> inv_cache;  // (L logical << 32 | version+1) -> aux logical
+  struct XT {
+    int kind, step, out, in0, in1, mode, ref;
+  };
+  std::vector<XT> xs;
+  xs.reserve(n + n / 8 + 8);
+  std::vector<char> is_aux;
+  std::vector<int32_t> first_exec_of_ref(n + 1, 0);
+  for (int64_t v = 0; v < n; ++v) {
+    const int32_t* f = table + v * TINV_TASK_FIELDS;
+    const int kind = f[F_KIND];
+    p->ref_kind[v] = kind;
+    first_exec_of_ref[v] = (int32_t)xs.size();
+    auto bad = [&](const std::string& why) {
+      set_err(err, (int32_t)v, kind, TINV_ERR_STREAM, -1);
+      tinv_plan_destroy(p);
+      return fail(c, TINV_ERR_STREAM, "task " + std::to_string(v) + ": " + why);
+    };
+    if (kind < TINV_COPY || kind > TINV_LAUUM) return bad("unknown kernel kind");
+    if (kind == TINV_GEMM && (f[F_STEP] < 1 || f[F_STEP] > 3)) return bad("unsupported gemm shape");
+    const int nr = f[F_NR];
+    if (nr != expected_reads(kind)) return bad("wrong number of operands");
+    int32_t in0 = -1, in1 = -1, o = -1;
+    if (nr >= 1 && !get_logical(f[F_R0L], f[F_R0R], f[F_R0C], true, v, in0)) return bad("read of a missing tile");
+    if (nr >= 2 && !get_logical(f[F_R1L], f[F_R1R], f[F_R1C], true, v, in1)) return bad("read of a missing tile");
+    if (!get_logical(f[F_OL], f[F_OR], f[F_OC], false, v, o)) return bad("output tile outside the matrix");
+    if (kind != TINV_COPY && f[F_OL] != 0 && o >= T && !written_dyn[o - T]) return bad("kernel on an unwritten tile");
+    if ((int64_t)last_writer_exec.size() < next_logical) last_writer_exec.resize(next_logical, -1);
+    if (kind == TINV_TRSM) {
+      const int64_t key = ((int64_t)in0 << 32) | (int64_t)(last_writer_exec[in0] + 1);
+      auto it = inv_cache.find(key);
+      int32_t aux;
+      if (it == inv_cache.end()) {
+        aux = (int32_t)next_logical++;
+        written_dyn.push_back(1);
+        is_aux.resize(next_logical - T, 0);
+        is_aux[aux - T] = 1;
+        last_writer_exec.resize(next_logical, -1);
+        last_writer_exec[aux] = (int32_t)xs.size();
+        xs.push_back({KIND_INV, f[F_STEP], aux, in0, -1, 1, (int)v});
+        inv_cache[key] = aux;
+      } else {
+        aux = it->second;
+      }
+      in0 = aux;
+    }
+    if (o >= T) written_dyn[o - T] = 1;
+    last_writer_exec[o] = (int32_t)xs.size();
+    xs.push_back({kind, f[F_STEP], o, in0, in1, f[F_OM] == 2 ? 2 : 1, (int)v});
+  }
+  first_exec_of_ref[n] = (int32_t)xs.size();
+  p->nexec = (int64_t)xs.size();
+  p->nlogical = next_logical;
+  const int64_t nx = p->nexec;
+
+  // ---- hazard DAG over exec tasks (+ barrier edges at translated positions)
+  {
+    std::vector<std::vector<Acc>> acc(nx);
+    for (int64_t v = 0; v < nx; ++v) {
+      if (xs[v].in0 >= 0) acc[v].push_back({xs[v].in0, 0});
+      if (xs[v].in1 >= 0) acc[v].push_back({xs[v].in1, 0});
+      acc[v].push_back({xs[v].out, xs[v].mode});
+    }
+    std::vector<int64_t> bars;
+    for (int64_t x = 0; x < (barriers ? nbar : 0); ++x) {
+      const int64_t pos = barriers[x];
+      if (pos < 0 || pos > n) {
+        tinv_plan_destroy(p);
+        return fail(c, TINV_ERR_STREAM, "barrier position out of range");
+      }
+      bars.push_back(first_exec_of_ref[pos]);
+    }
+    std::vector<Edge> edges;
+    scoreboard(nx, acc, bars, edges);
+    if (flags & TINV_SERIAL)
+      for (int64_t v = 0; v + 1 < nx; ++v) edges.push_back({(int32_t)v, (int32_t)(v + 1), 3});
+    std::vector<std::vector<int32_t>> adj(nx);
+    for (const Edge& e : edges) adj[e.u].push_back(e.v);
+    p->indeg0.assign(nx, 0);
+    p->tasks.resize(nx);
+    int64_t ne = 0;
+    for (int64_t u = 0; u < nx; ++u) {
+      auto& a = adj[u];
+      std::sort(a.begin(), a.end());
+      a.erase(std::unique(a.begin(), a.end()), a.end());
+      p->tasks[u].succ_begin = (int32_t)p->succ.size();
+      for (int32_t v : a) {
+        p->succ.push_back(v);
+        p->indeg0[v]++;
+      }
+      p->tasks[u].succ_end = (int32_t)p->succ.size();
+      ne += (int64_t)a.size();
+    }
+    p->nedges = ne;
+  }
+
+  // ---- items, renaming, priorities (flop-weighted bottom level)
+  std::vector<double> bl(nx, 0.0);
+  double blmax = 0.0;
+  for (int64_t u = nx - 1; u >= 0; --u) {
+    double m = 0.0;
+    for (int32_t k = p->tasks[u].succ_begin; k < p->tasks[u].succ_end; ++k) m = std::max(m, bl[p->succ[k]]);
+    bl[u] = weight_of(xs[u].kind) + m;
+    blmax = std::max(blmax, bl[u]);
+  }
+  std::vector<char> renamed_tile(p->nlogical, 0);
+  std::vector<int64_t> lev_items(NLEV, 0);
+  p->exec_ref.resize(nx);
+  for (int64_t u = 0; u < nx; ++u) {
+    TaskDev& d = p->tasks[u];
+    const XT& x = xs[u];
+    d.kind = (int8_t)x.kind;
+    d.step = (int8_t)x.step;
+    d.out = x.out;
+    d.in0 = x.in0;
+    d.in1 = x.in1;
+    d.ref_id = x.ref;
+    d.nitems = items_of(x.kind, R);
+    d.flags = 0;
+    const bool alias = (x.in0 == x.out || x.in1 == x.out);
+    if (x.kind == TINV_TRMM_LEFT || x.kind == TINV_TRMM_RIGHT_NEG || x.kind == TINV_TRMM_LEFT_T ||
+        x.kind == TINV_LAUUM || x.kind == TINV_TRSM ||
+        (alias && (x.kind == TINV_GEMM || x.kind == TINV_SYRK_SUB || x.kind == TINV_SYRK_ADD_T))) {
+      d.flags |= TF_RENAMED;
+      renamed_tile[x.out] = 1;
+    }
+    int lev = blmax > 0 ? (int)std::floor(NLEV * (1.0 - bl[u] / blmax)) : 0;
+    lev = std::min(NLEV - 1, std::max(0, lev));
+    d.level = (int8_t)lev;
+    lev_items[lev] += d.nitems;
+    p->items += d.nitems;
+    p->exec_ref[u] = x.ref;
+  }
+  p->q_off[0] = 0;
+  for (int l = 0; l < NLEV; ++l) p->q_off[l + 1] = p->q_off[l] + lev_items[l];
+  p->tail0.assign(NLEV, 0);
+  p->q_init.assign(p->q_off[NLEV], 0ull);
+  for (int64_t u = 0; u < nx; ++u)
+    if (p->indeg0[u] == 0) {
+      const TaskDev& d = p->tasks[u];
+      for (int i = 0; i < d.nitems; ++i)
+        p->q_init[p->q_off[d.level] + p->tail0[d.level]++] = ((unsigned long long)(u + 1) << 32) | (unsigned)i;
+    }
+
+  // ---- slots of the non-matrix logical tiles: [2T, 2T + dyn)
+  p->cur0.assign(p->nlogical, -1);
+  p->alt0.assign(p->nlogical, -1);
+  int64_t next_slot = 2 * T;
+  for (int64_t l = T; l < p->nlogical; ++l) {
+    p->cur0[l] = (int32_t)next_slot++;
+    p->alt0[l] = renamed_tile[l] ? (int32_t)next_slot++ : p->cur0[l];
+  }
+  p->dyn_slots = next_slot - 2 * T;
+
+  // ---- device buffers
+  auto ckm = [&](void** ptr, size_t bytes) { return cudaMalloc(ptr, std::max<size_t>(bytes, 16)); };
+  if (cudaSetDevice(c->device) != cudaSuccess || ckm((void**)&p->d_tasks, nx * sizeof(TaskDev)) ||
+      ckm((void**)&p->d_succ, p->succ.size() * 4) || ckm((void**)&p->d_indeg, nx * 4) ||
+      ckm((void**)&p->d_done, nx * 4) || ckm((void**)&p->d_cur, p->nlogical * 4) ||
+      ckm((void**)&p->d_alt, p->nlogical * 4) || ckm((void**)&p->d_queue, p->q_off[NLEV] * 8) ||
+      ckm((void**)&p->d_head, NLEV * 4) || ckm((void**)&p->d_tail, NLEV * 4) || ckm((void**)&p->d_ctr, 2 * 4) ||
+      ckm((void**)&p->d_err, 8) || ckm((void**)&p->d_progress, 4) || cudaEventCreate(&p->ev0) ||
+      cudaEventCreate(&p->ev1)) {
+    tinv_plan_destroy(p);
+    cudaGetLastError();
+    return fail(c, TINV_ERR_CUDA, "plan allocation failed");
+  }
+  if (flags & TINV_TRACE) {
+    if (ckm((void**)&p->d_ts, nx * 8) || ckm((void**)&p->d_te, nx * 8) || ckm((void**)&p->d_tsm, nx * 4)) {
+      tinv_plan_destroy(p);
+      return fail(c, TINV_ERR_CUDA, "trace allocation failed");
+    }
+  }
+  if (flags & TINV_KEEP_ON_FAILURE) {
+    if (ckm((void**)&p->d_snap_from, T * 4) || ckm((void**)&p->d_snap_to, T * 4)) {
+      tinv_plan_destroy(p);
+      return fail(c, TINV_ERR_CUDA, "snapshot allocation failed");
+    }
+  }
+  cudaMemcpy(p->d_tasks, p->tasks.data(), nx * sizeof(TaskDev), cudaMemcpyHostToDevice);
+  if (!p->succ.empty()) cudaMemcpy(p->d_succ, p->succ.data(), p->succ.size() * 4, cudaMemcpyHostToDevice);
+  if (cudaGetLastError() != cudaSuccess) {
+    tinv_plan_destroy(p);
+    return fail(c, TINV_ERR_CUDA, "plan upload failed");
+  }
+  *out = p;
+  return TINV_OK;
+}
+
+int tinv_plan_stats(const tinv_plan* p, int64_t* exec_tasks, int64_t* items, int64_t* edges) {
+  if (!p) return TINV_ERR_BAD_ARG;
+  if (exec_tasks) *exec_tasks = p->nexec;
+  if (items) *items = p->items;
+  if (edges) *edges = p->nedges;
+  return TINV_OK;
+}
+
+int tinv_plan_exec(tinv_plan* p, tinv_err* err, double* ms) {
+  set_err(err, -1, -1, TINV_OK, -1);
+  if (!p) return TINV_ERR_BAD_ARG;
+  tinv_ctx* c = p->ctx;
+  const int64_t T = c->T, nx = p->nexec;
+  CK(c, cudaSetDevice(c->device));
+  const int64_t scratch_base = 2 * T + p->dyn_slots;
+  const bool keep = (p->flags & TINV_KEEP_ON_FAILURE) != 0;
+  const int64_t backup_base = scratch_base + c->nsm;
+  int rc = ensure_pool(c, backup_base + (keep ? T : 0));
+  if (rc) return rc;
+  if (nx == 0) {
+    if (ms) *ms = 0.0;
+    return TINV_OK;
+  }
+  cudaStream_t st = c->st;
+  // reset the mutable executor state
+  for (int64_t k = 0; k < T; ++k) {
+    p->cur0[k] = c->a_slot[k];
+    p->alt0[k] = (int32_t)(c->a_slot[k] < T ? k + T : k);
+  }
+  CK(c, cudaMemcpyAsync(p->d_indeg, p->indeg0.data(), nx * 4, cudaMemcpyHostToDevice, st));
+  CK(c, cudaMemsetAsync(p->d_done, 0, nx * 4, st));
+  CK(c, cudaMemcpyAsync(p->d_cur, p->cur0.data(), p->nlogical * 4, cudaMemcpyHostToDevice, st));
+  CK(c, cudaMemcpyAsync(p->d_alt, p->alt0.data(), p->nlogical * 4, cudaMemcpyHostToDevice, st));
+  CK(c, cudaMemcpyAsync(p->d_queue, p->q_init.data(), p->q_off[NLEV] * 8, cudaMemcpyHostToDevice, st));
+  CK(c, cudaMemsetAsync(p->d_head, 0, NLEV * 4, st));
+  CK(c, cudaMemcpyAsync(p->d_tail, p->tail0.data(), NLEV * 4, cudaMemcpyHostToDevice, st));
+  const int32_t ctr[2] = {(int32_t)nx, 0};
+  CK(c, cudaMemcpyAsync(p->d_ctr, ctr, 8, cudaMemcpyHostToDevice, st));
+  CK(c, cudaMemsetAsync(p->d_err, 0xff, 8, st));
+  CK(c, cudaMemsetAsync(p->d_progress, 0, 4, st));
+  if (p->d_ts) {
+    CK(c, cudaMemsetAsync(p->d_ts, 0xff, nx * 8, st));
+    CK(c, cudaMemsetAsync(p->d_te, 0, nx * 8, st));
+    CK(c, cudaMemsetAsync(p->d_tsm, 0xff, nx * 4, st));
+  }
+  std::vector<int32_t> from(T), to(T);
+  if (keep) {
+    for (int64_t k = 0; k < T; ++k) {
+      from[k] = c->a_slot[k];
+      to[k] = (int32_t)(backup_base + k);
+    }
+    CK(c, cudaMemcpyAsync(p->d_snap_from, from.data(), T * 4, cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(p->d_snap_to, to.data(), T * 4, cudaMemcpyHostToDevice, st));
+    CK(c, launch_copy_slots(c->pool, c->slot_elems, p->d_snap_from, p->d_snap_to, T, st));
+  }
+  ExecParams P;
+  memset(&P, 0, sizeof(P));
+  P.pool = c->pool;
+  P.slot_elems = c->slot_elems;
+  P.bp = (int32_t)c->bp;
+  P.R = (int32_t)c->R;
+  P.ntasks = (int32_t)nx;
+  P.scratch_base = (int32_t)scratch_base;
+  P.tasks = p->d_tasks;
+  P.succ = p->d_succ;
+  P.indeg = p->d_indeg;
+  P.done = p->d_done;
+  P.cur_slot = p->d_cur;
+  P.alt_slot = p->d_alt;
+  P.queue = p->d_queue;
+  for (int l = 0; l <= NLEV; ++l) P.q_off[l] = p->q_off[l];
+  P.q_head = p->d_head;
+  P.q_tail = p->d_tail;
+  P.remaining = p->d_ctr;
+  P.abort_flag = p->d_ctr + 1;
+  P.err = p->d_err;
+  P.progress = p->d_progress;
+  P.trace_start = p->d_ts;
+  P.trace_end = p->d_te;
+  P.trace_sm = p->d_tsm;
+  P.t0 = 0;
+  CK(c, cudaEventRecord(p->ev0, st));
+  CK(c, launch_exec(c->tmK, c->tmM, P, (int)c->b, c->nsm, st));
+  CK(c, cudaEventRecord(p->ev1, st));
+  CK(c, cudaStreamSynchronize(st));
+  if (ms) {
+    float f = 0.f;
+    cudaEventElapsedTime(&f, p->ev0, p->ev1);
+    *ms = f;
+  }
+  unsigned long long ekey = 0;
+  int32_t ctr_out[2];
+  CK(c, cudaMemcpy(&ekey, p->d_err, 8, cudaMemcpyDeviceToHost));
+  CK(c, cudaMemcpy(ctr_out, p->d_ctr, 8, cudaMemcpyDeviceToHost));
+  if (p->d_ts) {
+    p->h_ts.resize(nx);
+    p->h_te.resize(nx);
+    p->h_tsm.resize(nx);
+    CK(c, cudaMemcpy(p->h_ts.data(), p->d_ts, nx * 8, cudaMemcpyDeviceToHost));
+    CK(c, cudaMemcpy(p->h_te.data(), p->d_te, nx * 8, cudaMemcpyDeviceToHost));
+    CK(c, cudaMemcpy(p->h_tsm.data(), p->d_tsm, nx * 4, cudaMemcpyDeviceToHost));
+  }
+  if (ekey != ~0ull || ctr_out[0] != 0) {
+    if (keep) {
+      CK(c, cudaMemcpyAsync(p->d_snap_from, to.data(), T * 4, cudaMemcpyHostToDevice, st));
+      CK(c, cudaMemcpyAsync(p->d_snap_to, from.data(), T * 4, cudaMemcpyHostToDevice, st));
+      CK(c, launch_copy_slots(c->pool, c->slot_elems, p->d_snap_from, p->d_snap_to, T, st));
+      CK(c, cudaStreamSynchronize(st));
+    }
+    if (ekey == ~0ull) {
+      set_err(err, -1, -1, TINV_ERR_INTERNAL, -1);
+      return fail(c, TINV_ERR_INTERNAL, "executor finished with " + std::to_string(ctr_out[0]) + " tasks pending");
+    }
+    const int32_t task = (int32_t)(ekey >> 32);
+    const int32_t code = (int32_t)((ekey >> 24) & 0xff);
+    const int32_t index = (int32_t)(ekey & 0xffffff);
+    if (code == TINV_ERR_INTERNAL) {
+      set_err(err, -1, -1, code, -1);
+      return fail(c, code, "executor watchdog: no progress");
+    }
+    set_err(err, task, task >= 0 && task < p->nref ? p->ref_kind[task] : -1, code, index);
+    return fail(c, code, "task " + std::to_string(task) + " failed");
+  }
+  // success: adopt the renamed slots of the matrix tiles
+  CK(c, cudaMemcpy(c->a_slot.data(), p->d_cur, T * 4, cudaMemcpyDeviceToHost));
+  return TINV_OK;
+}
+
+int tinv_plan_trace(const tinv_plan* p, int64_t* start_ns, int64_t* end_ns, int32_t* sm, int64_t ntasks) {
+  if (!p || ntasks < p->nref || p->h_ts.empty()) return TINV_ERR_BAD_ARG;
+  unsigned long long base = ~0ull;
+  for (int64_t u = 0; u < p->nexec; ++u) base = std::min(base, p->h_ts[u]);
+  for (int64_t r = 0; r < p->nref; ++r) {
+    start_ns[r] = -1;
+    end_ns[r] = -1;
+    sm[r] = -1;
+  }
+  for (int64_t u = 0; u < p->nexec; ++u) {
+    const int32_t r = p->exec_ref[u];
+    const int64_t s = (int64_t)(p->h_ts[u] - base), e = (int64_t)(p->h_te[u] - base);
+    if (start_ns[r] < 0 || s < start_ns[r]) start_ns[r] = s;
+    if (e > end_ns[r]) {
+      end_ns[r] = e;
+      sm[r] = p->h_tsm[u];
+    }
+  }
+  return TINV_OK;
+}
+
+int tinv_run(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, const int64_t* barriers, int64_t nbar,
+             uint32_t flags, tinv_err* err) {
+  tinv_plan* p = nullptr;
+  int rc = tinv_plan_create(c, table, n, stream_t, barriers, nbar, flags, &p, err);
+  if (rc) return rc;
+  rc = tinv_plan_exec(p, err, nullptr);
+  tinv_plan_destroy(p);
+  return rc;
+}
+
+}  // extern "C"

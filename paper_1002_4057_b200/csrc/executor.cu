@@ -1,0 +1,947 @@
+// Persistent on-device task executor for the SPD tile inversion
+// (B200 / sm_100a). Replaces the reference's threaded dynamic scheduler
+// (scheduler.py:261-351) and its numpy tile kernels (kernels.py:59-151).
+//
+// One CTA per SM, 288 threads:
+//   warps 0-7  "consumers": FP64 DMMA (mma.sync m8n8k4 -> SASS DMMA.8x8x4)
+//              on 128x128 output blocks, epilogues, diagonal-block phases,
+//              and task completion (successor release) for the scheduler;
+//   warp 8     "producer": pops ready work items from the device queues,
+//              expands each into jobs and streams their operand chunks into a
+//              4-stage shared-memory ring with TMA (cp.async.bulk.tensor,
+//              128B swizzle) on mbarriers, running ahead across items.
+// A task of kind K over tiles of order bp = R*128 is split into work items
+// (128x128 output blocks) which run on any CTA; the last item to finish
+// releases the task's successors in the hazard DAG (RAW/WAR/WAW edges built
+// by the host planner from the stream exactly as scheduler.py:101-153).
+// In-place kernels whose output block depends on other blocks of the same
+// tile (TRMM*, LAUUM, TRSM) are array-renamed at the tile level: they read
+// the current slot and write the alternate one, swapped at completion.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tinv_internal.h"
+
+namespace tinv {
+
+// ---------------------------------------------------------------- PTX glue
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void tma_load3(const CUtensorMap* map, void* dst, uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch3(const CUtensorMap* map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void cons_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int ld_relaxed_s32(const int32_t* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_cta_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned s;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(s));
+  return s;
+}
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double2 lds128(const char* p) { return *reinterpret_cast<const double2*>(p); }
+// permutation of the 8 rows of an MMA fragment so that 128-bit fragment
+// loads from 128B-swizzled TMA tiles are bank-conflict free per quarter warp
+__device__ __forceinline__ int rho(int x) { return (x >> 1) | ((x & 1) << 2); }
+
+// ---------------------------------------------------------------- jobs
+enum Variant : int8_t { V_NT = 0, V_NN = 1, V_TN = 2 };
+enum JobType : int8_t { J_GEMM = 0, J_SPECIAL = 1 };
+enum Special : int8_t { SP_POTRF_DIAG = 0, SP_TRTRI_DIAG = 1, SP_INV_INIT = 2, SP_COPY_ROWS = 3 };
+
+struct ItemInfo {
+  int32_t task, item, kind, step;
+  int32_t out_s, alt_s, in0_s, in1_s, scr_s;
+  int32_t ref_id, nitems, njobs, flags, pad;
+};
+
+struct Job {
+  int8_t type, variant, special, mirror, dep, sign;
+  int16_t d;     // special parameter
+  int32_t a_s, a_fix, a_k0, b_s, b_fix, b_k0;
+  int32_t k0, k1, a_mask, b_mask;
+  int32_t o_s, o_r, o_c, c_s;
+};
+
+__device__ __forceinline__ void lower_pair(int i, int& r, int& c) {
+  r = 0;
+  while ((r + 1) * (r + 2) / 2 <= i) ++r;
+  c = i - r * (r + 1) / 2;
+}
+
+__device__ __forceinline__ int item_count(int kind, int R) {
+  switch (kind) {
+    case TINV_SYRK_SUB:
+    case TINV_SYRK_ADD_T:
+    case TINV_LAUUM:
+      return R * (R + 1) / 2;
+    case TINV_POTRF:
+    case TINV_TRTRI:
+    case KIND_INV:
+      return 1;
+    case TINV_COPY:
+      return R;
+    default:
+      return R * R;
+  }
+}
+
+__device__ __forceinline__ int job_count(const ItemInfo& it, int R) {
+  switch (it.kind) {
+    case TINV_POTRF: {
+      int n = R;
+      for (int d = 0; d < R; ++d) n += (R - 1 - d) + (R - 1 - d) * (R - d) / 2;
+      return n;
+    }
+    case TINV_TRTRI:
+      return R + R * (R - 1);
+    case KIND_INV:
+      return 1 + R + R * (R - 1);
+    default:
+      return 1;
+  }
+}
+
+__device__ __forceinline__ void gemm_job(Job& j, int8_t v, int a_s, int a_fix, int a_k0, int b_s, int b_fix,
+                                         int b_k0, int k0, int k1, int o_s, int o_r, int o_c, int c_s,
+                                         int sign) {
+  j.type = J_GEMM;
+  j.variant = v;
+  j.special = 0;
+  j.mirror = 0;
+  j.dep = 0;
+  j.sign = (int8_t)sign;
+  j.d = 0;
+  j.a_s = a_s;
+  j.a_fix = a_fix;
+  j.a_k0 = a_k0;
+  j.b_s = b_s;
+  j.b_fix = b_fix;
+  j.b_k0 = b_k0;
+  j.k0 = k0;
+  j.k1 = k1;
+  j.a_mask = -1;
+  j.b_mask = -1;
+  j.o_s = o_s;
+  j.o_r = o_r;
+  j.o_c = o_c;
+  j.c_s = c_s;
+}
+
+__device__ __forceinline__ void special_job(Job& j, int8_t sp, int d) {
+  j.type = J_SPECIAL;
+  j.special = sp;
+  j.d = (int16_t)d;
+  j.dep = 1;
+}
+
+// TRTRI job list (in place on slot s), shared by TRTRI and INV (offset by 1).
+//   for d = R-1 .. 0:  [diag inverse of block d]
+//     rows r = R-1 .. d+1:  A[r][d] <- sum_{k=d+1..r} X[r][k] L[k][d]
+//     rows r = R-1 .. d+1:  A[r][d] <- -A[r][d] X[d][d]
+__device__ __forceinline__ void trtri_job(int n, int s, int R, Job& j) {
+  for (int d = R - 1; d >= 0; --d) {
+    if (n == 0) {
+      special_job(j, SP_TRTRI_DIAG, d);
+      return;
+    }
+    n -= 1;
+    const int m = R - 1 - d;
+    if (n < m) {
+      const int r = R - 1 - n;
+      gemm_job(j, V_NN, s, r, d + 1, s, d, d + 1, d + 1, r + 1, s, r, d, -1, 1);
+      j.a_mask = r;
+      return;
+    }
+    n -= m;
+    if (n < m) {
+      const int r = R - 1 - n;
+      gemm_job(j, V_NN, s, r, d, s, d, d, d, d + 1, s, r, d, -1, -1);
+      j.b_mask = d;
+      j.dep = (n == 0);
+      return;
+    }
+    n -= m;
+  }
+}
+
+__device__ void get_job(const ItemInfo& it, int n, int R, Job& j) {
+  const int o = it.out_s, a = it.alt_s, x = it.in0_s, y = it.in1_s;
+  const int kind = it.kind;
+  if (kind == TINV_POTRF) {
+    for (int d = 0; d < R; ++d) {
+      if (n == 0) {
+        special_job(j, SP_POTRF_DIAG, d);
+        return;
+      }
+      n -= 1;
+      const int m = R - 1 - d;
+      if (n < m) {  // panel solve A[r][d] <- A[r][d] inv(L_dd)^T
+        const int r = d + 1 + n;
+        gemm_job(j, V_NT, o, r, d, it.scr_s, 0, 0, d, d + 1, o, r, d, -1, 1);
+        j.b_mask = d;
+        return;
+      }
+      n -= m;
+      const int u = m * (m + 1) / 2;
+      if (n < u) {  // trailing update A[r][c] -= A[r][d] A[c][d]^T, r >= c > d
+        int rr, cc;
+        lower_pair(n, rr, cc);
+        const int r = d + 1 + rr, c = d + 1 + cc;
+        gemm_job(j, V_NT, o, r, d, o, c, d, d, d + 1, o, r, c, o, -1);
+        j.dep = (n == 0);
+        return;
+      }
+      n -= u;
+    }
+    return;
+  }
+  if (kind == TINV_TRTRI) {
+    trtri_job(n, o, R, j);
+    return;
+  }
+  if (kind == KIND_INV) {
+    if (n == 0) {
+      special_job(j, SP_INV_INIT, 0);
+      return;
+    }
+    trtri_job(n - 1, o, R, j);
+    return;
+  }
+  if (kind == TINV_COPY) {
+    special_job(j, SP_COPY_ROWS, it.item);
+    return;
+  }
+  int r, c;
+  if (kind == TINV_SYRK_SUB || kind == TINV_SYRK_ADD_T || kind == TINV_LAUUM) {
+    lower_pair(it.item, r, c);
+  } else if (kind == TINV_TRSM) {  // longest items (largest c) first
+    c = R - 1 - it.item / R;
+    r = it.item % R;
+  } else {
+    r = it.item / R;
+    c = it.item % R;
+  }
+  // accumulate kernels write in place unless an operand aliases the output
+  const int w = (it.flags & TF_RENAMED) ? a : o;
+  switch (kind) {
+    case TINV_GEMM:
+      if (it.step == TINV_STEP_CHOLESKY)
+        gemm_job(j, V_NT, x, r, 0, y, c, 0, 0, R, w, r, c, o, -1);
+      else if (it.step == TINV_STEP_TRINV)
+        gemm_job(j, V_NN, x, r, 0, y, c, 0, 0, R, w, r, c, o, 1);
+      else
+        gemm_job(j, V_TN, x, r, 0, y, c, 0, 0, R, w, r, c, o, 1);
+      return;
+    case TINV_SYRK_SUB:
+      gemm_job(j, V_NT, x, r, 0, x, c, 0, 0, R, w, r, c, o, -1);
+      j.mirror = 1;
+      return;
+    case TINV_SYRK_ADD_T:
+      gemm_job(j, V_TN, x, r, 0, x, c, 0, 0, R, w, r, c, o, 1);
+      j.mirror = 1;
+      return;
+    case TINV_TRMM_LEFT:  // tril(T) A : sum_{s<=r} T[r][s] A[s][c]
+      gemm_job(j, V_NN, x, r, 0, o, c, 0, 0, r + 1, a, r, c, -1, 1);
+      j.a_mask = r;
+      return;
+    case TINV_TRMM_RIGHT_NEG:  // -A tril(T) : -sum_{s>=c} A[r][s] T[s][c]
+      gemm_job(j, V_NN, o, r, c, x, c, c, c, R, a, r, c, -1, -1);
+      j.b_mask = c;
+      return;
+    case TINV_TRMM_LEFT_T:  // tril(T)^T A : sum_{s>=r} T[s][r]^T A[s][c]
+      gemm_job(j, V_TN, x, r, r, o, c, r, r, R, a, r, c, -1, 1);
+      j.a_mask = r;
+      return;
+    case TINV_LAUUM:  // tril(L)^T tril(L) : sum_{s>=r} L[s][r]^T L[s][c]
+      gemm_job(j, V_TN, o, r, r, o, c, r, r, R, a, r, c, -1, 1);
+      j.a_mask = r;
+      j.b_mask = c;
+      j.mirror = 1;
+      return;
+    case TINV_TRSM:  // X = A tril(L)^-T = sum_{s<=c} A[r][s] Linv[c][s]
+      gemm_job(j, V_NT, o, r, 0, x, c, 0, 0, c + 1, a, r, c, -1, 1);
+      j.b_mask = c;
+      return;
+    default:
+      return;
+  }
+}
+
+// ---------------------------------------------------------------- smem
+struct SmemCtl {
+  uint64_t full[NSTAGE];
+  uint64_t empty[NSTAGE];
+  uint64_t item_full[2];
+  uint64_t item_empty[2];
+  ItemInfo items[2];
+  unsigned jobs_done;
+  int fail_code;   // per item: 0 none
+  int fail_index;
+  int scan_min;
+  double pivot;
+};
+
+// ---------------------------------------------------------------- consumers: DMMA chunk
+// Warp w: rows [64*(w&1), +64), cols [32*(w>>1), +32) of the 128x128 block.
+// A/B stage layouts: K-major = TMA box {16 k, 128 rows}; MN-major = 8 boxes
+// {16 cols, 16 k-rows} at 2 KB each; both 128B-swizzled (16B chunk c of row r
+// stored at c ^ (r & 7)).
+template <int V, bool MA, bool MB>
+__device__ __forceinline__ void chunk_mma(const char* sA, const char* sB, double (&acc)[8][4][2], int wm, int wn,
+                                          int g, int tg, int kb16) {
+  const int rg = rho(g);
+  if constexpr (V == V_NT || V == V_NN) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double2 a[8];
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const int row = 64 * wm + 8 * p + rg;
+        a[p] = lds128(sA + row * 128 + (((tg + 4 * h) ^ rg) << 4));
+        if constexpr (MA) {  // keep A(m,k) iff k <= m
+          const int k = kb16 + 2 * (tg + 4 * h);
+          if (k > row) a[p].x = 0.0;
+          if (k + 1 > row) a[p].y = 0.0;
+        }
+      }
+      if constexpr (V == V_NT) {
+        double2 b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int n = 32 * wn + 8 * q + rg;
+          b[q] = lds128(sB + n * 128 + (((tg + 4 * h) ^ rg) << 4));
+          if constexpr (MB) {  // keep B(k,n) iff k <= n  (stored [n][k] lower)
+            const int k = kb16 + 2 * (tg + 4 * h);
+            if (k > n) b[q].x = 0.0;
+            if (k + 1 > n) b[q].y = 0.0;
+          }
+        }
+#pragma unroll
+        for (int p = 0; p < 8; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dmma(acc[p][q], a[p].x, b[q].x);
+#pragma unroll
+        for (int p = 0; p < 8; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dmma(acc[p][q], a[p].y, b[q].y);
+      } else {  // NN: B stored [k][n], pairs of n per lane (sigma = identity)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int k = 2 * tg + 8 * h + e;
+          double2 b[2];
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            b[v] = lds128(sB + (2 * wn + v) * 2048 + k * 128 + ((g ^ (k & 7)) << 4));
+            if constexpr (MB) {  // keep B(k,n) iff n <= k (stored [k][n] lower)
+              const int n0 = 32 * wn + 16 * v + 2 * g;
+              if (n0 > kb16 + k) b[v].x = 0.0;
+              if (n0 + 1 > kb16 + k) b[v].y = 0.0;
+            }
+          }
+#pragma unroll
+          for (int p = 0; p < 8; ++p) {
+            const double av = e ? a[p].y : a[p].x;
+            dmma(acc[p][0], av, b[0].x);
+            dmma(acc[p][1], av, b[0].y);
+            dmma(acc[p][2], av, b[1].x);
+            dmma(acc[p][3], av, b[1].y);
+          }
+        }
+      }
+    }
+  } else {  // TN: A stored [k][m], B stored [k][n], sigma = rho for both
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int k = 4 * s + tg;
+      const int sw = (rg ^ (k & 7)) << 4;
+      double2 a[4], b[2];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        a[w] = lds128(sA + (4 * wm + w) * 2048 + k * 128 + sw);
+        if constexpr (MA) {  // keep A(m,k) iff m <= k (stored [k][m] lower)
+          const int m0 = 64 * wm + 16 * w + 2 * rg;
+          if (m0 > kb16 + k) a[w].x = 0.0;
+          if (m0 + 1 > kb16 + k) a[w].y = 0.0;
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        b[v] = lds128(sB + (2 * wn + v) * 2048 + k * 128 + sw);
+        if constexpr (MB) {
+          const int n0 = 32 * wn + 16 * v + 2 * rg;
+          if (n0 > kb16 + k) b[v].x = 0.0;
+          if (n0 + 1 > kb16 + k) b[v].y = 0.0;
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const double av = (p & 1) ? a[p >> 1].y : a[p >> 1].x;
+        dmma(acc[p][0], av, b[0].x);
+        dmma(acc[p][1], av, b[0].y);
+        dmma(acc[p][2], av, b[1].x);
+        dmma(acc[p][3], av, b[1].y);
+      }
+    }
+  }
+}
+
+template <int V>
+__device__ __forceinline__ int out_row(int wm, int p, int g) {
+  if constexpr (V == V_TN) return 64 * wm + 16 * (p >> 1) + 2 * rho(g) + (p & 1);
+  return 64 * wm + 8 * p + rho(g);
+}
+template <int V>
+__device__ __forceinline__ int out_col(int wn, int q, int j) {
+  if constexpr (V == V_NT) return 32 * wn + 8 * q + rho(j);
+  if constexpr (V == V_NN) return 32 * wn + 16 * (q >> 1) + 2 * j + (q & 1);
+  return 32 * wn + 16 * (q >> 1) + 2 * rho(j) + (q & 1);
+}
+
+template <int V>
+__device__ __forceinline__ void run_gemm(const Job& jb, const ExecParams& P, SmemCtl& ctl, char* ring, unsigned& ks) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp & 1, wn = warp >> 1, g = lane >> 2, tg = lane & 3;
+  double acc[8][4][2];
+#pragma unroll
+  for (int p = 0; p < 8; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[p][q][0] = acc[p][q][1] = 0.0;
+
+  for (int kb = jb.k0; kb < jb.k1; ++kb) {
+    const bool ma = (kb == jb.a_mask), mb = (kb == jb.b_mask);
+    for (int ch = 0; ch < BLK / KCH; ++ch, ++ks) {
+      const int st = ks % NSTAGE;
+      mbar_wait(&ctl.full[st], (ks / NSTAGE) & 1);
+      const char* sA = ring + st * STAGE_BYTES;
+      const char* sB = sA + STAGE_BYTES / 2;
+      const int kb16 = ch * KCH;
+      if (!ma && !mb)
+        chunk_mma<V, false, false>(sA, sB, acc, wm, wn, g, tg, kb16);
+      else if (ma && !mb)
+        chunk_mma<V, true, false>(sA, sB, acc, wm, wn, g, tg, kb16);
+      else if (!ma && mb)
+        chunk_mma<V, false, true>(sA, sB, acc, wm, wn, g, tg, kb16);
+      else
+        chunk_mma<V, true, true>(sA, sB, acc, wm, wn, g, tg, kb16);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctl.empty[st]);
+    }
+  }
+
+  // epilogue: out = [C +] sign * acc ; mirror -> also the transposed block
+  const int64_t bp = P.bp;
+  double* O = P.pool + (int64_t)jb.o_s * P.slot_elems + (int64_t)jb.o_r * BLK * bp + jb.o_c * BLK;
+  double* OT = P.pool + (int64_t)jb.o_s * P.slot_elems + (int64_t)jb.o_c * BLK * bp + jb.o_r * BLK;
+  const double* C =
+      jb.c_s >= 0 ? P.pool + (int64_t)jb.c_s * P.slot_elems + (int64_t)jb.o_r * BLK * bp + jb.o_c * BLK : nullptr;
+  const bool diag = jb.o_r == jb.o_c;
+  const double sg = (double)jb.sign;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int r = out_row<V>(wm, p, g);
+    double cv[4][2];
+    if (C) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = out_col<V>(wn, q, 2 * tg + e);
+          cv[q][e] = (jb.mirror && diag && c > r) ? 0.0 : __ldcg(C + r * bp + c);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = out_col<V>(wn, q, 2 * tg + e);
+        if (jb.mirror && diag && c > r) continue;
+        double v = sg * acc[p][q][e];
+        if (C) v = cv[q][e] + v;
+        O[r * bp + c] = v;
+        if (jb.mirror && !(diag && c == r)) OT[c * bp + r] = v;
+      }
+  }
+}
+
+// ---------------------------------------------------------------- consumers: diagonal phases
+// 128x128 block in shared memory, row stride 129 doubles (bank spread).
+constexpr int SLD = BLK + 1;
+
+__device__ void load_block_lower(double* S, const double* src, int64_t bp) {
+  for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
+    const int i = e >> 7, j = e & 127;
+    S[i * SLD + j] = (j <= i) ? __ldcg(src + i * bp + j) : 0.0;
+  }
+}
+__device__ void store_block_lower(const double* S, double* dst, int64_t bp) {
+  for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
+    const int i = e >> 7, j = e & 127;
+    dst[i * bp + j] = (j <= i) ? S[i * SLD + j] : 0.0;
+  }
+}
+__device__ void zero_upper_blocks(double* tile, int R, int64_t bp) {
+  for (int r = 0; r < R; ++r)
+    for (int c = r + 1; c < R; ++c) {
+      double* blk = tile + (int64_t)r * BLK * bp + c * BLK;
+      for (int e = threadIdx.x; e < BLK * BLK / 2; e += 256) {
+        const int i = e >> 6, j = (e & 63) * 2;
+        *reinterpret_cast<double2*>(blk + i * bp + j) = make_double2(0.0, 0.0);
+      }
+    }
+}
+
+// unblocked right-looking Cholesky of the lower 128x128 block in S;
+// returns -1 or the first failing pivot (kernels.py:68-71 semantics)
+__device__ int small_potrf(double* S, SmemCtl& ctl) {
+  const int tid = threadIdx.x;
+  for (int k = 0; k < BLK; ++k) {
+    if (tid == 0) {
+      const double d = S[k * SLD + k];
+      if (!(d > 0.0) || !isfinite(d)) {
+        ctl.scan_min = k;
+      } else {
+        S[k * SLD + k] = sqrt(d);
+      }
+    }
+    cons_bar();
+    if (ctl.scan_min >= 0) return ctl.scan_min;
+    const double dk = S[k * SLD + k];
+    for (int i = k + 1 + tid; i < BLK; i += 256) S[i * SLD + k] = S[i * SLD + k] / dk;
+    cons_bar();
+    const int m = BLK - 1 - k;
+    for (int e = tid; e < m * m; e += 256) {
+      const int i = k + 1 + e / m, j = k + 1 + e % m;
+      if (j <= i) S[i * SLD + j] -= S[i * SLD + k] * S[j * SLD + k];
+    }
+    cons_bar();
+  }
+  return -1;
+}
+
+// in-place inverse of the lower-triangular 128x128 block in S (LAPACK trti2
+// order: columns right to left, X[i][j] = -X[j][j] sum_{k=j+1..i} X[i][k] L[k][j])
+__device__ void small_trtri(double* S) {
+  const int tid = threadIdx.x;
+  for (int j = BLK - 1; j >= 0; --j) {
+    if (tid == 0) S[j * SLD + j] = 1.0 / S[j * SLD + j];
+    cons_bar();
+    const double ajj = S[j * SLD + j];
+    const int row = j + 1 + (tid >> 1);
+    double part = 0.0;
+    if (row < BLK) {
+      for (int k = j + 1 + (tid & 1); k <= row; k += 2) part += S[row * SLD + k] * S[k * SLD + j];
+    }
+    part += __shfl_xor_sync(0xffffffffu, part, 1);
+    cons_bar();
+    if (row < BLK && (tid & 1) == 0) S[row * SLD + j] = -ajj * part;
+    cons_bar();
+  }
+}
+
+__device__ void scan_zero_diag(const double* tile, int b, int64_t bp, SmemCtl& ctl) {
+  for (int i = threadIdx.x; i < b; i += 256)
+    if (__ldcg(tile + (int64_t)i * bp + i) == 0.0) atomicMin(&ctl.scan_min, i);
+}
+
+__device__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams& P, SmemCtl& ctl, double* S,
+                            int b) {
+  const int64_t bp = P.bp;
+  const int R = P.R;
+  double* tile = P.pool + (int64_t)it.out_s * P.slot_elems;
+  const int d = jb.d;
+  if (ctl.fail_code) return;  // item already failed: keep the job protocol, skip work
+  switch (jb.special) {
+    case SP_POTRF_DIAG: {
+      if (d == 0) zero_upper_blocks(tile, R, bp);
+      double* blk = tile + (int64_t)d * BLK * bp + d * BLK;
+      if (threadIdx.x == 0) ctl.scan_min = -1;
+      load_block_lower(S, blk, bp);
+      cons_bar();
+      const int f = small_potrf(S, ctl);
+      if (f >= 0) {
+        if (threadIdx.x == 0) {
+          ctl.fail_code = TINV_ERR_NOT_SPD;
+          ctl.fail_index = d * BLK + f;
+        }
+        cons_bar();
+        return;
+      }
+      store_block_lower(S, blk, bp);
+      cons_bar();
+      small_trtri(S);
+      store_block_lower(S, P.pool + (int64_t)it.scr_s * P.slot_elems, bp);
+      break;
+    }
+    case SP_INV_INIT: {  // aux <- tril(L) (lower tiles of L, zero upper), then scan
+      const double* src = P.pool + (int64_t)it.in0_s * P.slot_elems;
+      for (int r = 0; r < R; ++r)
+        for (int c = 0; c < R; ++c) {
+          const double* sb = src + (int64_t)r * BLK * bp + c * BLK;
+          double* db = tile + (int64_t)r * BLK * bp + c * BLK;
+          for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
+            const int i = e >> 7, j = e & 127;
+            db[i * bp + j] = (r > c || (r == c && j <= i)) ? __ldcg(sb + i * bp + j) : 0.0;
+          }
+        }
+      break;
+    }
+    case SP_TRTRI_DIAG: {
+      if (d == R - 1) {  // first diagonal phase: zero-pivot scan (kernels.py:125-127), clear upper
+        if (threadIdx.x == 0) ctl.scan_min = 1 << 30;
+        cons_bar();
+        scan_zero_diag(tile, b, bp, ctl);
+        cons_bar();
+        if (ctl.scan_min < (1 << 30)) {
+          if (threadIdx.x == 0) {
+            ctl.fail_code = TINV_ERR_SINGULAR;
+            ctl.fail_index = ctl.scan_min;
+          }
+          cons_bar();
+          return;
+        }
+        zero_upper_blocks(tile, R, bp);
+      }
+      double* blk = tile + (int64_t)d * BLK * bp + d * BLK;
+      load_block_lower(S, blk, bp);
+      cons_bar();
+      small_trtri(S);
+      store_block_lower(S, blk, bp);
+      break;
+    }
+    case SP_COPY_ROWS: {
+      const double* src = P.pool + (int64_t)it.in0_s * P.slot_elems + (int64_t)d * BLK * bp;
+      double* dst = tile + (int64_t)d * BLK * bp;
+      const int64_t n2 = (int64_t)BLK * bp / 2;
+      for (int64_t e = threadIdx.x; e < n2; e += 256)
+        reinterpret_cast<double2*>(dst)[e] = __ldcg(reinterpret_cast<const double2*>(src) + e);
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+// ---------------------------------------------------------------- scheduler (device side)
+__device__ __forceinline__ void push_task(const ExecParams& P, int s) {
+  const TaskDev& t = P.tasks[s];
+  const int lev = t.level;
+  const int pos = atomicAdd(&P.q_tail[lev], t.nitems);
+  unsigned long long* q = P.queue + P.q_off[lev] + pos;
+  for (int i = 0; i < t.nitems; ++i) st_release_u64(q + i, ((unsigned long long)(s + 1) << 32) | (unsigned)i);
+}
+
+constexpr unsigned long long POP_EXIT = ~0ull;
+
+__device__ unsigned long long pop_item(const ExecParams& P) {
+  unsigned last_prog = ld_relaxed_u32(P.progress);
+  unsigned long long t_last = globaltimer();
+  unsigned spin = 0;
+  while (true) {
+    if (ld_relaxed_s32(P.abort_flag)) return POP_EXIT;
+    if (ld_relaxed_s32(P.remaining) <= 0) return POP_EXIT;
+    for (int lev = 0; lev < NLEV; ++lev) {
+      int h = ld_relaxed_s32(P.q_head + lev);
+      const int t = ld_relaxed_s32(P.q_tail + lev);
+      while (h < t) {
+        const int prev = atomicCAS(P.q_head + lev, h, h + 1);
+        if (prev == h) {
+          const unsigned long long* slot = P.queue + P.q_off[lev] + h;
+          unsigned long long v;
+          while ((v = ld_acquire_u64(slot)) == 0ull) {
+          }
+          return v;
+        }
+        h = prev;
+      }
+    }
+    __nanosleep(spin < 64 ? 32 : 256);
+    ++spin;
+    if ((spin & 255) == 0) {  // watchdog: no item completed anywhere for 30 s
+      const unsigned pr = ld_relaxed_u32(P.progress);
+      const unsigned long long now = globaltimer();
+      if (pr != last_prog) {
+        last_prog = pr;
+        t_last = now;
+      } else if (now - t_last > 30ull * 1000000000ull) {
+        atomicMin(P.err, ((unsigned long long)0x7fffffffu << 32) | ((unsigned long long)TINV_ERR_INTERNAL << 24));
+        atomicExch(P.abort_flag, 1);
+        return POP_EXIT;
+      }
+    }
+  }
+}
+
+__device__ void complete_item(const ExecParams& P, const ItemInfo& it, SmemCtl& ctl) {
+  // warp 0 of the consumers; all consumer threads fenced their stores already
+  const int lane = threadIdx.x & 31;
+  int last = 0;
+  if (lane == 0) {
+    if (ctl.fail_code) {
+      const unsigned long long key = ((unsigned long long)(unsigned)it.ref_id << 32) |
+                                     ((unsigned long long)ctl.fail_code << 24) |
+                                     (unsigned long long)(ctl.fail_index & 0xffffff);
+      atomicMin(P.err, key);
+      atomicExch(P.abort_flag, 1);
+    } else {
+      const int old = atomicAdd(P.done + it.task, 1);
+      last = (old == it.nitems - 1);
+      if (last) {
+        const TaskDev& t = P.tasks[it.task];
+        if (t.flags & TF_RENAMED) {
+          const int cs = __ldcg(P.cur_slot + t.out);
+          P.cur_slot[t.out] = __ldcg(P.alt_slot + t.out);
+          P.alt_slot[t.out] = cs;
+        }
+        if (P.trace_end) {
+          atomicMax(P.trace_end + it.task, globaltimer() - P.t0);
+          P.trace_sm[it.task] = (int)smid();
+        }
+        __threadfence();
+      }
+    }
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (last) {
+    __syncwarp();
+    const TaskDev& t = P.tasks[it.task];
+    for (int k = t.succ_begin + lane; k < t.succ_end; k += 32) {
+      const int s = P.succ[k];
+      if (atomicSub(P.indeg + s, 1) == 1) push_task(P, s);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      atomicSub(P.remaining, 1);
+    }
+  }
+  if (lane == 0) atomicAdd(P.progress, 1u);
+}
+
+// ---------------------------------------------------------------- the kernel
+__global__ void __launch_bounds__(NTHREADS, 1)
+    exec_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmM, ExecParams P,
+                int b) {
+  extern __shared__ __align__(1024) char dsmem[];
+  __shared__ SmemCtl ctl;
+  char* ring = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
+  double* S = reinterpret_cast<double*>(ring);  // diagonal phases reuse the drained ring (+ extra)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int R = P.R;
+
+  if (tid == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&ctl.full[s], 1);
+      mbar_init(&ctl.empty[s], NCONS_WARPS);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&ctl.item_full[s], 1);
+      mbar_init(&ctl.item_empty[s], NCONS_WARPS);
+    }
+    ctl.jobs_done = 0;
+    ctl.fail_code = 0;
+    ctl.fail_index = -1;
+    ctl.scan_min = -1;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp >= NCONS_WARPS) {
+    // ============================ producer / scheduler warp
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PROD_REGS));
+    if (warp != NCONS_WARPS || lane != 0) return;
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmM)) : "memory");
+    unsigned ks = 0, issued = 0;
+    for (unsigned itn = 0;; ++itn) {
+      const int slot = itn & 1;
+      mbar_wait(&ctl.item_empty[slot], ((itn >> 1) & 1) ^ 1);
+      const unsigned long long e = pop_item(P);
+      ItemInfo it;
+      if (e == POP_EXIT) {
+        it.task = -1;
+        ctl.items[slot] = it;
+        mbar_arrive(&ctl.item_full[slot]);
+        break;
+      }
+      it.task = (int)(e >> 32) - 1;
+      it.item = (int)(e & 0xffffffffu);
+      const TaskDev t = P.tasks[it.task];
+      it.kind = t.kind;
+      it.step = t.step;
+      it.ref_id = t.ref_id;
+      it.nitems = t.nitems;
+      it.flags = t.flags;
+      it.out_s = __ldcg(P.cur_slot + t.out);
+      it.alt_s = (t.flags & TF_RENAMED) ? __ldcg(P.alt_slot + t.out) : -1;
+      it.in0_s = t.in0 >= 0 ? __ldcg(P.cur_slot + t.in0) : -1;
+      it.in1_s = t.in1 >= 0 ? __ldcg(P.cur_slot + t.in1) : -1;
+      it.scr_s = P.scratch_base + blockIdx.x;
+      it.njobs = job_count(it, R);
+      fence_proxy_async();  // tiles written by other SMs (generic proxy) -> TMA reads
+      ctl.items[slot] = it;
+      mbar_arrive(&ctl.item_full[slot]);
+      for (int jn = 0; jn < it.njobs; ++jn, ++issued) {
+        Job jb;
+        get_job(it, jn, R, jb);
+        if (jb.type == J_SPECIAL) {
+          while (ld_acquire_cta_u32(&ctl.jobs_done) < issued + 1) {
+          }
+          fence_proxy_async();
+          continue;
+        }
+        if (jb.dep) {
+          while (ld_acquire_cta_u32(&ctl.jobs_done) < issued) {
+          }
+          fence_proxy_async();
+        }
+        if (jb.c_s >= 0)  // warm L2 with the C block for the epilogue
+          for (int x = 0; x < BLK; x += 16) tma_prefetch3(&tmK, jb.o_c * BLK + x, jb.o_r * BLK, jb.c_s);
+        const bool aK = (jb.variant != V_TN), bK = (jb.variant == V_NT);
+        for (int kb = jb.k0; kb < jb.k1; ++kb) {
+          const int ka = jb.a_k0 + (kb - jb.k0), kbb = jb.b_k0 + (kb - jb.k0);
+          for (int ch = 0; ch < BLK / KCH; ++ch, ++ks) {
+            const int st = ks % NSTAGE;
+            mbar_wait(&ctl.empty[st], ((ks / NSTAGE) & 1) ^ 1);
+            char* sA = ring + st * STAGE_BYTES;
+            char* sB = sA + STAGE_BYTES / 2;
+            mbar_arrive_tx(&ctl.full[st], STAGE_BYTES);
+            if (aK) {
+              tma_load3(&tmK, sA, &ctl.full[st], ka * BLK + ch * KCH, jb.a_fix * BLK, jb.a_s);
+            } else {
+              for (int q = 0; q < 8; ++q)
+                tma_load3(&tmM, sA + q * 2048, &ctl.full[st], jb.a_fix * BLK + 16 * q, ka * BLK + ch * KCH, jb.a_s);
+            }
+            if (bK) {
+              tma_load3(&tmK, sB, &ctl.full[st], kbb * BLK + ch * KCH, jb.b_fix * BLK, jb.b_s);
+            } else {
+              for (int q = 0; q < 8; ++q)
+                tma_load3(&tmM, sB + q * 2048, &ctl.full[st], jb.b_fix * BLK + 16 * q, kbb * BLK + ch * KCH, jb.b_s);
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ============================ consumer warps
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONS_REGS));
+  unsigned ks = 0, jobs = 0;
+  for (unsigned itn = 0;; ++itn) {
+    const int slot = itn & 1;
+    mbar_wait(&ctl.item_full[slot], (itn >> 1) & 1);
+    const ItemInfo it = ctl.items[slot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ctl.item_empty[slot]);
+    if (it.task < 0) break;
+    if (tid == 0 && P.trace_start) atomicMin(P.trace_start + it.task, globaltimer() - P.t0);
+    for (int jn = 0; jn < it.njobs; ++jn) {
+      Job jb;
+      get_job(it, jn, R, jb);
+      if (jb.type == J_SPECIAL) {
+        run_special(jb, it, P, ctl, S, b);
+      } else if (jb.variant == V_NT) {
+        run_gemm<V_NT>(jb, P, ctl, ring, ks);
+      } else if (jb.variant == V_NN) {
+        run_gemm<V_NN>(jb, P, ctl, ring, ks);
+      } else {
+        run_gemm<V_TN>(jb, P, ctl, ring, ks);
+      }
+      fence_proxy_async();
+      cons_bar();
+      ++jobs;
+      if (tid == 0) st_release_cta_u32(&ctl.jobs_done, jobs);
+    }
+    __threadfence();
+    cons_bar();
+    if (warp == 0) complete_item(P, it, ctl);
+    cons_bar();
+    if (tid == 0) {
+      ctl.fail_code = 0;
+      ctl.fail_index = -1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host launch
+int exec_smem_bytes() { return SMEM_BYTES; }
+
+cudaError_t launch_exec(const CUtensorMap& tmK, const CUtensorMap& tmM, const ExecParams& P, int b, int grid,
+                        cudaStream_t stream) {
+  cudaError_t e = cudaFuncSetAttribute(exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  exec_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(tmK, tmM, P, b);
+  return cudaGetLastError();
+}
+
+}  // namespace tinv

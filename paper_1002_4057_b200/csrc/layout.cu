@@ -1,0 +1,150 @@
+// Dense <-> tile layout conversion (tile_matrix.py:84-119 on the device).
+//
+// Device tile store: every lower tile (i >= j) of the matrix is a contiguous
+// row-major bp x bp FP64 slot, bp = b rounded up to the 128 block. Padding is
+// closed under every kernel of the inversion: off-diagonal tiles pad with 0,
+// diagonal tiles pad with the identity.
+//
+// put: destination-driven copy of the real b x b part, pad filled.
+// get: destination-driven gather into a dense row-major matrix; mode LOWER
+// writes the lower tiles verbatim (to_dense on authoritative tiles), mode
+// SYMMETRIZE writes the full matrix with the upper triangle mirrored from the
+// lower one (symmetrize_lower(to_dense(tm)), tile_matrix.py:117-119), the
+// transposed sub-blocks staged through shared memory for coalescing.
+// Both are HBM-bound: 8 bytes read + 8 written per element moved.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tinv_internal.h"
+
+namespace tinv {
+
+__device__ __forceinline__ void tri_decode(int64_t x, int& i, int& j) {
+  int64_t r = (int64_t)((sqrt(8.0 * (double)x + 1.0) - 1.0) * 0.5);
+  while (r * (r + 1) / 2 > x) --r;
+  while ((r + 1) * (r + 2) / 2 <= x) ++r;
+  i = (int)r;
+  j = (int)(x - r * (r + 1) / 2);
+}
+
+// grid.x: lower tiles tri_lo .. tri_lo + gridDim.x - 1; grid.y: 8-row groups of bp
+// src: dense rows starting at global row `row0`
+__global__ void __launch_bounds__(256) k_put(const double* __restrict__ src, int64_t lda, int64_t row0,
+                                            double* __restrict__ pool, int64_t slot_elems,
+                                            const int32_t* __restrict__ slot_of, int b, int bp, int64_t tri_lo) {
+  int i, j;
+  const int64_t x = tri_lo + blockIdx.x;
+  tri_decode(x, i, j);
+  double* dst = pool + (int64_t)slot_of[x] * slot_elems;
+  const int rr = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (rr >= bp) return;
+  const double* srow = src + ((int64_t)i * b + rr - row0) * lda + (int64_t)j * b;
+  double* drow = dst + (int64_t)rr * bp;
+  for (int cc = threadIdx.x & 31; cc < bp; cc += 32) {
+    double v;
+    if (rr < b && cc < b)
+      v = __ldg(srow + cc);
+    else
+      v = (i == j && rr == cc) ? 1.0 : 0.0;
+    drow[cc] = v;
+  }
+}
+
+// One 32x32 destination sub-block per CTA (blockDim 32 x 8).
+// grid.x: destination tiles; for panel gathers the tile row I is fixed
+// (`panel_i` >= 0) and J = blockIdx.x; otherwise (I, J) enumerates the lower
+// tiles (LOWER) or the full t x t grid (SYMMETRIZE). grid.y: sub-block index.
+__global__ void __launch_bounds__(256) k_get(double* __restrict__ dst, int64_t ldd, int64_t row0,
+                                            const double* __restrict__ pool, int64_t slot_elems,
+                                            const int32_t* __restrict__ slot_of, int b, int bp, int t,
+                                            int panel_i, int64_t tile_lo, int symmetrize) {
+  __shared__ double sm[32][33];
+  int I, J;
+  if (panel_i >= 0) {
+    I = panel_i;
+    J = (int)(tile_lo + blockIdx.x);
+  } else if (symmetrize) {
+    const int64_t x = tile_lo + blockIdx.x;
+    I = (int)(x / t);
+    J = (int)(x % t);
+  } else {
+    tri_decode(tile_lo + blockIdx.x, I, J);
+  }
+  const int nsb = (b + 31) / 32;
+  const int sr = blockIdx.y / nsb, sc = blockIdx.y % nsb;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  // source tile and whether the sub-block is read transposed
+  bool transp;
+  int si, sj;
+  if (I > J) {
+    transp = false;
+    si = I;
+    sj = J;
+  } else if (I < J) {
+    transp = true;
+    si = J;
+    sj = I;
+  } else {
+    si = sj = I;
+    transp = symmetrize && (sr < sc);
+  }
+  const double* tile = pool + (int64_t)slot_of[(int64_t)si * (si + 1) / 2 + sj] * slot_elems;
+  // source sub-block coordinates
+  const int br = transp ? sc : sr, bc = transp ? sr : sc;
+  for (int k = ty; k < 32; k += 8) {
+    const int r = br * 32 + k, c = bc * 32 + tx;
+    sm[k][tx] = (r < b && c < b) ? tile[(int64_t)r * bp + c] : 0.0;
+  }
+  __syncthreads();
+  const bool diag_mix = symmetrize && I == J && sr == sc;
+  for (int k = ty; k < 32; k += 8) {
+    const int r = sr * 32 + k, c = sc * 32 + tx;  // destination element within tile (I, J)
+    if (r >= b || c >= b) continue;
+    double v;
+    if (diag_mix)
+      v = (k >= tx) ? sm[k][tx] : sm[tx][k];
+    else
+      v = transp ? sm[tx][k] : sm[k][tx];
+    dst[((int64_t)I * b + r - row0) * ldd + (int64_t)J * b + c] = v;
+  }
+}
+
+cudaError_t launch_put(const double* src, int64_t lda, int64_t row0, double* pool, int64_t slot_elems,
+                       const int32_t* slot_of, int b, int bp, int64_t tri_lo, int64_t ntiles, cudaStream_t st) {
+  if (ntiles <= 0) return cudaSuccess;
+  dim3 grid((unsigned)ntiles, (unsigned)((bp + 7) / 8));
+  k_put<<<grid, 256, 0, st>>>(src, lda, row0, pool, slot_elems, slot_of, b, bp, tri_lo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_get(double* dst, int64_t ldd, int64_t row0, const double* pool, int64_t slot_elems,
+                       const int32_t* slot_of, int b, int bp, int t, int panel_i, int64_t tile_lo,
+                       int64_t ntiles, int symmetrize, cudaStream_t st) {
+  if (ntiles <= 0) return cudaSuccess;
+  const int nsb = (b + 31) / 32;
+  dim3 grid((unsigned)ntiles, (unsigned)(nsb * nsb));
+  k_get<<<grid, 256, 0, st>>>(dst, ldd, row0, pool, slot_elems, slot_of, b, bp, t, panel_i, tile_lo, symmetrize);
+  return cudaGetLastError();
+}
+
+// D2D copy of whole slots (snapshot / restore for TINV_KEEP_ON_FAILURE)
+__global__ void k_copy_slots(double* pool, int64_t slot_elems, const int32_t* from, const int32_t* to) {
+  const double2* s = reinterpret_cast<const double2*>(pool + (int64_t)from[blockIdx.y] * slot_elems);
+  double2* d = reinterpret_cast<double2*>(pool + (int64_t)to[blockIdx.y] * slot_elems);
+  const int64_t n2 = slot_elems / 2;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (int64_t)gridDim.x * blockDim.x)
+    d[e] = s[e];
+}
+
+cudaError_t launch_copy_slots(double* pool, int64_t slot_elems, const int32_t* from, const int32_t* to,
+                              int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  for (int64_t off = 0; off < n; off += 65535) {
+    const int64_t cnt = (n - off) < 65535 ? (n - off) : 65535;
+    dim3 grid(8, (unsigned)cnt);
+    k_copy_slots<<<grid, 256, 0, st>>>(pool, slot_elems, from + off, to + off);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace tinv

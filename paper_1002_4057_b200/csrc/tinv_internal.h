@@ -1,0 +1,80 @@
+// Internal structures shared by the host planner (plan.cpp) and the device
+// executor (executor.cu). Not part of the C-ABI.
+#pragma once
+#include <stdint.h>
+
+#include "../../include/tileinv_b200.h"
+
+namespace tinv {
+
+// The sub-tile ("block") every device job works on: 128 x 128 FP64.
+constexpr int BLK = 128;
+// Work-item queue priority levels (0 = most critical).
+constexpr int NLEV = 8;
+// Executor CTA: two consumer warpgroups (8 DMMA warps) + one producer
+// warpgroup (warp 8 = scheduler + TMA issue); registers are rebalanced with
+// setmaxnreg (producer 56, consumers 224).
+constexpr int NCONS_WARPS = 8;
+constexpr int NTHREADS = (NCONS_WARPS + 4) * 32;
+constexpr int PROD_REGS = 56;
+constexpr int CONS_REGS = 224;
+// TMA ring: stages of (A 128x16 + B 128x16) doubles.
+constexpr int NSTAGE = 4;
+constexpr int KCH = 16;                         // K per chunk
+constexpr int STAGE_BYTES = 2 * BLK * KCH * 8;  // 32 KB
+constexpr int EXTRA_SMEM = 64 * 1024;           // extra scratch for diagonal phases
+constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + EXTRA_SMEM + 2048;
+
+// Hidden task kind inserted by the planner: INV(L) -> aux = tril(L)^-1,
+// shared by every TRSM reading that version of L (TRSM then runs as a
+// DMMA triangular multiply by the inverse).
+constexpr int KIND_INV = 11;
+
+enum TaskFlags : int32_t {
+  TF_RENAMED = 1,  // output written to the alternate slot, slots swapped at completion
+};
+
+struct TaskDev {
+  int8_t kind;
+  int8_t step;
+  int8_t flags;
+  int8_t level;
+  int32_t nitems;
+  int32_t out;     // logical tile ids
+  int32_t in0;
+  int32_t in1;
+  int32_t ref_id;  // reference task id (errors / trace)
+  int32_t succ_begin;
+  int32_t succ_end;
+};
+
+struct ExecParams {
+  double* pool;            // all tile slots, slot s at pool + s * slot_elems
+  int64_t slot_elems;      // bp * bp
+  int32_t bp;              // padded tile order (multiple of BLK)
+  int32_t R;               // bp / BLK
+  int32_t ntasks;
+  int32_t scratch_base;    // slot of CTA 0's scratch tile; CTA c uses scratch_base + c
+  const TaskDev* tasks;
+  const int32_t* succ;
+  int32_t* indeg;
+  int32_t* done;           // items finished per task
+  int32_t* cur_slot;       // logical tile -> physical slot (mutable: renaming)
+  int32_t* alt_slot;
+  unsigned long long* queue;       // all levels back to back
+  int64_t q_off[NLEV + 1];         // level l occupies queue[q_off[l] .. q_off[l+1])
+  int32_t* q_head;                 // NLEV
+  int32_t* q_tail;                 // NLEV
+  int32_t* remaining;              // tasks not yet completed
+  int32_t* abort_flag;
+  unsigned long long* err;         // packed min failure (ref task << 32 | code << 24 | index)
+  unsigned int* progress;          // completed items (watchdog)
+  unsigned long long* trace_start; // per exec task, optional
+  unsigned long long* trace_end;
+  int32_t* trace_sm;
+  unsigned long long t0;           // globaltimer at launch (trace base)
+};
+
+inline int64_t tri_index(int64_t i, int64_t j) { return i * (i + 1) / 2 + j; }
+
+}  // namespace tinv

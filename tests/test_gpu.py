@@ -1,0 +1,270 @@
+"""Parity of the B200 path against the oracle and the reference's golden
+vectors. Runs on the GPU box (pytest -m gpu); every call goes through the
+C-ABI library (libtileinv_b200.so).
+
+Tolerances (BASELINE.json north_star, SURVEY.md §8(d) finding 12):
+  * inversion / per-step outputs: normwise max|X-R|/max|R| <= 1e-10 * cond(A)
+    and residual ||I - A X||_1 / (n ||A||_1 ||X||_1 eps) = O(1) (< 10);
+  * single tile kernels vs the reference kernels: <= 1e-12 relative
+    normwise;
+  * schedule independence: bitwise.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1002_4057_b200 as P
+from paper_1002_4057_b200 import _native
+from paper_1002_4057_b200 import kernels as K
+from oracle import tileinv_oracle as O
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def rel(x, r):
+    return float(np.max(np.abs(x - r)) / max(np.max(np.abs(r)), 1e-300))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if _native.device_count() < 1:
+        pytest.fail("no B200 visible: the GPU tests must run on the GPU box")
+
+
+# ---------------------------------------------------------------- tile kernels
+@pytest.mark.parametrize("b", [1, 3, 8, 17])
+def test_tile_kernels_vs_reference_golden(b):
+    g = np.load(os.path.join(GOLD, "kernels.npz"))
+    f = lambda k: g[f"b{b}_{k}"]  # noqa: E731
+    spd, lo, c, a, bb = f("spd"), f("lo"), f("c"), f("a"), f("b")
+    tol = 1e-12
+    assert rel(K.potrf(spd), f("potrf")) < tol
+    assert rel(K.trsm_right_lt(a, lo), f("trsm")) < tol
+    assert rel(K.syrk_sub(c, a), f("syrk_sub")) < tol
+    assert rel(K.syrk_add_t(c, a), f("syrk_add_t")) < tol
+    assert rel(K.gemm(c, a, bb, False, -1), f("gemm_nt")) < tol
+    assert rel(K.gemm(c, a, bb, False, 1), f("gemm_nn")) < tol
+    assert rel(K.gemm(c, a, bb, True, 1), f("gemm_tn")) < tol
+    assert rel(K.trtri(lo), f("trtri")) < tol
+    assert rel(K.trmm_left(a, lo), f("trmm_left")) < tol
+    assert rel(K.trmm_right_neg(a, lo), f("trmm_right_neg")) < tol
+    assert rel(K.trmm_left_t(a, lo), f("trmm_left_t")) < tol
+    assert rel(K.lauum(lo), f("lauum")) < tol
+
+
+@pytest.mark.parametrize("b", [64, 128, 200, 256, 512])
+def test_tile_kernels_vs_oracle(b):
+    rng = np.random.default_rng(b)
+    m = rng.standard_normal((b, b))
+    spd = m @ m.T / b + np.eye(b)
+    lo = np.tril(rng.standard_normal((b, b))) / np.sqrt(b) + 2 * np.eye(b)
+    lo_dirty = lo + np.triu(rng.standard_normal((b, b)), 1)
+    c, a, bb = (rng.standard_normal((b, b)) for _ in range(3))
+    tol = 1e-12
+    assert rel(K.potrf(spd + np.triu(rng.standard_normal((b, b)), 1)), O.potrf(spd)) < tol
+    assert rel(K.trsm_right_lt(a, lo_dirty), O.trsm_right_lt(a, lo)) < tol
+    assert rel(K.syrk_sub(c, a), O.syrk_sub(c, a)) < tol
+    assert rel(K.syrk_add_t(c, a), O.syrk_add_t(c, a)) < tol
+    for ta, sg in ((False, -1), (False, 1), (True, 1)):
+        assert rel(K.gemm(c, a, bb, ta, sg), O.gemm(c, a, bb, ta, sg)) < tol
+    assert rel(K.trtri(lo_dirty), O.trtri(lo)) < tol
+    assert rel(K.trmm_left(a, lo_dirty), O.trmm_left(a, lo)) < tol
+    assert rel(K.trmm_right_neg(a, lo_dirty), O.trmm_right_neg(a, lo)) < tol
+    assert rel(K.trmm_left_t(a, lo_dirty), O.trmm_left_t(a, lo)) < tol
+    assert rel(K.lauum(lo_dirty), O.lauum(lo)) < tol
+    # output structure: strict upper zero for POTRF / TRTRI, symmetric LAUUM / SYRK
+    assert not np.triu(K.potrf(spd), 1).any()
+    assert not np.triu(K.trtri(lo_dirty), 1).any()
+    s = K.syrk_add_t(c, a)
+    assert np.array_equal(s, s.T)
+
+
+def test_tile_kernel_errors():
+    with pytest.raises(K.NotPositiveDefiniteError) as ei:
+        K.potrf(np.array([[1.0, 0.0], [2.0, 1.0]]))
+    assert ei.value.index == 1
+    a = np.eye(300) * 4
+    a[257, 257] = -1.0
+    with pytest.raises(K.NotPositiveDefiniteError) as ei:
+        K.potrf(a)
+    assert ei.value.index == 257
+    l = np.eye(200)
+    l[150, 150] = 0.0
+    l[170, 170] = 0.0
+    with pytest.raises(K.SingularTileError) as ei:
+        K.trtri(l)
+    assert ei.value.index == 150
+    with pytest.raises(K.SingularTileError) as ei:
+        K.trsm_right_lt(np.ones((200, 200)), l)
+    assert ei.value.index == 150
+
+
+# ---------------------------------------------------------------- golden numerics
+def _tile_mask(n, b):
+    t = n // b
+    m = np.zeros((n, n), bool)
+    for i in range(t):
+        for j in range(i + 1):
+            m[i * b:(i + 1) * b, j * b:(j + 1) * b] = True
+    return m
+
+
+@pytest.mark.parametrize("n,b", [(64, 16), (120, 40)])
+def test_steps_and_inversions_vs_reference_golden(n, b):
+    g = np.load(os.path.join(GOLD, "numeric.npz"))
+    a = g[f"n{n}_A"]
+    t = n // b
+    tol = 1e-10 * np.linalg.cond(a)
+    mask = _tile_mask(n, b)
+    for pl in P.Placement:
+        tm = P.from_dense(a, b)
+        P.execute(P.gen_step1(t, "U"), tm)
+        x1 = P.to_dense(tm)
+        assert rel(np.tril(x1), g[f"n{n}_{pl.value}_step1"]) < tol
+        assert np.array_equal(x1[~mask], a[~mask])  # upper tiles stay stale A
+        P.execute(P.gen_step2(t, "D", pl), tm)
+        assert rel(np.tril(P.to_dense(tm)), g[f"n{n}_{pl.value}_step2"]) < tol
+        P.execute(P.gen_step3(t, "U", pl), tm)
+        x3 = P.to_dense(tm)
+        r3 = g[f"n{n}_{pl.value}_step3"]
+        assert rel(x3[mask], r3[mask]) < tol
+        assert np.array_equal(x3[~mask], r3[~mask])
+    for pl in P.Placement:
+        for loops in ("UDU", "UUU"):
+            for pipe in (True, False):
+                tm = P.from_dense(a, b)
+                P.execute(P.gen_inversion(t, P.VariantConfig(pl, loops, pipe)), tm)
+                x = P.symmetrize_lower(P.to_dense(tm))
+                assert rel(x, g[f"n{n}_full_{pl.value}_{loops}_{int(pipe)}"]) < tol
+                assert O.residual(a, x) < 10
+
+
+def test_errors_vs_reference_golden():
+    with open(os.path.join(GOLD, "errors.json")) as fh:
+        g = json.load(fh)
+    a = np.load(os.path.join(GOLD, "npd_A.npy"))
+    for pl in P.Placement:
+        tm = P.from_dense(a, 16)
+        before = P.to_dense(tm)
+        with pytest.raises(P.ExecutionError) as ei:
+            P.execute(P.gen_inversion(4, P.VariantConfig(pl)), tm, workers=3)
+        exp = g[f"npd_{pl.value}"]
+        assert ei.value.task.id == exp["task"]
+        assert str(ei.value.task).startswith(exp["kind"])
+        assert isinstance(ei.value.cause, P.NotPositiveDefiniteError)
+        assert ei.value.cause.index == exp["index"]
+        assert np.array_equal(P.to_dense(tm), before)  # a unchanged on failure
+    l = np.load(os.path.join(GOLD, "singular_L.npy"))
+    tm = P.from_dense(l, 16)
+    with pytest.raises(P.ExecutionError) as ei:
+        P.execute(P.gen_step2(4, "D"), tm)
+    assert ei.value.task.id == g["singular_step2"]["task"]
+    assert isinstance(ei.value.cause, P.SingularTileError)
+    assert ei.value.cause.index == g["singular_step2"]["index"]
+
+
+def _stream(t, specs):
+    """TaskStream from (kind, step, indices, reads, out) tuples on label A."""
+    tasks = []
+    for tid, (kind, step, idx, reads, out) in enumerate(specs):
+        acc = tuple(P.Access(P.TileId("A", *r), P.Mode.READ) for r in reads)
+        acc += (P.Access(P.TileId("A", *out), P.Mode.READWRITE),)
+        tasks.append(P.Task(tid, kind, idx, acc, step))
+    return P.TaskStream(tasks, set(), t)
+
+
+def test_failure_after_device_run_restores_device_state():
+    # run 1 succeeds and leaves the device copy authoritative (host stale);
+    # run 2 fails -> `a` must hold exactly the run-1 result (scheduler.py:345-351)
+    n, b = 256, 64
+    a = O.spd_matrix(n)
+    k = P.KernelKind
+    run1 = _stream(4, [(k.SYRK_SUB, P.Step.CHOLESKY, (1, 0), [(1, 0)], (1, 1))] * 50)
+    run2 = _stream(4, [(k.POTRF, P.Step.CHOLESKY, (1,), [], (1, 1))])
+    twin = P.from_dense(a, b)
+    P.execute(run1, twin)
+    expect = P.to_dense(twin)
+    tm = P.from_dense(a, b)
+    P.execute(run1, tm)
+    with pytest.raises(P.ExecutionError) as ei:
+        P.execute(run2, tm)
+    assert isinstance(ei.value.cause, P.NotPositiveDefiniteError)
+    assert np.array_equal(P.to_dense(tm), expect)
+
+
+# ---------------------------------------------------------------- BASELINE config 1 and larger
+def test_config1_full_and_steps_vs_oracle():
+    n, b = 1024, 128
+    a = O.spd_matrix(n, 0, 1.0)
+    cond = np.linalg.cond(a)
+    ref = O.invert(a, b)
+    x = P.invert(a, b)
+    assert rel(x, ref) <= 1e-10 * cond
+    assert O.residual(a, x) < 10
+    st = O.run_in_order(O.gen_stream(8, (1,), "U"), O.lower_tiles(a, b))
+    tm = P.from_dense(a, b)
+    P.execute(P.gen_step1(8, "U"), tm)
+    assert rel(np.tril(P.to_dense(tm)), O.assemble_lower(st, n, b)) <= 1e-10 * cond
+    st = O.run_in_order(O.gen_stream(8, (2,), "D"), st)
+    P.execute(P.gen_step2(8, "D"), tm)
+    assert rel(np.tril(P.to_dense(tm)), O.assemble_lower(st, n, b)) <= 1e-10 * cond
+    st = O.run_in_order(O.gen_stream(8, (3,), "U"), st)
+    P.execute(P.gen_step3(8, "U"), tm)
+    assert rel(P.to_dense(tm)[_tile_mask(n, b)], O.assemble_lower(st, n, b)[_tile_mask(n, b)]) <= 1e-10 * cond
+
+
+@pytest.mark.parametrize("n,b", [(1024, 256), (2048, 512), (2048, 1024), (1536, 384), (1000, 200)])
+def test_larger_tiles_vs_numpy(n, b):
+    a = O.spd_matrix(n, 1, 1e-2)
+    x = P.invert(a, b, P.VariantConfig(P.Placement.OUT_OF_PLACE))
+    ref = np.linalg.inv(a)
+    assert rel(x, ref) <= 1e-10 * np.linalg.cond(a)
+    assert O.residual(a, x) < 10
+
+
+def test_variants_and_determinism():
+    n, b = 768, 96
+    a = O.spd_matrix(n, 3, 0.5)
+    ref = O.invert(a, b)
+    outs = []
+    for pl in P.Placement:
+        for loops in ("UDU", "UUU", "DDD"):
+            for pipe in (True, False):
+                x = P.invert(a, b, P.VariantConfig(pl, loops, pipe))
+                assert rel(x, ref) < 1e-12
+                outs.append(x)
+    # bitwise determinism: repeated runs and sequential replay
+    s = P.gen_inversion(8, P.VariantConfig(P.Placement.OUT_OF_PLACE))
+    runs = []
+    for _ in range(3):
+        tm = P.from_dense(a, b)
+        P.execute(s, tm)
+        runs.append(P.to_dense(tm))
+    tm = P.from_dense(a, b)
+    P.run_in_order(s, tm)
+    runs.append(P.to_dense(tm))
+    for r in runs[1:]:
+        assert np.array_equal(r, runs[0])
+
+
+def test_layout_roundtrip_and_trace(tmp_path):
+    n, b = 640, 160
+    a = np.random.default_rng(5).standard_normal((n, n))
+    tm = P.from_dense(a, b)
+    tm._device()
+    tm._state = 2  # force a device read-back of the lower tiles
+    assert np.array_equal(P.to_dense(tm), a)
+    spd = O.spd_matrix(n, 2)
+    tm = P.from_dense(spd, b)
+    trace = tmp_path / "trace.csv"
+    P.execute(P.gen_inversion(4, P.VariantConfig()), tm, trace_path=str(trace))
+    rows = trace.read_text().strip().split("\n")
+    assert rows[0] == "task_id,kind,indices,worker,start_ns,end_ns"
+    assert len(rows) == 1 + 60
+    for r in rows[1:]:
+        tid, kind, idx, w, s, e = r.split(",")
+        assert 0 <= int(s) <= int(e)
