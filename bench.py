@@ -1,0 +1,334 @@
+"""Benchmark: FP64 SPD tile inversion Gflop/s (n^3 / t) on B200.
+
+Workload (BASELINE.json metric, config 3, fits one B200): n = 32768,
+nb = 512, A = G G^T / n + I with G iid N(0,1) (generated on the device,
+seed 0), the paper's best variant (out-of-place, UDU, pipelined).
+
+One step = dense A (resident in HBM) -> tile store (layout kernel) ->
+persistent executor over the whole POTRF/TRTRI/LAUUM DAG -> symmetrized dense
+A^-1 (layout kernel). Inputs are 8.6 GB, far above the 126 MB L2, so no flush
+is needed between steps. `e2e` repeats the step through the C-ABI with pinned
+HOST buffers (H2D of the lower tiles + D2H of the full inverse inside the
+timed region, plan creation included).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Under torchrun (N > 1) every rank inverts its own matrix (replicas, weak
+scaling): the distributed 2D block-cyclic path is not built yet.
+`--impl reference` times the reference algorithm on the host cores (the
+oracle port of tileinv: numpy kernels + threaded hazard-DAG executor).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SPD inversion FP64 Gflop/s (n³/t) at n=32768, 1/2/4/8 B200; % of FP64 peak"
+DMMA_PEAK_TFLOPS = 37.07   # measured: tools/fp64_peak.cu, profiles/r01_fp64_peak.log (sustained, 1965 MHz)
+DGEMM_TFLOPS = 35.47       # cuBLAS DGEMM 8192^3 comparator, profiles/r01_dgemm_peak.json
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--n", type=int, default=32768)
+    p.add_argument("--nb", type=int, default=512)
+    p.add_argument("--placement", default="out", choices=["in", "out"])
+    p.add_argument("--loops", default="UDU")
+    p.add_argument("--barriered", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-sample-n", type=int, default=8192)
+    p.add_argument("--cpu-worker", action="store_true", help=argparse.SUPPRESS)
+    return p.parse_args()
+
+
+# --------------------------------------------------------------------- CPU side
+def cpu_worker(n, nb, steps, warmup, placement, loops, pipelined):
+    """Runs in a subprocess with OPENBLAS_NUM_THREADS=1: the reference's CPU
+    algorithm (oracle port) with one worker thread per host core."""
+    import numpy as np
+
+    from oracle import tileinv_oracle as O
+    from threadpoolctl import threadpool_limits
+    cores = len(os.sched_getaffinity(0))
+    a = O.spd_matrix(n, 0, 1.0)  # input generation uses every BLAS thread
+    s = O.gen_stream(n // nb, (1, 2, 3), loops, placement == "out", pipelined)
+    times = []
+    with threadpool_limits(1, "blas"):  # the reference's fastest mode: workers = cores, BLAS 1 thread
+        for k in range(warmup + steps):
+            t0 = time.perf_counter()
+            O.execute(s, O.lower_tiles(a, nb), workers=cores)
+            dt = time.perf_counter() - t0
+            if k >= warmup:
+                times.append(dt)
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            model = next(l.split(":", 1)[1].strip() for l in fh if l.startswith("model name"))
+    except Exception:  # noqa: BLE001
+        pass
+    print(json.dumps({"times": times, "cores": cores, "cpu": model, "flops": float(n) ** 3}))
+
+
+def run_cpu(n, nb, steps, warmup, placement, loops, pipelined):
+    env = dict(os.environ)
+    for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        env.pop(k, None)
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-worker", "--n", str(n), "--nb", str(nb),
+           "--steps", str(steps), "--warmup", str(warmup), "--placement", placement, "--loops", loops]
+    if not pipelined:
+        cmd.append("--barriered")
+    out = subprocess.run(cmd, env=env, capture_output=True, text=True, check=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+# --------------------------------------------------------------------- clocks
+class Clocks:
+    def __init__(self, index):
+        self.samples = []
+        self.stop = threading.Event()
+        self.index = index
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits", "-lms", "200"],
+                                 stdout=subprocess.PIPE, text=True)
+        except FileNotFoundError:
+            return
+        while not self.stop.is_set():
+            line = p.stdout.readline()
+            if not line:
+                break
+            self.samples.append([x.strip() for x in line.split(",")])
+        p.terminate()
+
+    def __enter__(self):
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+        time.sleep(0.5)
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=3)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        smax = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        loaded = [v for v in sm if v > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------- GPU side
+def main():
+    args = parse()
+    if args.cpu_worker:
+        cpu_worker(args.n, args.nb, args.steps, args.warmup, args.placement, args.loops, not args.barriered)
+        return
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n, nb = args.n, args.nb
+    t = n // nb
+    pipelined = not args.barriered
+    flops = float(n) ** 3
+    config = {"workload": f"BASELINE config 3: n={n}, nb={nb}, FP64 SPD inversion "
+                          f"({args.placement}-of-place, {args.loops}, {'pipelined' if pipelined else 'barriered'})",
+              "n": n, "nb": nb, "t": t, "placement": args.placement, "loops": args.loops,
+              "pipelined": pipelined, "input": "A = G G^T/n + I, G iid N(0,1) seed 0",
+              "l2": "inputs 8.6 GB >> 126 MB L2 (no flush needed)",
+              "parallelism": "1 GPU" if world == 1 else f"replicas x{world} (independent matrices)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        steps = max(1, args.steps)
+        warm = max(0, min(args.warmup, 1))
+        r = run_cpu(args.cpu_sample_n, nb, steps, warm, args.placement, args.loops, pipelined)
+        ts = r["times"]
+        med = statistics.median(ts)
+        v = r["flops"] / med / 1e9
+        sample = (f"n={args.cpu_sample_n}, nb={nb} (t={args.cpu_sample_n // nb}) full inversion per step, "
+                  f"same variant; median of {len(ts)}")
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": v, "unit": "Gflop/s", "n_gpus": args.gpus,
+            "steps": steps, "warmup": warm, "ms_per_step": med * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+            "cpu_baseline": {"value": v, "unit": "Gflop/s", "cores": r["cores"], "kind": "port",
+                             "sample": sample, "cpu": r["cpu"]},
+            "e2e": {"value": v, "unit": "Gflop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }))
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_1002_4057_b200 as P
+    from paper_1002_4057_b200 import _native
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        v = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        return float(v.item())
+
+    # input on the device
+    gen = torch.Generator(device="cuda").manual_seed(rank)
+    g = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=gen)
+    a = torch.matmul(g, g.T)
+    del g
+    a.div_(n)
+    a.diagonal().add_(1.0)
+    a = torch.tril(a) + torch.tril(a, -1).T
+    x = torch.empty_like(a)
+
+    stream = torch.cuda.current_stream()
+    ctx = _native.Context(n, nb, local)
+    ctx.set_stream(stream.cuda_stream)
+    s = P.gen_inversion(t, P.VariantConfig(P.Placement(args.placement), args.loops, pipelined))
+    table = s.table()
+    bars = np.array(sorted(s.barriers), dtype=np.int64)
+    plan = _native.Plan(ctx, table, t, bars)
+    if plan.rc != 0:
+        raise RuntimeError(plan.msg)
+    stats = plan.stats()
+
+    kern_ms = []
+
+    def step():
+        ctx.put_dense_device(a.data_ptr(), n)
+        rc, err, ms = plan.run()
+        if rc != 0:
+            raise RuntimeError(f"executor failed: {plan.msg} task {err.task_id}")
+        kern_ms.append(ms)
+        ctx.get_dense_device(x.data_ptr(), n, _native.DENSE_SYMMETRIZE)
+
+    for _ in range(args.warmup):
+        step()
+    kern_ms.clear()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_step = ms_total / args.steps
+    value = world * flops / (ms_step * 1e-3) / 1e9
+    kern_avg = statistics.mean(kern_ms)
+    achieved = flops / (kern_avg * 1e-3) / 1e12
+
+    # numerical check of the last step (outside the timed region)
+    eye = torch.eye(n, dtype=torch.float64, device="cuda")
+    r = eye - a @ x
+    res = float(torch.linalg.matrix_norm(r, 1) / (n * torch.linalg.matrix_norm(a, 1)
+                                                   * torch.linalg.matrix_norm(x, 1) * 2.220446049250313e-16))
+    sym_err = float((x - x.T).abs().max())
+    del r, eye
+
+    # end to end through the C-ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        ha = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        ha.copy_(a)
+        hx = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        del a, x
+        torch.cuda.empty_cache()
+        ha_np, hx_np = ha.numpy(), hx.numpy()
+        ctx.set_stream(0)
+        plan.close()
+
+        def e2e_step():
+            st = P.gen_inversion(t, P.VariantConfig(P.Placement(args.placement), args.loops, pipelined))
+            ctx.put_dense(ha_np)
+            pl = _native.Plan(ctx, st.table(), t, np.array(sorted(st.barriers), dtype=np.int64))
+            rc, err, _ = pl.run()
+            pl.close()
+            if rc != 0:
+                raise RuntimeError("e2e executor failed")
+            ctx.get_dense(hx_np, _native.DENSE_SYMMETRIZE)
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        k = max(1, min(args.steps, 3))
+        for _ in range(k):
+            e2e_step()
+        barrier()
+        e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / k)
+        T = t * (t + 1) // 2
+        e2e = {"value": world * flops / (e2e_ms * 1e-3) / 1e9, "unit": "Gflop/s",
+               "h2d_bytes_per_step": T * nb * nb * 8, "d2h_bytes_per_step": n * n * 8,
+               "ms_per_step": e2e_ms, "steps": k,
+               "path": "gen_stream + put_dense(pinned host) + plan_create + plan_exec + get_dense(symmetrize, pinned host)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r = run_cpu(args.cpu_sample_n, nb, 1, 0, args.placement, args.loops, pipelined)
+        cpu = {"value": r["flops"] / statistics.median(r["times"]) / 1e9, "unit": "Gflop/s", "cores": r["cores"],
+               "kind": "port", "cpu": r["cpu"],
+               "sample": f"n={args.cpu_sample_n}, nb={nb} full inversion (oracle port of tileinv: numpy kernels, "
+                         f"threaded hazard-DAG executor, {r['cores']} workers, BLAS 1 thread)"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "Gflop/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / DMMA_PEAK_TFLOPS, "traffic": None,
+                         "kernel": "tinv::exec_kernel (persistent DAG executor, DMMA.8x8x4)",
+                         "algorithmic": f"n^3 = {flops:.3e} flop per launch",
+                         "peak_source": "measured FP64 DMMA peak (tools/fp64_peak.cu); cuBLAS DGEMM "
+                                        f"{DGEMM_TFLOPS} TF/s for context; MEASURED_PEAKS.json has no FP64 entry"},
+            "pct_fp64_peak": 100.0 * value / world / 1e3 / DMMA_PEAK_TFLOPS,
+            "kernel_ms": kern_avg, "plan": stats,
+            "residual": res, "symmetry_err": sym_err,
+            "gpu_launches": 3 * args.steps,
+            "clocks": clk.summary(),
+            "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(out))
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

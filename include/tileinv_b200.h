@@ -100,6 +100,9 @@ const char* tinv_last_error(const tinv_ctx* ctx);
 int tinv_create(tinv_ctx** ctx, int64_t n, int64_t b, int device);
 int tinv_destroy(tinv_ctx* ctx);
 int tinv_shape(const tinv_ctx* ctx, int64_t* n, int64_t* b, int64_t* t, int64_t* padded_b);
+/* run the context's device work on a caller-owned cudaStream_t (NULL restores
+ * the context's own stream), so callers can time it with their own events */
+int tinv_set_stream(tinv_ctx* ctx, void* cuda_stream);
 
 /* dense row-major matrices (leading dimension lda >= n). `host` variants take
  * host pointers (pinned memory is faster, pageable works); `device` variants

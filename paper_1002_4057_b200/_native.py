@@ -23,7 +23,7 @@ DENSE_LOWER, DENSE_SYMMETRIZE = 0, 1
 # every symbol include/tileinv_b200.h declares
 EXPORTS = (
     "tinv_abi_version", "tinv_device_count", "tinv_last_error", "tinv_create", "tinv_destroy",
-    "tinv_shape", "tinv_put_dense", "tinv_get_dense", "tinv_put_dense_device", "tinv_get_dense_device",
+    "tinv_shape", "tinv_set_stream", "tinv_put_dense", "tinv_get_dense", "tinv_put_dense_device", "tinv_get_dense_device",
     "tinv_put_tile", "tinv_get_tile", "tinv_gen_stream", "tinv_dag_edges", "tinv_plan_create",
     "tinv_plan_exec", "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
 )
@@ -67,6 +67,7 @@ def lib():
         "tinv_create": ([ctypes.POINTER(_P), _I64, _I64, ctypes.c_int], ctypes.c_int),
         "tinv_destroy": ([_P], ctypes.c_int),
         "tinv_shape": ([_P, _I64P, _I64P, _I64P, _I64P], ctypes.c_int),
+        "tinv_set_stream": ([_P, _P], ctypes.c_int),
         "tinv_put_dense": ([_P, _DP, _I64], ctypes.c_int),
         "tinv_get_dense": ([_P, _DP, _I64, ctypes.c_int], ctypes.c_int),
         "tinv_put_dense_device": ([_P, _P, _I64], ctypes.c_int),
@@ -174,6 +175,10 @@ class Context:
             self.close()
         except Exception:  # noqa: BLE001 - interpreter shutdown
             pass
+
+    def set_stream(self, stream_ptr):
+        """Launch on a caller-owned cudaStream_t (int handle); 0 -> own stream."""
+        check(lib().tinv_set_stream(self.h, ctypes.c_void_p(stream_ptr or None)), self.h)
 
     def put_dense(self, m):
         m = np.ascontiguousarray(m, dtype=np.float64)

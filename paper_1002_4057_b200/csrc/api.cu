@@ -35,7 +35,7 @@ static std::string g_err;
 struct tinv_ctx {
   int64_t n = 0, b = 0, t = 0, bp = 0, R = 0, T = 0;
   int device = 0, nsm = 0;
-  cudaStream_t st = nullptr, st2 = nullptr;
+  cudaStream_t st = nullptr, st2 = nullptr, own = nullptr;
   double* pool = nullptr;
   int64_t pool_slots = 0, slot_elems = 0;
   std::vector<int32_t> a_slot;  // current slot of each lower tile (home k or shadow T+k)
@@ -162,6 +162,7 @@ int tinv_create(tinv_ctx** out, int64_t n, int64_t b, int device) {
   if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(nullptr, TINV_ERR_CUDA, "stream create failed"));
+  c->own = c->st;
   c->a_slot.resize(c->T);
   for (int64_t k = 0; k < c->T; ++k) c->a_slot[k] = (int32_t)k;
   if (cudaMalloc(&c->d_a_slot, c->T * sizeof(int32_t)) != cudaSuccess)
@@ -183,9 +184,15 @@ int tinv_destroy(tinv_ctx* c) {
   if (c->d_a_slot) cudaFree(c->d_a_slot);
   for (auto& s : c->staging)
     if (s) cudaFree(s);
-  if (c->st) cudaStreamDestroy(c->st);
+  if (c->own) cudaStreamDestroy(c->own);
   if (c->st2) cudaStreamDestroy(c->st2);
   delete c;
+  return TINV_OK;
+}
+
+int tinv_set_stream(tinv_ctx* c, void* stream) {
+  if (!c) return TINV_ERR_BAD_ARG;
+  c->st = stream ? (cudaStream_t)stream : c->own;
   return TINV_OK;
 }
 
