@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -17,8 +18,8 @@
 #include "tinv_internal.h"
 
 namespace tinv {
-cudaError_t launch_exec(const CUtensorMap& tmK, const CUtensorMap& tmM, const ExecParams& P, int b, int grid,
-                        cudaStream_t stream);
+cudaError_t launch_exec(const CUtensorMap& tmK, const CUtensorMap& tmM, const CUtensorMap& tmE, const ExecParams& P,
+                        int b, int grid, cudaStream_t stream);
 cudaError_t launch_put(const double* src, int64_t lda, int64_t row0, double* pool, int64_t slot_elems,
                        const int32_t* slot_of, int b, int bp, int64_t tri_lo, int64_t ntiles, cudaStream_t st);
 cudaError_t launch_get(double* dst, int64_t ldd, int64_t row0, const double* pool, int64_t slot_elems,
@@ -42,7 +43,7 @@ struct tinv_ctx {
   int32_t* d_a_slot = nullptr;
   double* staging[2] = {nullptr, nullptr};
   size_t staging_bytes = 0;
-  CUtensorMap tmK, tmM;
+  CUtensorMap tmK, tmM, tmE;
   std::string err;
 };
 
@@ -82,13 +83,17 @@ static int make_maps(tinv_ctx* c) {
   cuuint32_t estr[3] = {1, 1, 1};
   cuuint32_t boxK[3] = {KCH, BLK, 1};  // 16 doubles (128 B) x 128 rows
   cuuint32_t boxM[3] = {16, KCH, 1};   // 16 doubles x 16 rows
+  cuuint32_t boxE[3] = {16, 64, 1};    // epilogue: 16 doubles x 64 rows
   CUresult r1 = fn(&c->tmK, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->pool, dims, strides, boxK, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   CUresult r2 = fn(&c->tmM, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->pool, dims, strides, boxM, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS)
+  CUresult r3 = fn(&c->tmE, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->pool, dims, strides, boxE, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS || r3 != CUDA_SUCCESS)
     return fail(c, TINV_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r1) + "/" + std::to_string(r2));
   return TINV_OK;
 }
@@ -566,6 +571,7 @@ struct tinv_plan {
   unsigned long long *d_ts = nullptr, *d_te = nullptr;
   int32_t* d_tsm = nullptr;
   int32_t *d_snap_from = nullptr, *d_snap_to = nullptr;
+  unsigned long long* d_phase = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<unsigned long long> h_ts, h_te;
   std::vector<int32_t> h_tsm;
@@ -631,7 +637,7 @@ int tinv_plan_destroy(tinv_plan* p) {
   cudaSetDevice(p->ctx->device);
   void* ptrs[] = {p->d_tasks, p->d_succ, p->d_indeg, p->d_done, p->d_cur,      p->d_alt,       p->d_queue, p->d_head,
                   p->d_tail,  p->d_ctr,  p->d_err,   p->d_progress, p->d_ts, p->d_te, p->d_tsm, p->d_snap_from,
-                  p->d_snap_to};
+                  p->d_snap_to, p->d_phase};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->ev0) cudaEventDestroy(p->ev0);
@@ -963,8 +969,13 @@ int tinv_plan_exec(tinv_plan* p, tinv_err* err, double* ms) {
   P.trace_end = p->d_te;
   P.trace_sm = p->d_tsm;
   P.t0 = 0;
+  if (getenv("TINV_PHASE_PROFILE")) {
+    if (!p->d_phase) CK(c, cudaMalloc(&p->d_phase, (size_t)c->nsm * NPHASE * 8));
+    CK(c, cudaMemsetAsync(p->d_phase, 0, (size_t)c->nsm * NPHASE * 8, st));
+    P.phase = p->d_phase;
+  }
   CK(c, cudaEventRecord(p->ev0, st));
-  CK(c, launch_exec(c->tmK, c->tmM, P, (int)c->b, c->nsm, st));
+  CK(c, launch_exec(c->tmK, c->tmM, c->tmE, P, (int)c->b, c->nsm, st));
   CK(c, cudaEventRecord(p->ev1, st));
   CK(c, cudaStreamSynchronize(st));
   if (ms) {
@@ -983,6 +994,19 @@ int tinv_plan_exec(tinv_plan* p, tinv_err* err, double* ms) {
     CK(c, cudaMemcpy(p->h_ts.data(), p->d_ts, nx * 8, cudaMemcpyDeviceToHost));
     CK(c, cudaMemcpy(p->h_te.data(), p->d_te, nx * 8, cudaMemcpyDeviceToHost));
     CK(c, cudaMemcpy(p->h_tsm.data(), p->d_tsm, nx * 4, cudaMemcpyDeviceToHost));
+  }
+  if (p->d_phase) {
+    std::vector<unsigned long long> ph((size_t)c->nsm * NPHASE);
+    CK(c, cudaMemcpy(ph.data(), p->d_phase, ph.size() * 8, cudaMemcpyDeviceToHost));
+    double tot[NPHASE] = {0};
+    for (int x = 0; x < c->nsm; ++x)
+      for (int k = 0; k < NPHASE; ++k) tot[k] += (double)ph[x * NPHASE + k];
+    const double items = tot[6] > 0 ? tot[6] : 1;
+    fprintf(stderr,
+            "[tinv phase] per item (cycles): item-wait %.0f mainloop %.0f epilogue %.0f job-end %.0f item-end %.0f "
+            "completion %.0f | items %.0f jobs %.0f\n",
+            tot[0] / items, tot[1] / items, tot[2] / items, tot[3] / items, tot[4] / items, tot[5] / items, tot[6],
+            tot[7]);
   }
   if (ekey != ~0ull || ctr_out[0] != 0) {
     if (keep) {

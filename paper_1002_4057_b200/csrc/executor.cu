@@ -65,6 +65,24 @@ __device__ __forceinline__ void tma_prefetch3(const CUtensorMap* map, int x, int
                "r"(x), "r"(y), "r"(z)
                : "memory");
 }
+__device__ __forceinline__ void tma_store3(const CUtensorMap* map, const void* src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+// global += smem (FP64 add performed by the TMA unit; verified exact on B200,
+// tools/tma_f64_reduce_test.cu)
+__device__ __forceinline__ void tma_reduce_add3(const CUtensorMap* map, const void* src, int x, int y, int z) {
+  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void cons_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -467,8 +485,9 @@ __device__ __forceinline__ int out_col(int wn, int q, int j) {
   return 32 * wn + 16 * (q >> 1) + 2 * rho(j) + (q & 1);
 }
 
-template <int V>
-__device__ __forceinline__ void run_gemm(const Job& jb, const ExecParams& P, SmemCtl& ctl, char* ring, unsigned& ks) {
+template <int V, typename Tick>
+__device__ __forceinline__ void run_gemm(const Job& jb, const ExecParams& P, SmemCtl& ctl, char* ring, unsigned& ks,
+                                         Tick& tick, const CUtensorMap* tmE) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp & 1, wn = warp >> 1, g = lane >> 2, tg = lane & 3;
   double acc[8][4][2];
@@ -498,37 +517,80 @@ __device__ __forceinline__ void run_gemm(const Job& jb, const ExecParams& P, Sme
     }
   }
 
-  // epilogue: out = [C +] sign * acc ; mirror -> also the transposed block
+  tick(1);
+  const double sg = (double)jb.sign;
+  if (!jb.mirror && (jb.c_s < 0 || jb.c_s == jb.o_s)) {
+    // TMA epilogue: stage sign*acc (64 rows at a time, 128B-swizzled boxes of
+    // 16 cols x 64 rows) in the spare 64 KB, then one thread stores it -- or,
+    // for C += sign*acc, reduce-adds it -- with cp.(reduce.)async.bulk.tensor.
+    char* stg = ring + NSTAGE * STAGE_BYTES;
+    const bool red = jb.c_s >= 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (wm == h) {
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          const int r = out_row<V>(wm, p, g) - 64 * h;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int c = out_col<V>(wn, q, 2 * tg + e);
+              *reinterpret_cast<double*>(stg + (c >> 4) * 8192 + r * 128 + ((((c & 15) >> 1) ^ (r & 7)) << 4) +
+                                         (c & 1) * 8) = sg * acc[p][q][e];
+            }
+        }
+      }
+      fence_proxy_async_smem();
+      cons_bar();
+      if (threadIdx.x == 0) {
+        for (int q = 0; q < 8; ++q) {
+          if (red)
+            tma_reduce_add3(tmE, stg + q * 8192, jb.o_c * BLK + 16 * q, jb.o_r * BLK + 64 * h, jb.o_s);
+          else
+            tma_store3(tmE, stg + q * 8192, jb.o_c * BLK + 16 * q, jb.o_r * BLK + 64 * h, jb.o_s);
+        }
+        bulk_commit();
+        bulk_wait_read();
+      }
+      cons_bar();
+    }
+    if (threadIdx.x == 0) bulk_wait_all();  // writes performed before the job is reported done
+    return;
+  }
+  // general epilogue: out = [C +] sign * acc ; mirror -> also the transposed block
   const int64_t bp = P.bp;
   double* O = P.pool + (int64_t)jb.o_s * P.slot_elems + (int64_t)jb.o_r * BLK * bp + jb.o_c * BLK;
   double* OT = P.pool + (int64_t)jb.o_s * P.slot_elems + (int64_t)jb.o_c * BLK * bp + jb.o_r * BLK;
   const double* C =
       jb.c_s >= 0 ? P.pool + (int64_t)jb.c_s * P.slot_elems + (int64_t)jb.o_r * BLK * bp + jb.o_c * BLK : nullptr;
   const bool diag = jb.o_r == jb.o_c;
-  const double sg = (double)jb.sign;
+  // pass 1: v = [C +] sign * acc, all C loads independent of any store
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
     const int r = out_row<V>(wm, p, g);
-    double cv[4][2];
-    if (C) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int c = out_col<V>(wn, q, 2 * tg + e);
-          cv[q][e] = (jb.mirror && diag && c > r) ? 0.0 : __ldcg(C + r * bp + c);
-        }
-    }
+      for (int e = 0; e < 2; ++e) {
+        const int c = out_col<V>(wn, q, 2 * tg + e);
+        double v = sg * acc[p][q][e];
+        if (C && !(jb.mirror && diag && c > r)) v += __ldcg(C + r * bp + c);
+        acc[p][q][e] = v;
+      }
+  }
+  // pass 2: stores (and the transposed copy for symmetric outputs)
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int r = out_row<V>(wm, p, g);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = out_col<V>(wn, q, 2 * tg + e);
         if (jb.mirror && diag && c > r) continue;
-        double v = sg * acc[p][q][e];
-        if (C) v = cv[q][e] + v;
-        O[r * bp + c] = v;
-        if (jb.mirror && !(diag && c == r)) OT[c * bp + r] = v;
+        O[r * bp + c] = acc[p][q][e];
+        if (jb.mirror && !(diag && c == r)) OT[c * bp + r] = acc[p][q][e];
       }
   }
 }
@@ -789,11 +851,13 @@ __device__ void complete_item(const ExecParams& P, const ItemInfo& it, SmemCtl& 
 
 // ---------------------------------------------------------------- the kernel
 __global__ void __launch_bounds__(NTHREADS, 1)
-    exec_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmM, ExecParams P,
-                int b) {
+    exec_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmM,
+                const __grid_constant__ CUtensorMap tmE, ExecParams P, int b) {
   extern __shared__ __align__(1024) char dsmem[];
   __shared__ SmemCtl ctl;
-  char* ring = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(dsmem) + 1023) & ~uintptr_t(1023));
+  // keep the pointer derived from the __shared__ array (arithmetic through an
+  // integer would lose the address space and turn LDS into generic LD)
+  char* ring = dsmem + ((1024u - (smem_u32(dsmem) & 1023u)) & 1023u);
   double* S = reinterpret_cast<double*>(ring);  // diagonal phases reuse the drained ring (+ extra)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int R = P.R;
@@ -821,6 +885,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (warp != NCONS_WARPS || lane != 0) return;
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmM)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmE)) : "memory");
     unsigned ks = 0, issued = 0;
     for (unsigned itn = 0;; ++itn) {
       const int slot = itn & 1;
@@ -897,9 +962,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // ============================ consumer warps
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONS_REGS));
   unsigned ks = 0, jobs = 0;
+  unsigned long long ph[NPHASE] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tc = clock64();
+  auto tick = [&](int k) {
+    const long long now = clock64();
+    ph[k] += (unsigned long long)(now - tc);
+    tc = now;
+  };
   for (unsigned itn = 0;; ++itn) {
     const int slot = itn & 1;
     mbar_wait(&ctl.item_full[slot], (itn >> 1) & 1);
+    tick(0);
     const ItemInfo it = ctl.items[slot];
     __syncwarp();
     if (lane == 0) mbar_arrive(&ctl.item_empty[slot]);
@@ -911,36 +984,44 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (jb.type == J_SPECIAL) {
         run_special(jb, it, P, ctl, S, b);
       } else if (jb.variant == V_NT) {
-        run_gemm<V_NT>(jb, P, ctl, ring, ks);
+        run_gemm<V_NT>(jb, P, ctl, ring, ks, tick, &tmE);
       } else if (jb.variant == V_NN) {
-        run_gemm<V_NN>(jb, P, ctl, ring, ks);
+        run_gemm<V_NN>(jb, P, ctl, ring, ks, tick, &tmE);
       } else {
-        run_gemm<V_TN>(jb, P, ctl, ring, ks);
+        run_gemm<V_TN>(jb, P, ctl, ring, ks, tick, &tmE);
       }
+      tick(2);
       fence_proxy_async();
       cons_bar();
       ++jobs;
       if (tid == 0) st_release_cta_u32(&ctl.jobs_done, jobs);
+      tick(3);
     }
     __threadfence();
     cons_bar();
+    tick(4);
     if (warp == 0) complete_item(P, it, ctl);
     cons_bar();
+    tick(5);
+    ph[6] += 1;
+    ph[7] += it.njobs;
     if (tid == 0) {
       ctl.fail_code = 0;
       ctl.fail_index = -1;
     }
   }
+  if (P.phase && tid == 0)
+    for (int k = 0; k < NPHASE; ++k) P.phase[blockIdx.x * NPHASE + k] = ph[k];
 }
 
 // ---------------------------------------------------------------- host launch
 int exec_smem_bytes() { return SMEM_BYTES; }
 
-cudaError_t launch_exec(const CUtensorMap& tmK, const CUtensorMap& tmM, const ExecParams& P, int b, int grid,
-                        cudaStream_t stream) {
+cudaError_t launch_exec(const CUtensorMap& tmK, const CUtensorMap& tmM, const CUtensorMap& tmE, const ExecParams& P,
+                        int b, int grid, cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  exec_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(tmK, tmM, P, b);
+  exec_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(tmK, tmM, tmE, P, b);
   return cudaGetLastError();
 }
 

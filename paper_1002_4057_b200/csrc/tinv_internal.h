@@ -73,7 +73,9 @@ struct ExecParams {
   unsigned long long* trace_end;
   int32_t* trace_sm;
   unsigned long long t0;           // globaltimer at launch (trace base)
+  unsigned long long* phase;       // optional per-CTA phase cycle counters (NPHASE each)
 };
+constexpr int NPHASE = 8;  // item-wait, mainloop, epilogue, job-end, item-end, completion, items, jobs
 
 inline int64_t tri_index(int64_t i, int64_t j) { return i * (i + 1) / 2 + j; }
 
