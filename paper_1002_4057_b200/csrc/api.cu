@@ -83,7 +83,7 @@ static int make_maps(tinv_ctx* c) {
   cuuint32_t estr[3] = {1, 1, 1};
   cuuint32_t boxK[3] = {KCH, BLK, 1};  // 16 doubles (128 B) x 128 rows
   cuuint32_t boxM[3] = {16, KCH, 1};   // 16 doubles x 16 rows
-  cuuint32_t boxE[3] = {16, 64, 1};    // epilogue: 16 doubles x 64 rows
+  cuuint32_t boxE[3] = {16, 32, 1};    // epilogue: 16 doubles x 32 rows
   CUresult r1 = fn(&c->tmK, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->pool, dims, strides, boxK, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -356,12 +356,23 @@ __device__ void get_job(const ItemInfo& it, int n, int R, Job& j) {
 }
 
 // ---------------------------------------------------------------- smem
+// consumer -> storer hand-off records
+enum RecType : int32_t { R_QUARTER = 0, R_JOB_END = 1, R_ITEM_END = 2, R_EXIT = 3 };
+struct Rec {
+  int32_t type, a, b, c, d, e, f, g;
+};
+constexpr int NREC = 16;
+
 struct SmemCtl {
   uint64_t full[NSTAGE];
   uint64_t empty[NSTAGE];
   uint64_t item_full[2];
   uint64_t item_empty[2];
+  uint64_t rec_full[NREC];
+  uint64_t rec_empty[NREC];
+  uint64_t stg_free[2];
   ItemInfo items[2];
+  Rec recs[NREC];
   unsigned jobs_done;
   int fail_code;   // per item: 0 none
   int fail_index;
@@ -485,9 +496,35 @@ __device__ __forceinline__ int out_col(int wn, int q, int j) {
   return 32 * wn + 16 * (q >> 1) + 2 * rho(j) + (q & 1);
 }
 
+struct EpiState {
+  unsigned rec;    // next hand-off record index (identical in every consumer thread)
+  unsigned tjobs;  // TMA-epilogue jobs so far (staging buffer phases)
+  unsigned jobs;   // jobs so far (published as jobs_done by the storer)
+  int generic;     // this job / item wrote global memory with generic stores
+};
+
+__device__ __forceinline__ void push_rec(SmemCtl& ctl, unsigned idx, Rec r) {
+  const int s = idx % NREC;
+  mbar_wait(&ctl.rec_empty[s], ((idx / NREC) & 1) ^ 1);
+  ctl.recs[s] = r;
+  mbar_arrive(&ctl.rec_full[s]);
+}
+
+// Before a diagonal phase: every earlier job of this CTA has been retired by
+// the storer (its TMA writes performed, its staged quarters read), so global
+// reads see them and the staging area can serve as scratch.
+__device__ __forceinline__ void drain_jobs(SmemCtl& ctl, const EpiState& es) {
+  cons_bar();
+  if (threadIdx.x == 0)
+    while (ld_acquire_cta_u32(&ctl.jobs_done) < es.jobs) {
+    }
+  cons_bar();
+  fence_proxy_async();
+}
+
 template <int V, typename Tick>
 __device__ __forceinline__ void run_gemm(const Job& jb, const ExecParams& P, SmemCtl& ctl, char* ring, unsigned& ks,
-                                         Tick& tick, const CUtensorMap* tmE) {
+                                         Tick& tick, EpiState& es) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp & 1, wn = warp >> 1, g = lane >> 2, tg = lane & 3;
   double acc[8][4][2];
@@ -520,44 +557,44 @@ __device__ __forceinline__ void run_gemm(const Job& jb, const ExecParams& P, Sme
   tick(1);
   const double sg = (double)jb.sign;
   if (!jb.mirror && (jb.c_s < 0 || jb.c_s == jb.o_s)) {
-    // TMA epilogue: stage sign*acc (64 rows at a time, 128B-swizzled boxes of
-    // 16 cols x 64 rows) in the spare 64 KB, then one thread stores it -- or,
-    // for C += sign*acc, reduce-adds it -- with cp.(reduce.)async.bulk.tensor.
+    // TMA epilogue: sign*acc staged 32 rows at a time (quarter k = rows
+    // 32k..32k+31, written by the 4 warps owning them) into two alternating
+    // 32 KB buffers of 128B-swizzled {16 cols x 32 rows} boxes; the storer
+    // warp stores -- or for C += sign*acc reduce-adds -- each quarter with
+    // cp.(reduce.)async.bulk.tensor while the consumers move on.
     char* stg = ring + NSTAGE * STAGE_BYTES;
-    const bool red = jb.c_s >= 0;
+    const int red = jb.c_s >= 0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (wm == h) {
+    for (int k = 0; k < 4; ++k) {
+      if (wm == (k >> 1)) {
+        const int buf = k & 1;
+        const unsigned use = 2 * es.tjobs + (k >> 1);
+        mbar_wait(&ctl.stg_free[buf], (use & 1) ^ 1);
+        char* sb = stg + buf * 32768;
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
-          const int r = out_row<V>(wm, p, g) - 64 * h;
+        for (int pp = 0; pp < 4; ++pp) {
+          const int p = 4 * (k & 1) + pp;
+          const int r = out_row<V>(wm, p, g) - 32 * k;
 #pragma unroll
           for (int q = 0; q < 4; ++q)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int c = out_col<V>(wn, q, 2 * tg + e);
-              *reinterpret_cast<double*>(stg + (c >> 4) * 8192 + r * 128 + ((((c & 15) >> 1) ^ (r & 7)) << 4) +
+              *reinterpret_cast<double*>(sb + (c >> 4) * 4096 + r * 128 + ((((c & 15) >> 1) ^ (r & 7)) << 4) +
                                          (c & 1) * 8) = sg * acc[p][q][e];
             }
         }
+        fence_proxy_async_smem();
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + wm) : "memory");
+        if (warp == wm && lane == 0)
+          push_rec(ctl, es.rec + k, Rec{R_QUARTER, buf, jb.o_c * BLK, jb.o_r * BLK + 32 * k, jb.o_s, red, 0, 0});
       }
-      fence_proxy_async_smem();
-      cons_bar();
-      if (threadIdx.x == 0) {
-        for (int q = 0; q < 8; ++q) {
-          if (red)
-            tma_reduce_add3(tmE, stg + q * 8192, jb.o_c * BLK + 16 * q, jb.o_r * BLK + 64 * h, jb.o_s);
-          else
-            tma_store3(tmE, stg + q * 8192, jb.o_c * BLK + 16 * q, jb.o_r * BLK + 64 * h, jb.o_s);
-        }
-        bulk_commit();
-        bulk_wait_read();
-      }
-      cons_bar();
     }
-    if (threadIdx.x == 0) bulk_wait_all();  // writes performed before the job is reported done
+    es.rec += 4;
+    es.tjobs += 1;
     return;
   }
+  es.generic = 1;
   // general epilogue: out = [C +] sign * acc ; mirror -> also the transposed block
   const int64_t bp = P.bp;
   double* O = P.pool + (int64_t)jb.o_s * P.slot_elems + (int64_t)jb.o_r * BLK * bp + jb.o_c * BLK;
@@ -803,30 +840,32 @@ __device__ unsigned long long pop_item(const ExecParams& P) {
   }
 }
 
-__device__ void complete_item(const ExecParams& P, const ItemInfo& it, SmemCtl& ctl) {
-  // warp 0 of the consumers; all consumer threads fenced their stores already
+// Storer warp: completion of one work item (all its writes are performed and
+// visible). Last item of a task: swap rename slots, release successors.
+__device__ void complete_item(const ExecParams& P, const Rec& r) {
+  const int task = r.a, nitems = r.b, ref_id = r.c, fail_code = r.d, fail_index = r.e;
   const int lane = threadIdx.x & 31;
   int last = 0;
   if (lane == 0) {
-    if (ctl.fail_code) {
-      const unsigned long long key = ((unsigned long long)(unsigned)it.ref_id << 32) |
-                                     ((unsigned long long)ctl.fail_code << 24) |
-                                     (unsigned long long)(ctl.fail_index & 0xffffff);
+    if (fail_code) {
+      const unsigned long long key = ((unsigned long long)(unsigned)ref_id << 32) |
+                                     ((unsigned long long)fail_code << 24) |
+                                     (unsigned long long)(fail_index & 0xffffff);
       atomicMin(P.err, key);
       atomicExch(P.abort_flag, 1);
     } else {
-      const int old = atomicAdd(P.done + it.task, 1);
-      last = (old == it.nitems - 1);
+      const int old = atomicAdd(P.done + task, 1);
+      last = (old == nitems - 1);
       if (last) {
-        const TaskDev& t = P.tasks[it.task];
+        const TaskDev& t = P.tasks[task];
         if (t.flags & TF_RENAMED) {
           const int cs = __ldcg(P.cur_slot + t.out);
           P.cur_slot[t.out] = __ldcg(P.alt_slot + t.out);
           P.alt_slot[t.out] = cs;
         }
         if (P.trace_end) {
-          atomicMax(P.trace_end + it.task, globaltimer() - P.t0);
-          P.trace_sm[it.task] = (int)smid();
+          atomicMax(P.trace_end + task, globaltimer() - P.t0);
+          P.trace_sm[task] = (int)smid();
         }
         __threadfence();
       }
@@ -835,7 +874,7 @@ __device__ void complete_item(const ExecParams& P, const ItemInfo& it, SmemCtl& 
   last = __shfl_sync(0xffffffffu, last, 0);
   if (last) {
     __syncwarp();
-    const TaskDev& t = P.tasks[it.task];
+    const TaskDev& t = P.tasks[task];
     for (int k = t.succ_begin + lane; k < t.succ_end; k += 32) {
       const int s = P.succ[k];
       if (atomicSub(P.indeg + s, 1) == 1) push_task(P, s);
@@ -870,6 +909,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&ctl.item_full[s], 1);
       mbar_init(&ctl.item_empty[s], NCONS_WARPS);
+      mbar_init(&ctl.stg_free[s], 1);
+    }
+    for (int s = 0; s < NREC; ++s) {
+      mbar_init(&ctl.rec_full[s], 1);
+      mbar_init(&ctl.rec_empty[s], 1);
     }
     ctl.jobs_done = 0;
     ctl.fail_code = 0;
@@ -882,6 +926,43 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp >= NCONS_WARPS) {
     // ============================ producer / scheduler warp
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PROD_REGS));
+    if (warp == NCONS_WARPS + 1) {
+      // ============================ storer warp: epilogue TMA + completion
+      for (unsigned idx = 0;; ++idx) {
+        const int s = idx % NREC;
+        mbar_wait(&ctl.rec_full[s], (idx / NREC) & 1);
+        const Rec r = ctl.recs[s];
+        __syncwarp();
+        if (r.type == R_EXIT) break;
+        if (r.type == R_QUARTER) {
+          if (lane == 0) {
+            char* sb = ring + NSTAGE * STAGE_BYTES + r.a * 32768;
+            for (int q = 0; q < 8; ++q) {
+              if (r.e)
+                tma_reduce_add3(&tmE, sb + q * 4096, r.b + 16 * q, r.c, r.d);
+              else
+                tma_store3(&tmE, sb + q * 4096, r.b + 16 * q, r.c, r.d);
+            }
+            bulk_commit();
+            bulk_wait_read();
+            mbar_arrive(&ctl.stg_free[r.a]);
+          }
+        } else if (r.type == R_JOB_END) {
+          if (lane == 0) {
+            bulk_wait_all();
+            fence_proxy_async();
+            st_release_cta_u32(&ctl.jobs_done, (unsigned)r.a);
+          }
+        } else {
+          if (lane == 0) __threadfence();
+          __syncwarp();
+          complete_item(P, r);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ctl.rec_empty[s]);
+      }
+      return;
+    }
     if (warp != NCONS_WARPS || lane != 0) return;
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmM)) : "memory");
@@ -961,7 +1042,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   // ============================ consumer warps
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONS_REGS));
-  unsigned ks = 0, jobs = 0;
+  unsigned ks = 0;
+  EpiState es = {0u, 0u, 0u, 0};
   unsigned long long ph[NPHASE] = {0, 0, 0, 0, 0, 0, 0, 0};
   long long tc = clock64();
   auto tick = [&](int k) {
@@ -976,39 +1058,52 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const ItemInfo it = ctl.items[slot];
     __syncwarp();
     if (lane == 0) mbar_arrive(&ctl.item_empty[slot]);
-    if (it.task < 0) break;
+    if (it.task < 0) {
+      if (tid == 0) push_rec(ctl, es.rec, Rec{R_EXIT, 0, 0, 0, 0, 0, 0, 0});
+      break;
+    }
     if (tid == 0 && P.trace_start) atomicMin(P.trace_start + it.task, globaltimer() - P.t0);
+    int item_generic = 0;
     for (int jn = 0; jn < it.njobs; ++jn) {
       Job jb;
       get_job(it, jn, R, jb);
+      es.generic = 0;
       if (jb.type == J_SPECIAL) {
+        drain_jobs(ctl, es);
         run_special(jb, it, P, ctl, S, b);
+        es.generic = 1;
       } else if (jb.variant == V_NT) {
-        run_gemm<V_NT>(jb, P, ctl, ring, ks, tick, &tmE);
+        run_gemm<V_NT>(jb, P, ctl, ring, ks, tick, es);
       } else if (jb.variant == V_NN) {
-        run_gemm<V_NN>(jb, P, ctl, ring, ks, tick, &tmE);
+        run_gemm<V_NN>(jb, P, ctl, ring, ks, tick, es);
       } else {
-        run_gemm<V_TN>(jb, P, ctl, ring, ks, tick, &tmE);
+        run_gemm<V_TN>(jb, P, ctl, ring, ks, tick, es);
       }
       tick(2);
-      fence_proxy_async();
-      cons_bar();
-      ++jobs;
-      if (tid == 0) st_release_cta_u32(&ctl.jobs_done, jobs);
+      ++es.jobs;
+      if (es.generic) {  // generic global writes: visible to the async proxy before the job is done
+        fence_proxy_async();
+        cons_bar();
+        item_generic = 1;
+      }
+      if (tid == 0) push_rec(ctl, es.rec, Rec{R_JOB_END, (int)es.jobs, 0, 0, 0, 0, 0, 0});
+      es.rec += 1;
       tick(3);
     }
-    __threadfence();
-    cons_bar();
+    if (item_generic) {
+      __threadfence();
+      cons_bar();
+    }
     tick(4);
-    if (warp == 0) complete_item(P, it, ctl);
-    cons_bar();
-    tick(5);
-    ph[6] += 1;
-    ph[7] += it.njobs;
     if (tid == 0) {
+      push_rec(ctl, es.rec, Rec{R_ITEM_END, it.task, it.nitems, it.ref_id, ctl.fail_code, ctl.fail_index, 0, 0});
       ctl.fail_code = 0;
       ctl.fail_index = -1;
     }
+    es.rec += 1;
+    tick(5);
+    ph[6] += 1;
+    ph[7] += it.njobs;
   }
   if (P.phase && tid == 0)
     for (int k = 0; k < NPHASE; ++k) P.phase[blockIdx.x * NPHASE + k] = ph[k];
