@@ -513,23 +513,6 @@ int expected_reads(int kind) {
   }
 }
 
-int items_of(int kind, int R) {
-  switch (kind) {
-    case TINV_SYRK_SUB:
-    case TINV_SYRK_ADD_T:
-    case TINV_LAUUM:
-      return R * (R + 1) / 2;
-    case TINV_POTRF:
-    case TINV_TRTRI:
-    case KIND_INV:
-      return 1;
-    case TINV_COPY:
-      return R;
-    default:
-      return R * R;
-  }
-}
-
 double weight_of(int kind) {  // flops in units of b^3 (SURVEY.md §7 hard part 2)
   switch (kind) {
     case TINV_POTRF:
@@ -745,6 +728,11 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
       }
       in0 = aux;
     }
+    if (kind == TINV_POTRF) {  // private aux tile: inverses of the diagonal blocks of L
+      in0 = (int32_t)next_logical++;
+      written_dyn.push_back(1);
+      last_writer_exec.resize(next_logical, -1);
+    }
     if (o >= T) written_dyn[o - T] = 1;
     last_writer_exec[o] = (int32_t)xs.size();
     xs.push_back({kind, f[F_STEP], o, in0, in1, f[F_OM] == 2 ? 2 : 1, (int)v});
@@ -758,7 +746,7 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
   {
     std::vector<std::vector<Acc>> acc(nx);
     for (int64_t v = 0; v < nx; ++v) {
-      if (xs[v].in0 >= 0) acc[v].push_back({xs[v].in0, 0});
+      if (xs[v].in0 >= 0 && xs[v].kind != TINV_POTRF) acc[v].push_back({xs[v].in0, 0});
       if (xs[v].in1 >= 0) acc[v].push_back({xs[v].in1, 0});
       acc[v].push_back({xs[v].out, xs[v].mode});
     }
@@ -816,11 +804,13 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
     d.in0 = x.in0;
     d.in1 = x.in1;
     d.ref_id = x.ref;
-    d.nitems = items_of(x.kind, R);
+    d.nitems = total_items(x.kind, R);
+    d.nphases = (int16_t)phases_of(x.kind, R);
+    d.pad = 0;
     d.flags = 0;
     const bool alias = (x.in0 == x.out || x.in1 == x.out);
     if (x.kind == TINV_TRMM_LEFT || x.kind == TINV_TRMM_RIGHT_NEG || x.kind == TINV_TRMM_LEFT_T ||
-        x.kind == TINV_LAUUM || x.kind == TINV_TRSM ||
+        x.kind == TINV_LAUUM || x.kind == TINV_TRSM || x.kind == TINV_TRTRI ||
         (alias && (x.kind == TINV_GEMM || x.kind == TINV_SYRK_SUB || x.kind == TINV_SYRK_ADD_T))) {
       d.flags |= TF_RENAMED;
       renamed_tile[x.out] = 1;
@@ -839,7 +829,7 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
   for (int64_t u = 0; u < nx; ++u)
     if (p->indeg0[u] == 0) {
       const TaskDev& d = p->tasks[u];
-      for (int i = 0; i < d.nitems; ++i)
+      for (int i = 0; i < phase_items(d.kind, R, 0); ++i)
         p->q_init[p->q_off[d.level] + p->tail0[d.level]++] = ((unsigned long long)(u + 1) << 32) | (unsigned)i;
     }
 
@@ -1004,9 +994,11 @@ int tinv_plan_exec(tinv_plan* p, tinv_err* err, double* ms) {
     const double items = tot[6] > 0 ? tot[6] : 1;
     fprintf(stderr,
             "[tinv phase] per item (cycles): item-wait %.0f mainloop %.0f epilogue %.0f job-end %.0f item-end %.0f "
-            "completion %.0f | items %.0f jobs %.0f\n",
+            "completion %.0f | items %.0f jobs %.0f | special totals: load %.0f factor %.0f inverse %.0f store %.0f\n",
             tot[0] / items, tot[1] / items, tot[2] / items, tot[3] / items, tot[4] / items, tot[5] / items, tot[6],
-            tot[7]);
+            tot[7], tot[8], tot[9], tot[10], tot[11]);
+    fprintf(stderr, "[tinv phase] potrf factor %.0f subst %.0f trailing %.0f | trtri base %.0f l16 %.0f l32 %.0f l64 %.0f\n",
+            tot[12], tot[13], tot[14], tot[15], tot[16], tot[17], tot[18]);
   }
   if (ekey != ~0ull || ctr_out[0] != 0) {
     if (keep) {

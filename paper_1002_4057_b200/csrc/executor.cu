@@ -134,20 +134,21 @@ __device__ __forceinline__ int rho(int x) { return (x >> 1) | ((x & 1) << 2); }
 // ---------------------------------------------------------------- jobs
 enum Variant : int8_t { V_NT = 0, V_NN = 1, V_TN = 2 };
 enum JobType : int8_t { J_GEMM = 0, J_SPECIAL = 1 };
-enum Special : int8_t { SP_POTRF_DIAG = 0, SP_TRTRI_DIAG = 1, SP_INV_INIT = 2, SP_COPY_ROWS = 3 };
+enum Special : int8_t { SP_BPOTRF = 0, SP_BTRTRI = 1, SP_COPY_ROWS = 2 };
 
 struct ItemInfo {
-  int32_t task, item, kind, step;
+  int32_t task, item, phase, kind, step;
   int32_t out_s, alt_s, in0_s, in1_s, scr_s;
-  int32_t ref_id, nitems, njobs, flags, pad;
+  int32_t ref_id, nitems, njobs, flags;
 };
 
 struct Job {
   int8_t type, variant, special, mirror, dep, sign;
-  int16_t d;     // special parameter
+  int16_t d;  // special parameter (diagonal block)
   int32_t a_s, a_fix, a_k0, b_s, b_fix, b_k0;
   int32_t k0, k1, a_mask, b_mask;
   int32_t o_s, o_r, o_c, c_s;
+  int32_t src_s;  // special: source slot
 };
 
 __device__ __forceinline__ void lower_pair(int i, int& r, int& c) {
@@ -156,37 +157,10 @@ __device__ __forceinline__ void lower_pair(int i, int& r, int& c) {
   c = i - r * (r + 1) / 2;
 }
 
-__device__ __forceinline__ int item_count(int kind, int R) {
-  switch (kind) {
-    case TINV_SYRK_SUB:
-    case TINV_SYRK_ADD_T:
-    case TINV_LAUUM:
-      return R * (R + 1) / 2;
-    case TINV_POTRF:
-    case TINV_TRTRI:
-    case KIND_INV:
-      return 1;
-    case TINV_COPY:
-      return R;
-    default:
-      return R * R;
-  }
-}
-
-__device__ __forceinline__ int job_count(const ItemInfo& it, int R) {
-  switch (it.kind) {
-    case TINV_POTRF: {
-      int n = R;
-      for (int d = 0; d < R; ++d) n += (R - 1 - d) + (R - 1 - d) * (R - d) / 2;
-      return n;
-    }
-    case TINV_TRTRI:
-      return R + R * (R - 1);
-    case KIND_INV:
-      return 1 + R + R * (R - 1);
-    default:
-      return 1;
-  }
+// jobs of one work item: two for the off-diagonal items of TRTRI / INV
+// phases >= 1, one otherwise
+__device__ __forceinline__ int job_count(const ItemInfo& it) {
+  return ((it.kind == TINV_TRTRI || it.kind == KIND_INV) && it.phase > 0) ? 2 : 1;
 }
 
 __device__ __forceinline__ void gemm_job(Job& j, int8_t v, int a_s, int a_fix, int a_k0, int b_s, int b_fix,
@@ -213,90 +187,63 @@ __device__ __forceinline__ void gemm_job(Job& j, int8_t v, int a_s, int a_fix, i
   j.o_r = o_r;
   j.o_c = o_c;
   j.c_s = c_s;
+  j.src_s = -1;
 }
 
-__device__ __forceinline__ void special_job(Job& j, int8_t sp, int d) {
+__device__ __forceinline__ void special_job(Job& j, int8_t sp, int d, int src, int dst) {
   j.type = J_SPECIAL;
   j.special = sp;
   j.d = (int16_t)d;
   j.dep = 1;
-}
-
-// TRTRI job list (in place on slot s), shared by TRTRI and INV (offset by 1).
-//   for d = R-1 .. 0:  [diag inverse of block d]
-//     rows r = R-1 .. d+1:  A[r][d] <- sum_{k=d+1..r} X[r][k] L[k][d]
-//     rows r = R-1 .. d+1:  A[r][d] <- -A[r][d] X[d][d]
-__device__ __forceinline__ void trtri_job(int n, int s, int R, Job& j) {
-  for (int d = R - 1; d >= 0; --d) {
-    if (n == 0) {
-      special_job(j, SP_TRTRI_DIAG, d);
-      return;
-    }
-    n -= 1;
-    const int m = R - 1 - d;
-    if (n < m) {
-      const int r = R - 1 - n;
-      gemm_job(j, V_NN, s, r, d + 1, s, d, d + 1, d + 1, r + 1, s, r, d, -1, 1);
-      j.a_mask = r;
-      return;
-    }
-    n -= m;
-    if (n < m) {
-      const int r = R - 1 - n;
-      gemm_job(j, V_NN, s, r, d, s, d, d, d, d + 1, s, r, d, -1, -1);
-      j.b_mask = d;
-      j.dep = (n == 0);
-      return;
-    }
-    n -= m;
-  }
+  j.src_s = src;
+  j.o_s = dst;
 }
 
 __device__ void get_job(const ItemInfo& it, int n, int R, Job& j) {
   const int o = it.out_s, a = it.alt_s, x = it.in0_s, y = it.in1_s;
   const int kind = it.kind;
-  if (kind == TINV_POTRF) {
-    for (int d = 0; d < R; ++d) {
-      if (n == 0) {
-        special_job(j, SP_POTRF_DIAG, d);
+  if (kind == TINV_POTRF) {  // in place on o; inverses of the diagonal blocks kept in aux tile x
+    const int d = it.phase / 3;
+    switch (it.phase % 3) {
+      case 0:
+        special_job(j, SP_BPOTRF, d, x, o);
         return;
-      }
-      n -= 1;
-      const int m = R - 1 - d;
-      if (n < m) {  // panel solve A[r][d] <- A[r][d] inv(L_dd)^T
-        const int r = d + 1 + n;
-        gemm_job(j, V_NT, o, r, d, it.scr_s, 0, 0, d, d + 1, o, r, d, -1, 1);
+      case 1: {  // A[r][d] <- A[r][d] inv(L_dd)^T
+        const int r = d + 1 + it.item;
+        gemm_job(j, V_NT, o, r, d, x, d, d, d, d + 1, o, r, d, -1, 1);
         j.b_mask = d;
         return;
       }
-      n -= m;
-      const int u = m * (m + 1) / 2;
-      if (n < u) {  // trailing update A[r][c] -= A[r][d] A[c][d]^T, r >= c > d
+      default: {  // A[r][c] -= A[r][d] A[c][d]^T, r >= c > d
         int rr, cc;
-        lower_pair(n, rr, cc);
+        lower_pair(it.item, rr, cc);
         const int r = d + 1 + rr, c = d + 1 + cc;
         gemm_job(j, V_NT, o, r, d, o, c, d, d, d + 1, o, r, c, o, -1);
-        j.dep = (n == 0);
         return;
       }
-      n -= u;
     }
-    return;
   }
-  if (kind == TINV_TRTRI) {
-    trtri_job(n, o, R, j);
-    return;
-  }
-  if (kind == KIND_INV) {
-    if (n == 0) {
-      special_job(j, SP_INV_INIT, 0);
+  if (kind == TINV_TRTRI || kind == KIND_INV) {
+    // X = L^-1: source L in `src`, result in `dst` (TRTRI: renamed cur -> alt)
+    const int src = kind == KIND_INV ? x : o;
+    const int dst = kind == KIND_INV ? o : a;
+    if (it.phase == 0) {
+      special_job(j, SP_BTRTRI, it.item, src, dst);
       return;
     }
-    trtri_job(n - 1, o, R, j);
+    const int r = it.phase + it.item, d = r - it.phase;
+    if (n == 0) {  // X[r][d] <- sum_{k=d+1..r} X[r][k] L[k][d]
+      gemm_job(j, V_NN, dst, r, d + 1, src, d, d + 1, d + 1, r + 1, dst, r, d, -1, 1);
+      j.a_mask = r;
+    } else {  // X[r][d] <- -X[r][d] X[d][d]
+      gemm_job(j, V_NN, dst, r, d, dst, d, d, d, d + 1, dst, r, d, -1, -1);
+      j.b_mask = d;
+      j.dep = 1;
+    }
     return;
   }
   if (kind == TINV_COPY) {
-    special_job(j, SP_COPY_ROWS, it.item);
+    special_job(j, SP_COPY_ROWS, it.item, x, o);
     return;
   }
   int r, c;
@@ -377,7 +324,8 @@ struct SmemCtl {
   int fail_code;   // per item: 0 none
   int fail_index;
   int scan_min;
-  double pivot;
+  unsigned long long dbg[4];
+  unsigned long long dbg2[8];
 };
 
 // ---------------------------------------------------------------- consumers: DMMA chunk
@@ -633,100 +581,257 @@ __device__ __forceinline__ void run_gemm(const Job& jb, const ExecParams& P, Sme
 }
 
 // ---------------------------------------------------------------- consumers: diagonal phases
-// 128x128 block in shared memory, row stride 129 doubles (bank spread).
+// A 128x128 diagonal block in shared memory uses row stride 129 doubles.
 constexpr int SLD = BLK + 1;
 
-__device__ void load_block_lower(double* S, const double* src, int64_t bp) {
-  for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
-    const int i = e >> 7, j = e & 127;
-    S[i * SLD + j] = (j <= i) ? __ldcg(src + i * bp + j) : 0.0;
-  }
-}
 __device__ void store_block_lower(const double* S, double* dst, int64_t bp) {
   for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
     const int i = e >> 7, j = e & 127;
     dst[i * bp + j] = (j <= i) ? S[i * SLD + j] : 0.0;
   }
 }
-__device__ void zero_upper_blocks(double* tile, int R, int64_t bp) {
-  for (int r = 0; r < R; ++r)
-    for (int c = r + 1; c < R; ++c) {
-      double* blk = tile + (int64_t)r * BLK * bp + c * BLK;
-      for (int e = threadIdx.x; e < BLK * BLK / 2; e += 256) {
-        const int i = e >> 6, j = (e & 63) * 2;
-        *reinterpret_cast<double2*>(blk + i * bp + j) = make_double2(0.0, 0.0);
-      }
-    }
-}
-
-// unblocked right-looking Cholesky of the lower 128x128 block in S;
-// returns -1 or the first failing pivot (kernels.py:68-71 semantics)
-__device__ int small_potrf(double* S, SmemCtl& ctl) {
-  const int tid = threadIdx.x;
-  for (int k = 0; k < BLK; ++k) {
-    if (tid == 0) {
-      const double d = S[k * SLD + k];
-      if (!(d > 0.0) || !isfinite(d)) {
-        ctl.scan_min = k;
-      } else {
-        S[k * SLD + k] = sqrt(d);
-      }
-    }
-    cons_bar();
-    if (ctl.scan_min >= 0) return ctl.scan_min;
-    const double dk = S[k * SLD + k];
-    for (int i = k + 1 + tid; i < BLK; i += 256) S[i * SLD + k] = S[i * SLD + k] / dk;
-    cons_bar();
-    const int m = BLK - 1 - k;
-    for (int e = tid; e < m * m; e += 256) {
-      const int i = k + 1 + e / m, j = k + 1 + e % m;
-      if (j <= i) S[i * SLD + j] -= S[i * SLD + k] * S[j * SLD + k];
-    }
-    cons_bar();
-  }
-  return -1;
-}
-
-// in-place inverse of the lower-triangular 128x128 block in S (LAPACK trti2
-// order: columns right to left, X[i][j] = -X[j][j] sum_{k=j+1..i} X[i][k] L[k][j])
-__device__ void small_trtri(double* S) {
-  const int tid = threadIdx.x;
-  for (int j = BLK - 1; j >= 0; --j) {
-    if (tid == 0) S[j * SLD + j] = 1.0 / S[j * SLD + j];
-    cons_bar();
-    const double ajj = S[j * SLD + j];
-    const int row = j + 1 + (tid >> 1);
-    double part = 0.0;
-    if (row < BLK) {
-      for (int k = j + 1 + (tid & 1); k <= row; k += 2) part += S[row * SLD + k] * S[k * SLD + j];
-    }
-    part += __shfl_xor_sync(0xffffffffu, part, 1);
-    cons_bar();
-    if (row < BLK && (tid & 1) == 0) S[row * SLD + j] = -ajj * part;
-    cons_bar();
+// zero the blocks (d, c > d) of a tile (upper part of block row d)
+__device__ void zero_upper_row(double* tile, int d, int R, int64_t bp) {
+  const int w = (R - 1 - d) * BLK;  // doubles per row to clear
+  if (w <= 0) return;
+  double* base = tile + (int64_t)d * BLK * bp + (d + 1) * BLK;
+  for (int e = threadIdx.x; e < BLK * w / 2; e += 256) {
+    const int i = e / (w / 2), j = (e % (w / 2)) * 2;
+    *reinterpret_cast<double2*>(base + i * bp + j) = make_double2(0.0, 0.0);
   }
 }
 
-__device__ void scan_zero_diag(const double* tile, int b, int64_t bp, SmemCtl& ctl) {
-  for (int i = threadIdx.x; i < b; i += 256)
-    if (__ldcg(tile + (int64_t)i * bp + i) == 0.0) atomicMin(&ctl.scan_min, i);
+// ---- 128x128 diagonal-block kernels on S (shared, row stride SLD), blocked
+// over 16x16 sub-blocks: warp-shuffle factor / inverse of a 16x16 lower
+// sub-block (lane i&15 holds row i), 4x4 register micro-tiles for products.
+constexpr unsigned FULL = 0xffffffffu;
+
+// column-parallel inverse of the 16x16 lower matrix held row-wise in r[]
+// (lane i&15 = row i): lane j&15 returns column j of the inverse in x[].
+__device__ __forceinline__ void warp_inv16(const double (&r)[16], double (&x)[16]) {
+  const int jc = threadIdx.x & 15;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const double lii = __shfl_sync(FULL, r[i], i);
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) {
+      const double lik = __shfl_sync(FULL, r[k], i);
+      if (k >= jc) acc += lik * x[k];
+    }
+    x[i] = i < jc ? 0.0 : (i == jc ? 1.0 / lii : -acc / lii);
+  }
+}
+
+// In-place Cholesky of the lower 128x128 block in S (right-looking, 16-wide
+// panels): warp 0 factors the diagonal sub-block with shuffles, one thread per
+// row solves the panel by forward substitution, 4x4 micro-tiles update the
+// trailing lower part. Returns the first failing pivot (kernels.py:68-71) or -1.
+__device__ int block_potrf(double* S, SmemCtl& ctl) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* dinv = S + BLK * SLD;  // 1 / L[k][k] of the current panel
+  if (tid == 0) ctl.scan_min = 1 << 30;
+  cons_bar();
+  long long tq = clock64();
+  auto probe = [&](int k) {
+    const long long now = clock64();
+    if (tid == 0) ctl.dbg2[k] += now - tq;
+    tq = now;
+  };
+  for (int P = 0; P < 8; ++P) {
+    const int p0 = 16 * P;
+    if (warp == 0) {
+      const int i = lane & 15;
+      double r[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) r[j] = j <= i ? S[(p0 + i) * SLD + p0 + j] : 0.0;
+      unsigned badmask = 0;
+      double my_il = 1.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const double piv = __shfl_sync(FULL, r[k], k);
+        const bool bad = !(piv > 0.0) || !isfinite(piv);
+        badmask |= bad ? (1u << k) : 0u;
+        const double il = bad ? 1.0 : rsqrt(piv);  // every lane, no broadcast needed
+        const double l = bad ? 1.0 : piv * il;
+        my_il = (i == k) ? il : my_il;
+        r[k] = (i == k) ? l : (i > k ? r[k] * il : r[k]);
+#pragma unroll
+        for (int j = k + 1; j < 16; ++j) {
+          const double v = __shfl_sync(FULL, r[k], j);
+          r[j] = (i >= j) ? fma(-r[k], v, r[j]) : r[j];
+        }
+      }
+      if (lane == 0 && badmask) atomicMin(&ctl.scan_min, p0 + __ffs(badmask) - 1);
+      if (lane < 16) {
+        dinv[i] = my_il;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) S[(p0 + i) * SLD + p0 + j] = j <= i ? r[j] : 0.0;
+      }
+    }
+    cons_bar();
+    probe(0);
+    // panel rows: v L_PP^T = a by forward substitution
+    for (int row = p0 + 16 + tid; row < BLK; row += 256) {
+      double v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = S[row * SLD + p0 + k];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        double w0 = v[j], w1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < j; k += 2) {
+          w0 -= v[k] * S[(p0 + j) * SLD + p0 + k];
+          if (k + 1 < j) w1 -= v[k + 1] * S[(p0 + j) * SLD + p0 + k + 1];
+        }
+        v[j] = (w0 + w1) * dinv[j];
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) S[row * SLD + p0 + k] = v[k];
+    }
+    cons_bar();
+    probe(1);
+    // trailing: A[I][J] -= A[I][P] A[J][P]^T, P < J <= I, 4x4 micro-tiles
+    const int m = 7 - P;
+    for (int tt = tid; tt < 16 * m * (m + 1) / 2; tt += 256) {
+      int ii, jj;
+      lower_pair(tt >> 4, ii, jj);
+      const int mt = tt & 15;  // rows r0..r0+3, columns c0 + 4w (strided: conflict-free loads)
+      const int r0 = 16 * (P + 1 + ii) + 4 * (mt >> 2), c0 = 16 * (P + 1 + jj) + (mt & 3);
+      double acc[4][4] = {};
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        double a[4], b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          a[q] = S[(r0 + q) * SLD + p0 + k];
+          b[q] = S[(c0 + 4 * q) * SLD + p0 + k];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int w = 0; w < 4; ++w) acc[q][w] += a[q] * b[w];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) S[(r0 + q) * SLD + c0 + 4 * w] -= acc[q][w];
+    }
+    cons_bar();
+    probe(2);
+  }
+  const int f = ctl.scan_min;
+  return f < (1 << 30) ? f : -1;
+}
+
+// In-place inverse of the lower-triangular 128x128 block in S by recursive
+// doubling: the eight 16x16 diagonal blocks (one warp each), then for
+// s = 16, 32, 64 every pair [[A,0],[B,C]] -> [[A^-1,0],[-C^-1 B A^-1, C^-1]]
+// (two micro-tiled products per level, all pairs of a level at once).
+// Strict upper part of S must be zero on entry.
+__device__ void block_trtri(double* S, unsigned long long* ctl_dbg) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* T = S + BLK * SLD;  // B A^-1 of every pair, 64 x 65 doubles per level
+  long long tq = clock64();
+  int pk = 3;
+  auto probe = [&]() {
+    const long long now = clock64();
+    if (tid == 0) ctl_dbg[pk] += now - tq;
+    tq = now;
+    ++pk;
+  };
+  {
+    const int p0 = 16 * warp, i = lane & 15;
+    double r[16], x[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) r[j] = j <= i ? S[(p0 + i) * SLD + p0 + j] : 0.0;
+    warp_inv16(r, x);
+    __syncwarp();
+    if (lane < 16) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) S[(p0 + k) * SLD + p0 + lane] = x[k];
+    }
+  }
+  cons_bar();
+  probe();
+  for (int s = 16; s < BLK; s *= 2) {
+    const int per = (s / 4) * (s / 4), total = (BLK / (2 * s)) * per;
+    const int cs = s / 4;  // micro-tile columns c0 + cs*w (strided: conflict-free loads)
+    for (int tt = tid; tt < total; tt += 256) {  // T_c = B_c A_c^-1
+      const int c = tt / per, mt = tt % per;
+      const int tr = 4 * (mt / cs), c0 = mt % cs;
+      const int a0 = 2 * c * s, b0 = a0 + s;
+      double acc[4][4] = {};
+#pragma unroll 4
+      for (int k = c0; k < s; ++k) {  // A^-1 lower: rows k >= c0 only
+        double a[4], b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          a[q] = S[(b0 + tr + q) * SLD + a0 + k];
+          b[q] = S[(a0 + k) * SLD + a0 + c0 + cs * q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int w = 0; w < 4; ++w) acc[q][w] += a[q] * b[w];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) T[c * s * 65 + (tr + q) * 65 + c0 + cs * w] = acc[q][w];
+    }
+    cons_bar();
+    for (int tt = tid; tt < total; tt += 256) {  // X21_c = -C_c^-1 T_c
+      const int c = tt / per, mt = tt % per;
+      const int tr = 4 * (mt / cs), c0 = mt % cs;
+      const int a0 = 2 * c * s, b0 = a0 + s;
+      double acc[4][4] = {};
+#pragma unroll 4
+      for (int k = 0; k < tr + 4; ++k) {  // C^-1 lower: columns k <= row only
+        double a[4], b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          a[q] = S[(b0 + tr + q) * SLD + b0 + k];
+          b[q] = T[c * s * 65 + k * 65 + c0 + cs * q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int w = 0; w < 4; ++w) acc[q][w] += a[q] * b[w];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) S[(b0 + tr + q) * SLD + a0 + c0 + cs * w] = -acc[q][w];
+    }
+    cons_bar();
+    probe();
+  }
 }
 
 __device__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams& P, SmemCtl& ctl, double* S,
                             int b) {
   const int64_t bp = P.bp;
   const int R = P.R;
-  double* tile = P.pool + (int64_t)it.out_s * P.slot_elems;
   const int d = jb.d;
   if (ctl.fail_code) return;  // item already failed: keep the job protocol, skip work
+  double* dst = P.pool + (int64_t)jb.o_s * P.slot_elems;
   switch (jb.special) {
-    case SP_POTRF_DIAG: {
-      if (d == 0) zero_upper_blocks(tile, R, bp);
-      double* blk = tile + (int64_t)d * BLK * bp + d * BLK;
-      if (threadIdx.x == 0) ctl.scan_min = -1;
-      load_block_lower(S, blk, bp);
+    case SP_BPOTRF: {  // factor block (d,d) of dst in place; inverse -> aux block (d,d)
+      long long t0 = clock64();
+      double* blk = dst + (int64_t)d * BLK * bp + d * BLK;
+      for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
+        const int i = e >> 7, j = e & 127;
+        S[i * SLD + j] = (j <= i) ? __ldcg(blk + i * bp + j) : 0.0;
+      }
       cons_bar();
-      const int f = small_potrf(S, ctl);
+      long long t1 = clock64();
+      const int f = block_potrf(S, ctl);
+      long long t2 = clock64();
+      if (threadIdx.x == 0) {
+        ctl.dbg[0] += t1 - t0;
+        ctl.dbg[1] += t2 - t1;
+      }
       if (f >= 0) {
         if (threadIdx.x == 0) {
           ctl.fail_code = TINV_ERR_NOT_SPD;
@@ -735,54 +840,59 @@ __device__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams&
         cons_bar();
         return;
       }
+      t0 = clock64();
       store_block_lower(S, blk, bp);
+      zero_upper_row(dst, d, R, bp);
       cons_bar();
-      small_trtri(S);
-      store_block_lower(S, P.pool + (int64_t)it.scr_s * P.slot_elems, bp);
-      break;
-    }
-    case SP_INV_INIT: {  // aux <- tril(L) (lower tiles of L, zero upper), then scan
-      const double* src = P.pool + (int64_t)it.in0_s * P.slot_elems;
-      for (int r = 0; r < R; ++r)
-        for (int c = 0; c < R; ++c) {
-          const double* sb = src + (int64_t)r * BLK * bp + c * BLK;
-          double* db = tile + (int64_t)r * BLK * bp + c * BLK;
-          for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
-            const int i = e >> 7, j = e & 127;
-            db[i * bp + j] = (r > c || (r == c && j <= i)) ? __ldcg(sb + i * bp + j) : 0.0;
-          }
-        }
-      break;
-    }
-    case SP_TRTRI_DIAG: {
-      if (d == R - 1) {  // first diagonal phase: zero-pivot scan (kernels.py:125-127), clear upper
-        if (threadIdx.x == 0) ctl.scan_min = 1 << 30;
-        cons_bar();
-        scan_zero_diag(tile, b, bp, ctl);
-        cons_bar();
-        if (ctl.scan_min < (1 << 30)) {
-          if (threadIdx.x == 0) {
-            ctl.fail_code = TINV_ERR_SINGULAR;
-            ctl.fail_index = ctl.scan_min;
-          }
-          cons_bar();
-          return;
-        }
-        zero_upper_blocks(tile, R, bp);
+      t1 = clock64();
+      block_trtri(S, ctl.dbg2);
+      t2 = clock64();
+      double* aux = P.pool + (int64_t)jb.src_s * P.slot_elems;
+      store_block_lower(S, aux + (int64_t)d * BLK * bp + d * BLK, bp);
+      cons_bar();
+      if (threadIdx.x == 0) {
+        ctl.dbg[3] += t1 - t0 + clock64() - t2;
+        ctl.dbg[2] += t2 - t1;
       }
-      double* blk = tile + (int64_t)d * BLK * bp + d * BLK;
-      load_block_lower(S, blk, bp);
+      break;
+    }
+    case SP_BTRTRI: {  // dst block (d,d) <- inv(tril(src block (d,d))); zero dst blocks (d, c>d)
+      const double* sb = P.pool + (int64_t)jb.src_s * P.slot_elems + (int64_t)d * BLK * bp + d * BLK;
+      if (threadIdx.x == 0) ctl.scan_min = 1 << 30;
+      for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
+        const int i = e >> 7, j = e & 127;
+        S[i * SLD + j] = (j <= i) ? __ldcg(sb + i * bp + j) : 0.0;
+      }
       cons_bar();
-      small_trtri(S);
-      store_block_lower(S, blk, bp);
+      if (threadIdx.x < BLK && d * BLK + threadIdx.x < b && S[threadIdx.x * SLD + threadIdx.x] == 0.0)
+        atomicMin(&ctl.scan_min, threadIdx.x);  // kernels.py:125-127: zero diagonal
+      cons_bar();
+      if (ctl.scan_min < (1 << 30)) {
+        if (threadIdx.x == 0) {
+          ctl.fail_code = TINV_ERR_SINGULAR;
+          ctl.fail_index = d * BLK + ctl.scan_min;
+        }
+        cons_bar();
+        return;
+      }
+      long long t1 = clock64();
+      block_trtri(S, ctl.dbg2);
+      long long t2 = clock64();
+      store_block_lower(S, dst + (int64_t)d * BLK * bp + d * BLK, bp);
+      zero_upper_row(dst, d, R, bp);
+      cons_bar();
+      if (threadIdx.x == 0) {
+        ctl.dbg[2] += t2 - t1;
+        ctl.dbg[3] += clock64() - t2;
+      }
       break;
     }
     case SP_COPY_ROWS: {
-      const double* src = P.pool + (int64_t)it.in0_s * P.slot_elems + (int64_t)d * BLK * bp;
-      double* dst = tile + (int64_t)d * BLK * bp;
+      const double* src = P.pool + (int64_t)jb.src_s * P.slot_elems + (int64_t)d * BLK * bp;
+      double* out = dst + (int64_t)d * BLK * bp;
       const int64_t n2 = (int64_t)BLK * bp / 2;
       for (int64_t e = threadIdx.x; e < n2; e += 256)
-        reinterpret_cast<double2*>(dst)[e] = __ldcg(reinterpret_cast<const double2*>(src) + e);
+        reinterpret_cast<double2*>(out)[e] = __ldcg(reinterpret_cast<const double2*>(src) + e);
       break;
     }
     default:
@@ -791,12 +901,14 @@ __device__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams&
 }
 
 // ---------------------------------------------------------------- scheduler (device side)
-__device__ __forceinline__ void push_task(const ExecParams& P, int s) {
+__device__ __forceinline__ void push_task(const ExecParams& P, int s, int phase) {
   const TaskDev& t = P.tasks[s];
   const int lev = t.level;
-  const int pos = atomicAdd(&P.q_tail[lev], t.nitems);
+  const int n = phase_items(t.kind, P.R, phase);
+  const int pos = atomicAdd(&P.q_tail[lev], n);
   unsigned long long* q = P.queue + P.q_off[lev] + pos;
-  for (int i = 0; i < t.nitems; ++i) st_release_u64(q + i, ((unsigned long long)(s + 1) << 32) | (unsigned)i);
+  for (int i = 0; i < n; ++i)
+    st_release_u64(q + i, ((unsigned long long)(s + 1) << 32) | ((unsigned)phase << 16) | (unsigned)i);
 }
 
 constexpr unsigned long long POP_EXIT = ~0ull;
@@ -843,7 +955,7 @@ __device__ unsigned long long pop_item(const ExecParams& P) {
 // Storer warp: completion of one work item (all its writes are performed and
 // visible). Last item of a task: swap rename slots, release successors.
 __device__ void complete_item(const ExecParams& P, const Rec& r) {
-  const int task = r.a, nitems = r.b, ref_id = r.c, fail_code = r.d, fail_index = r.e;
+  const int task = r.a, ref_id = r.c, fail_code = r.d, fail_index = r.e, phase = r.f;
   const int lane = threadIdx.x & 31;
   int last = 0;
   if (lane == 0) {
@@ -854,20 +966,26 @@ __device__ void complete_item(const ExecParams& P, const Rec& r) {
       atomicMin(P.err, key);
       atomicExch(P.abort_flag, 1);
     } else {
+      const TaskDev& t = P.tasks[task];
       const int old = atomicAdd(P.done + task, 1);
-      last = (old == nitems - 1);
-      if (last) {
-        const TaskDev& t = P.tasks[task];
-        if (t.flags & TF_RENAMED) {
-          const int cs = __ldcg(P.cur_slot + t.out);
-          P.cur_slot[t.out] = __ldcg(P.alt_slot + t.out);
-          P.alt_slot[t.out] = cs;
+      if (old == phase_items(t.kind, P.R, phase) - 1) {  // phase complete
+        if (phase + 1 < t.nphases) {
+          P.done[task] = 0;  // every item of this phase has finished: no concurrent update
+          __threadfence();
+          push_task(P, task, phase + 1);
+        } else {
+          last = 1;
+          if (t.flags & TF_RENAMED) {
+            const int cs = __ldcg(P.cur_slot + t.out);
+            P.cur_slot[t.out] = __ldcg(P.alt_slot + t.out);
+            P.alt_slot[t.out] = cs;
+          }
+          if (P.trace_end) {
+            atomicMax(P.trace_end + task, globaltimer() - P.t0);
+            P.trace_sm[task] = (int)smid();
+          }
+          __threadfence();
         }
-        if (P.trace_end) {
-          atomicMax(P.trace_end + task, globaltimer() - P.t0);
-          P.trace_sm[task] = (int)smid();
-        }
-        __threadfence();
       }
     }
   }
@@ -877,7 +995,7 @@ __device__ void complete_item(const ExecParams& P, const Rec& r) {
     const TaskDev& t = P.tasks[task];
     for (int k = t.succ_begin + lane; k < t.succ_end; k += 32) {
       const int s = P.succ[k];
-      if (atomicSub(P.indeg + s, 1) == 1) push_task(P, s);
+      if (atomicSub(P.indeg + s, 1) == 1) push_task(P, s, 0);
     }
     __syncwarp();
     if (lane == 0) {
@@ -919,6 +1037,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     ctl.fail_code = 0;
     ctl.fail_index = -1;
     ctl.scan_min = -1;
+    for (int k = 0; k < 4; ++k) ctl.dbg[k] = 0;
+    for (int k = 0; k < 8; ++k) ctl.dbg2[k] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -980,7 +1100,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         break;
       }
       it.task = (int)(e >> 32) - 1;
-      it.item = (int)(e & 0xffffffffu);
+      it.phase = (int)((e >> 16) & 0xffffu);
+      it.item = (int)(e & 0xffffu);
       const TaskDev t = P.tasks[it.task];
       it.kind = t.kind;
       it.step = t.step;
@@ -992,7 +1113,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       it.in0_s = t.in0 >= 0 ? __ldcg(P.cur_slot + t.in0) : -1;
       it.in1_s = t.in1 >= 0 ? __ldcg(P.cur_slot + t.in1) : -1;
       it.scr_s = P.scratch_base + blockIdx.x;
-      it.njobs = job_count(it, R);
+      it.njobs = job_count(it);
       fence_proxy_async();  // tiles written by other SMs (generic proxy) -> TMA reads
       ctl.items[slot] = it;
       mbar_arrive(&ctl.item_full[slot]);
@@ -1044,7 +1165,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONS_REGS));
   unsigned ks = 0;
   EpiState es = {0u, 0u, 0u, 0};
-  unsigned long long ph[NPHASE] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long ph[NPHASE] = {};
   long long tc = clock64();
   auto tick = [&](int k) {
     const long long now = clock64();
@@ -1096,7 +1217,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     tick(4);
     if (tid == 0) {
-      push_rec(ctl, es.rec, Rec{R_ITEM_END, it.task, it.nitems, it.ref_id, ctl.fail_code, ctl.fail_index, 0, 0});
+      push_rec(ctl, es.rec, Rec{R_ITEM_END, it.task, it.nitems, it.ref_id, ctl.fail_code, ctl.fail_index, it.phase, 0});
       ctl.fail_code = 0;
       ctl.fail_index = -1;
     }
@@ -1104,6 +1225,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tick(5);
     ph[6] += 1;
     ph[7] += it.njobs;
+  }
+  if (tid == 0) {
+    for (int k = 0; k < 4; ++k) ph[8 + k] = ctl.dbg[k];
+    for (int k = 0; k < 8; ++k) ph[12 + k] = ctl.dbg2[k];
   }
   if (P.phase && tid == 0)
     for (int k = 0; k < NPHASE; ++k) P.phase[blockIdx.x * NPHASE + k] = ph[k];

@@ -25,6 +25,8 @@ constexpr int STAGE_BYTES = 2 * BLK * KCH * 8;  // 32 KB
 constexpr int EXTRA_SMEM = 64 * 1024;           // extra scratch for diagonal phases
 constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + EXTRA_SMEM + 2048;
 
+
+
 // Hidden task kind inserted by the planner: INV(L) -> aux = tril(L)^-1,
 // shared by every TRSM reading that version of L (TRSM then runs as a
 // DMMA triangular multiply by the inverse).
@@ -39,7 +41,9 @@ struct TaskDev {
   int8_t step;
   int8_t flags;
   int8_t level;
-  int32_t nitems;
+  int16_t nphases;  // diagonal tasks run as chains of parallel block phases
+  int16_t pad;
+  int32_t nitems;   // items over all phases
   int32_t out;     // logical tile ids
   int32_t in0;
   int32_t in1;
@@ -75,8 +79,52 @@ struct ExecParams {
   unsigned long long t0;           // globaltimer at launch (trace base)
   unsigned long long* phase;       // optional per-CTA phase cycle counters (NPHASE each)
 };
-constexpr int NPHASE = 8;  // item-wait, mainloop, epilogue, job-end, item-end, completion, items, jobs
+constexpr int NPHASE = 20;  // item-wait, mainloop, epilogue, job-end, item-end, completion, items, jobs,
+                            // special: load, factor, inverse, store
 
 inline int64_t tri_index(int64_t i, int64_t j) { return i * (i + 1) / 2 + j; }
+
+#ifdef __CUDACC__
+#define TINV_HD __host__ __device__ __forceinline__
+#else
+#define TINV_HD inline
+#endif
+
+// Phases of a task over tiles of R x R blocks (128 x 128).
+//  POTRF (3R-2 phases): d = p/3; p%3 == 0: factor + invert diagonal block d
+//    (1 item); 1: block TRSMs A[r][d] <- A[r][d] inv(L_dd)^T, r > d (R-1-d);
+//    2: trailing block updates A[r][c] -= A[r][d] A[c][d]^T, r >= c > d.
+//  TRTRI / INV (R phases): 0: invert every diagonal block (R items);
+//    s >= 1: X[r][r-s] for r = s..R-1 (R-s items, two block GEMMs each).
+//  everything else: one phase.
+TINV_HD int phases_of(int kind, int R) {
+  if (kind == TINV_POTRF) return 3 * R - 2;
+  if (kind == TINV_TRTRI || kind == KIND_INV) return R;
+  return 1;
+}
+TINV_HD int phase_items(int kind, int R, int p) {
+  switch (kind) {
+    case TINV_POTRF: {
+      const int d = p / 3, m = R - 1 - d;
+      return p % 3 == 0 ? 1 : (p % 3 == 1 ? m : m * (m + 1) / 2);
+    }
+    case TINV_TRTRI:
+    case KIND_INV:
+      return p == 0 ? R : R - p;
+    case TINV_SYRK_SUB:
+    case TINV_SYRK_ADD_T:
+    case TINV_LAUUM:
+      return R * (R + 1) / 2;
+    case TINV_COPY:
+      return R;
+    default:
+      return R * R;
+  }
+}
+TINV_HD int total_items(int kind, int R) {
+  int n = 0;
+  for (int p = 0; p < phases_of(kind, R); ++p) n += phase_items(kind, R, p);
+  return n;
+}
 
 }  // namespace tinv
