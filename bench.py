@@ -306,13 +306,21 @@ def main():
                "sample": f"n={args.cpu_sample_n}, nb={nb} full inversion (oracle port of tileinv: numpy kernels, "
                          f"threaded hazard-DAG executor, {r['cores']} workers, BLAS 1 thread)"}
 
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "exec_c3_traffic.json")
+    if os.path.exists(tpath) and (n, nb, args.placement) == (32768, 512, "out"):
+        with open(tpath) as fh:
+            traffic = json.load(fh)["traffic_bytes"]
+
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "Gflop/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / DMMA_PEAK_TFLOPS, "traffic": None,
+                         "frac": achieved / DMMA_PEAK_TFLOPS, "traffic": traffic,
+                         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one exec_kernel "
+                                           "launch, ncu application replay (profiles/exec_c3_traffic.json)",
                          "kernel": "tinv::exec_kernel (persistent DAG executor, DMMA.8x8x4)",
                          "algorithmic": f"n^3 = {flops:.3e} flop per launch",
                          "peak_source": "measured FP64 DMMA peak (tools/fp64_peak.cu); cuBLAS DGEMM "
