@@ -98,6 +98,12 @@ const char* tinv_last_error(const tinv_ctx* ctx);
 
 /* TileMatrix (tile_matrix.py:35-66): order n, tile order b, on `device`. */
 int tinv_create(tinv_ctx** ctx, int64_t n, int64_t b, int device);
+/* A batch of `batch` independent order-n matrices in one device store
+ * (BASELINE config 4). Dense transfers then move `batch` matrices stored back
+ * to back (matrix m at offset m * n * lda); a plan made from a one-matrix
+ * stream runs it on every matrix as one merged DAG (independent chains).
+ * Error task ids are m * ntasks + task. Tile calls address matrix 0. */
+int tinv_create_batch(tinv_ctx** ctx, int64_t batch, int64_t n, int64_t b, int device);
 int tinv_destroy(tinv_ctx* ctx);
 int tinv_shape(const tinv_ctx* ctx, int64_t* n, int64_t* b, int64_t* t, int64_t* padded_b);
 /* run the context's device work on a caller-owned cudaStream_t (NULL restores

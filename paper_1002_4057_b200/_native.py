@@ -22,7 +22,7 @@ DENSE_LOWER, DENSE_SYMMETRIZE = 0, 1
 
 # every symbol include/tileinv_b200.h declares
 EXPORTS = (
-    "tinv_abi_version", "tinv_device_count", "tinv_last_error", "tinv_create", "tinv_destroy",
+    "tinv_abi_version", "tinv_device_count", "tinv_last_error", "tinv_create", "tinv_create_batch", "tinv_destroy",
     "tinv_shape", "tinv_set_stream", "tinv_put_dense", "tinv_get_dense", "tinv_put_dense_device", "tinv_get_dense_device",
     "tinv_put_tile", "tinv_get_tile", "tinv_gen_stream", "tinv_dag_edges", "tinv_plan_create",
     "tinv_plan_exec", "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
@@ -65,6 +65,7 @@ def lib():
         "tinv_device_count": ([], ctypes.c_int),
         "tinv_last_error": ([_P], ctypes.c_char_p),
         "tinv_create": ([ctypes.POINTER(_P), _I64, _I64, ctypes.c_int], ctypes.c_int),
+        "tinv_create_batch": ([ctypes.POINTER(_P), _I64, _I64, _I64, ctypes.c_int], ctypes.c_int),
         "tinv_destroy": ([_P], ctypes.c_int),
         "tinv_shape": ([_P, _I64P, _I64P, _I64P, _I64P], ctypes.c_int),
         "tinv_set_stream": ([_P, _P], ctypes.c_int),
@@ -155,14 +156,14 @@ def dag_edges(table, barriers):
 class Context:
     """One device tile store (tinv_ctx) for an order-n matrix with tile order b."""
 
-    def __init__(self, n, b, device=0):
+    def __init__(self, n, b, device=0, batch=1):
         L = lib()
         h = _P()
-        rc = L.tinv_create(ctypes.byref(h), n, b, device)
+        rc = L.tinv_create_batch(ctypes.byref(h), batch, n, b, device)
         if rc != OK:
             raise NativeError(rc, last_error(None))
         self.h = h
-        self.n, self.b = n, b
+        self.n, self.b, self.batch = n, b, batch
         self.t = n // b
 
     def close(self):
@@ -182,11 +183,11 @@ class Context:
 
     def put_dense(self, m):
         m = np.ascontiguousarray(m, dtype=np.float64)
-        check(lib().tinv_put_dense(self.h, _dp(m), m.shape[1]), self.h)
+        check(lib().tinv_put_dense(self.h, _dp(m), m.shape[-1]), self.h)
 
     def get_dense(self, out, mode=DENSE_LOWER):
         assert out.dtype == np.float64 and out.flags["C_CONTIGUOUS"]
-        check(lib().tinv_get_dense(self.h, _dp(out), out.shape[1], mode), self.h)
+        check(lib().tinv_get_dense(self.h, _dp(out), out.shape[-1], mode), self.h)
         return out
 
     def put_dense_device(self, ptr, lda):

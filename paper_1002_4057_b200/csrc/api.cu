@@ -21,10 +21,11 @@ namespace tinv {
 cudaError_t launch_exec(const CUtensorMap& tmK, const CUtensorMap& tmM, const CUtensorMap& tmE, const ExecParams& P,
                         int b, int grid, cudaStream_t stream);
 cudaError_t launch_put(const double* src, int64_t lda, int64_t row0, double* pool, int64_t slot_elems,
-                       const int32_t* slot_of, int b, int bp, int64_t tri_lo, int64_t ntiles, cudaStream_t st);
+                       const int32_t* slot_of, int b, int bp, int64_t tri_lo, int64_t ntiles, cudaStream_t st,
+                       int64_t T1, int64_t mstride);
 cudaError_t launch_get(double* dst, int64_t ldd, int64_t row0, const double* pool, int64_t slot_elems,
                        const int32_t* slot_of, int b, int bp, int t, int panel_i, int64_t tile_lo,
-                       int64_t ntiles, int symmetrize, cudaStream_t st);
+                       int64_t ntiles, int symmetrize, cudaStream_t st, int64_t T1, int64_t mstride);
 cudaError_t launch_copy_slots(double* pool, int64_t slot_elems, const int32_t* from, const int32_t* to,
                               int64_t n, cudaStream_t st);
 }  // namespace tinv
@@ -35,6 +36,8 @@ static std::string g_err;
 
 struct tinv_ctx {
   int64_t n = 0, b = 0, t = 0, bp = 0, R = 0, T = 0;
+  int64_t nmat = 1, T1 = 0;  // batched store: nmat matrices of T1 lower tiles each (T = nmat * T1)
+  double* bstage = nullptr;  // batched host transfers: whole-batch device staging
   int device = 0, nsm = 0;
   cudaStream_t st = nullptr, st2 = nullptr, own = nullptr;
   double* pool = nullptr;
@@ -136,10 +139,13 @@ int tinv_device_count(void) {
   return ok;
 }
 
-int tinv_create(tinv_ctx** out, int64_t n, int64_t b, int device) {
+int tinv_create(tinv_ctx** out, int64_t n, int64_t b, int device) { return tinv_create_batch(out, 1, n, b, device); }
+
+int tinv_create_batch(tinv_ctx** out, int64_t batch, int64_t n, int64_t b, int device) {
   if (!out) return fail(nullptr, TINV_ERR_BAD_ARG, "null ctx pointer");
   *out = nullptr;
   if (n < 1 || b < 1 || n % b) return fail(nullptr, TINV_ERR_BAD_ARG, "matrix order not divisible by tile order");
+  if (batch < 1) return fail(nullptr, TINV_ERR_BAD_ARG, "batch must be >= 1");
   int nd = 0;
   if (cudaGetDeviceCount(&nd) != cudaSuccess || device < 0 || device >= nd) {
     cudaGetLastError();
@@ -154,7 +160,9 @@ int tinv_create(tinv_ctx** out, int64_t n, int64_t b, int device) {
   c->t = n / b;
   c->bp = (b + BLK - 1) / BLK * BLK;
   c->R = c->bp / BLK;
-  c->T = c->t * (c->t + 1) / 2;
+  c->T1 = c->t * (c->t + 1) / 2;
+  c->nmat = batch;
+  c->T = c->T1 * batch;
   c->device = device;
   c->nsm = prop.multiProcessorCount;
   c->slot_elems = c->bp * c->bp;
@@ -187,6 +195,7 @@ int tinv_destroy(tinv_ctx* c) {
   cudaSetDevice(c->device);
   if (c->pool) cudaFree(c->pool);
   if (c->d_a_slot) cudaFree(c->d_a_slot);
+  if (c->bstage) cudaFree(c->bstage);
   for (auto& s : c->staging)
     if (s) cudaFree(s);
   if (c->own) cudaStreamDestroy(c->own);
@@ -232,7 +241,8 @@ int tinv_put_dense_device(tinv_ctx* c, const double* dev, int64_t lda) {
   CK(c, cudaSetDevice(c->device));
   int rc = sync_slots(c);
   if (rc) return rc;
-  CK(c, launch_put(dev, lda, 0, c->pool, c->slot_elems, c->d_a_slot, (int)c->b, (int)c->bp, 0, c->T, c->st));
+  CK(c, launch_put(dev, lda, 0, c->pool, c->slot_elems, c->d_a_slot, (int)c->b, (int)c->bp, 0, c->T, c->st, c->T1,
+                   c->n * lda));
   CK(c, cudaStreamSynchronize(c->st));
   return TINV_OK;
 }
@@ -244,16 +254,29 @@ int tinv_get_dense_device(tinv_ctx* c, double* dev, int64_t lda, int mode) {
   if (rc) return rc;
   const int sym = mode == TINV_DENSE_SYMMETRIZE;
   CK(c, launch_get(dev, lda, 0, c->pool, c->slot_elems, c->d_a_slot, (int)c->b, (int)c->bp, (int)c->t, -1, 0,
-                   sym ? c->t * c->t : c->T, sym, c->st));
+                   sym ? c->nmat * c->t * c->t : c->T, sym, c->st, c->T1, c->n * lda));
   CK(c, cudaStreamSynchronize(c->st));
   return TINV_OK;
 }
 
 // Host transfers go by tile-row panels through two device staging buffers:
 // H2D of panel i+1 (copy stream) overlaps the conversion of panel i.
+static int ensure_bstage(tinv_ctx* c) {
+  if (c->bstage) return TINV_OK;
+  CK(c, cudaMalloc(&c->bstage, (size_t)c->nmat * c->n * c->n * 8));
+  return TINV_OK;
+}
+
 int tinv_put_dense(tinv_ctx* c, const double* host, int64_t lda) {
   if (!c || !host || lda < c->n) return fail(c, TINV_ERR_BAD_ARG, "bad put_dense arguments");
   CK(c, cudaSetDevice(c->device));
+  if (c->nmat > 1) {  // batch: one bulk copy of all matrices, then one conversion
+    int rc = ensure_bstage(c);
+    if (rc) return rc;
+    CK(c, cudaMemcpy2DAsync(c->bstage, c->n * 8, host, lda * 8, c->n * 8, c->nmat * c->n, cudaMemcpyHostToDevice,
+                            c->st));
+    return tinv_put_dense_device(c, c->bstage, c->n);
+  }
   int rc = ensure_staging(c);
   if (rc) return rc;
   rc = sync_slots(c);
@@ -273,7 +296,7 @@ int tinv_put_dense(tinv_ctx* c, const double* host, int64_t lda) {
     CK(c, cudaEventRecord(copied[k], c->st2));
     CK(c, cudaStreamWaitEvent(c->st, copied[k], 0));
     CK(c, launch_put(c->staging[k], n, i * b, c->pool, c->slot_elems, c->d_a_slot, (int)b, (int)c->bp,
-                     tri_index(i, 0), i + 1, c->st));
+                     tri_index(i, 0), i + 1, c->st, c->T1, 0));
     CK(c, cudaEventRecord(freed[k], c->st));
   }
   CK(c, cudaStreamSynchronize(c->st));
@@ -288,6 +311,19 @@ int tinv_put_dense(tinv_ctx* c, const double* host, int64_t lda) {
 int tinv_get_dense(tinv_ctx* c, double* host, int64_t lda, int mode) {
   if (!c || !host || lda < c->n) return fail(c, TINV_ERR_BAD_ARG, "bad get_dense arguments");
   CK(c, cudaSetDevice(c->device));
+  if (c->nmat > 1) {
+    int rc = ensure_bstage(c);
+    if (rc) return rc;
+    if (mode != TINV_DENSE_SYMMETRIZE)  // LOWER mode keeps the caller's upper tiles
+      CK(c, cudaMemcpy2DAsync(c->bstage, c->n * 8, host, lda * 8, c->n * 8, c->nmat * c->n, cudaMemcpyHostToDevice,
+                              c->st));
+    rc = tinv_get_dense_device(c, c->bstage, c->n, mode);
+    if (rc) return rc;
+    CK(c, cudaMemcpy2DAsync(host, lda * 8, c->bstage, c->n * 8, c->n * 8, c->nmat * c->n, cudaMemcpyDeviceToHost,
+                            c->st));
+    CK(c, cudaStreamSynchronize(c->st));
+    return TINV_OK;
+  }
   int rc = ensure_staging(c);
   if (rc) return rc;
   rc = sync_slots(c);
@@ -305,7 +341,7 @@ int tinv_get_dense(tinv_ctx* c, double* host, int64_t lda, int mode) {
     const int64_t ntile = sym ? c->t : i + 1;
     CK(c, cudaStreamWaitEvent(c->st, freed[k], 0));
     CK(c, launch_get(c->staging[k], n, i * b, c->pool, c->slot_elems, c->d_a_slot, (int)b, (int)c->bp,
-                     (int)c->t, (int)i, 0, ntile, sym, c->st));
+                     (int)c->t, (int)i, 0, ntile, sym, c->st, c->T1, 0));
     CK(c, cudaEventRecord(built[k], c->st));
     CK(c, cudaStreamWaitEvent(c->st2, built[k], 0));
     CK(c, cudaMemcpy2DAsync(host + i * b * lda, lda * 8, c->staging[k], n * 8, (size_t)ntile * b * 8, b,
@@ -331,7 +367,7 @@ int tinv_put_tile(tinv_ctx* c, int64_t i, int64_t j, const double* host) {
   CK(c, cudaMemcpyAsync(tmp, host, (size_t)c->b * c->b * 8, cudaMemcpyHostToDevice, c->st));
   const int64_t x = tri_index(i, j);
   CK(c, launch_put(tmp - i * c->b * c->b - j * c->b, c->b, 0, c->pool, c->slot_elems, c->d_a_slot, (int)c->b,
-                   (int)c->bp, x, 1, c->st));
+                   (int)c->bp, x, 1, c->st, c->T1, 0));
   CK(c, cudaStreamSynchronize(c->st));
   cudaFree(tmp);
   return TINV_OK;
@@ -653,21 +689,20 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
   tinv_plan* p = new tinv_plan();
   p->ctx = c;
   p->flags = flags;
-  p->nref = n;
-  p->ref_kind.resize(n);
 
   // ---- logical tiles, validation, INV insertion for TRSM (renamed inverse)
   std::unordered_map<int64_t, int32_t> logical;  // key -> logical id (non-matrix tiles)
   std::vector<char> written_dyn;                 // per non-matrix logical: written so far
   int64_t next_logical = T;
+  int64_t mm = 0;  // matrix of a batched store the task is replicated for
   auto get_logical = [&](int label, int r, int cc, bool is_read, int64_t task, int32_t& id) -> bool {
     if (label == 0) {
       if (r < 0 || r >= t || cc < 0 || cc > r) return false;
-      id = (int32_t)tri_index(r, cc);
+      id = (int32_t)(mm * c->T1 + tri_index(r, cc));
       return true;
     }
-    if (label < 0 || r < 0 || r >= t || cc < 0 || cc >= t) return false;
-    const int64_t key = tile_key(label, r, cc);
+    if (label < 0 || label >= 1024 || r < 0 || r >= t || cc < 0 || cc >= t) return false;
+    const int64_t key = tile_key(label, r, cc) | (mm << 50);
     auto it = logical.find(key);
     if (it == logical.end()) {
       if (is_read) return false;  // reference: store KeyError (never written)
@@ -686,12 +721,21 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
   struct XT {
     int kind, step, out, in0, in1, mode, ref;
   };
+  const int64_t nm = c->nmat;  // batched store: the stream is replicated per matrix (no cross edges)
+  if (nm > 1 && barriers && nbar > 0) {
+    tinv_plan_destroy(p);
+    return fail(c, TINV_ERR_BAD_ARG, "barriers are not supported on a batched store");
+  }
+  p->nref = n * nm;
+  p->ref_kind.resize(n * nm);
   std::vector<XT> xs;
-  xs.reserve(n + n / 8 + 8);
+  xs.reserve(nm * (n + n / 8 + 8));
   std::vector<char> is_aux;
-  std::vector<int32_t> first_exec_of_ref(n + 1, 0);
-  for (int64_t v = 0; v < n; ++v) {
-    const int32_t* f = table + v * TINV_TASK_FIELDS;
+  std::vector<int32_t> first_exec_of_ref(n * nm + 1, 0);
+  for (int64_t rv = 0; rv < n * nm; ++rv) {
+    mm = rv / n;
+    const int64_t v = rv;
+    const int32_t* f = table + (rv % n) * TINV_TASK_FIELDS;
     const int kind = f[F_KIND];
     p->ref_kind[v] = kind;
     first_exec_of_ref[v] = (int32_t)xs.size();
@@ -737,7 +781,7 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
     last_writer_exec[o] = (int32_t)xs.size();
     xs.push_back({kind, f[F_STEP], o, in0, in1, f[F_OM] == 2 ? 2 : 1, (int)v});
   }
-  first_exec_of_ref[n] = (int32_t)xs.size();
+  first_exec_of_ref[n * nm] = (int32_t)xs.size();
   p->nexec = (int64_t)xs.size();
   p->nlogical = next_logical;
   const int64_t nx = p->nexec;

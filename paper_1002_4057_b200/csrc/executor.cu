@@ -615,11 +615,14 @@ __device__ __forceinline__ void warp_inv16(const double (&r)[16], double (&x)[16
     const double lii = __shfl_sync(FULL, r[i], i);
     double acc = 0.0;
 #pragma unroll
-    for (int k = 0; k < i; ++k) {
-      const double lik = __shfl_sync(FULL, r[k], i);
-      if (k >= jc) acc += lik * x[k];
+    for (int k = 0; k < 15; ++k) {  // constant trip count: r[] / x[] stay in registers
+      if (k < i) {
+        const double lik = __shfl_sync(FULL, r[k], i);
+        acc = (k >= jc) ? fma(lik, x[k], acc) : acc;
+      }
     }
-    x[i] = i < jc ? 0.0 : (i == jc ? 1.0 / lii : -acc / lii);
+    const double inv = 1.0 / lii;
+    x[i] = i < jc ? 0.0 : (i == jc ? inv : -acc * inv);
   }
 }
 
@@ -657,9 +660,11 @@ __device__ int block_potrf(double* S, SmemCtl& ctl) {
         my_il = (i == k) ? il : my_il;
         r[k] = (i == k) ? l : (i > k ? r[k] * il : r[k]);
 #pragma unroll
-        for (int j = k + 1; j < 16; ++j) {
-          const double v = __shfl_sync(FULL, r[k], j);
-          r[j] = (i >= j) ? fma(-r[k], v, r[j]) : r[j];
+        for (int j = 1; j < 16; ++j) {  // constant trip count: r[] stays in registers
+          if (j > k) {
+            const double v = __shfl_sync(FULL, r[k], j);
+            r[j] = (i >= j) ? fma(-r[k], v, r[j]) : r[j];
+          }
         }
       }
       if (lane == 0 && badmask) atomicMin(&ctl.scan_min, p0 + __ffs(badmask) - 1);
@@ -680,9 +685,13 @@ __device__ int block_potrf(double* S, SmemCtl& ctl) {
       for (int j = 0; j < 16; ++j) {
         double w0 = v[j], w1 = 0.0;
 #pragma unroll
-        for (int k = 0; k < j; k += 2) {
-          w0 -= v[k] * S[(p0 + j) * SLD + p0 + k];
-          if (k + 1 < j) w1 -= v[k + 1] * S[(p0 + j) * SLD + p0 + k + 1];
+        for (int k = 0; k < 15; ++k) {  // constant trip count: v[] stays in registers
+          if (k < j) {
+            if (k & 1)
+              w1 -= v[k] * S[(p0 + j) * SLD + p0 + k];
+            else
+              w0 -= v[k] * S[(p0 + j) * SLD + p0 + k];
+          }
         }
         v[j] = (w0 + w1) * dinv[j];
       }

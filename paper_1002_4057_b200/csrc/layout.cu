@@ -29,16 +29,19 @@ __device__ __forceinline__ void tri_decode(int64_t x, int& i, int& j) {
 
 // grid.x: lower tiles tri_lo .. tri_lo + gridDim.x - 1; grid.y: 8-row groups of bp
 // src: dense rows starting at global row `row0`
+// batched stores: tile x belongs to matrix x / T1 (matrices `mstride` doubles apart)
 __global__ void __launch_bounds__(256) k_put(const double* __restrict__ src, int64_t lda, int64_t row0,
                                             double* __restrict__ pool, int64_t slot_elems,
-                                            const int32_t* __restrict__ slot_of, int b, int bp, int64_t tri_lo) {
+                                            const int32_t* __restrict__ slot_of, int b, int bp, int64_t tri_lo,
+                                            int64_t T1, int64_t mstride) {
   int i, j;
   const int64_t x = tri_lo + blockIdx.x;
-  tri_decode(x, i, j);
+  const int64_t m = x / T1;
+  tri_decode(x - m * T1, i, j);
   double* dst = pool + (int64_t)slot_of[x] * slot_elems;
   const int rr = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (rr >= bp) return;
-  const double* srow = src + ((int64_t)i * b + rr - row0) * lda + (int64_t)j * b;
+  const double* srow = src + m * mstride + ((int64_t)i * b + rr - row0) * lda + (int64_t)j * b;
   double* drow = dst + (int64_t)rr * bp;
   for (int cc = threadIdx.x & 31; cc < bp; cc += 32) {
     double v;
@@ -57,19 +60,26 @@ __global__ void __launch_bounds__(256) k_put(const double* __restrict__ src, int
 __global__ void __launch_bounds__(256) k_get(double* __restrict__ dst, int64_t ldd, int64_t row0,
                                             const double* __restrict__ pool, int64_t slot_elems,
                                             const int32_t* __restrict__ slot_of, int b, int bp, int t,
-                                            int panel_i, int64_t tile_lo, int symmetrize) {
+                                            int panel_i, int64_t tile_lo, int symmetrize, int64_t T1,
+                                            int64_t mstride) {
   __shared__ double sm[32][33];
   int I, J;
+  int64_t m = 0;
   if (panel_i >= 0) {
     I = panel_i;
     J = (int)(tile_lo + blockIdx.x);
   } else if (symmetrize) {
     const int64_t x = tile_lo + blockIdx.x;
-    I = (int)(x / t);
-    J = (int)(x % t);
+    m = x / ((int64_t)t * t);
+    const int64_t loc = x - m * t * t;
+    I = (int)(loc / t);
+    J = (int)(loc % t);
   } else {
-    tri_decode(tile_lo + blockIdx.x, I, J);
+    const int64_t x = tile_lo + blockIdx.x;
+    m = x / T1;
+    tri_decode(x - m * T1, I, J);
   }
+  dst += m * mstride;
   const int nsb = (b + 31) / 32;
   const int sr = blockIdx.y / nsb, sc = blockIdx.y % nsb;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -88,7 +98,7 @@ __global__ void __launch_bounds__(256) k_get(double* __restrict__ dst, int64_t l
     si = sj = I;
     transp = symmetrize && (sr < sc);
   }
-  const double* tile = pool + (int64_t)slot_of[(int64_t)si * (si + 1) / 2 + sj] * slot_elems;
+  const double* tile = pool + (int64_t)slot_of[m * T1 + (int64_t)si * (si + 1) / 2 + sj] * slot_elems;
   // source sub-block coordinates
   const int br = transp ? sc : sr, bc = transp ? sr : sc;
   for (int k = ty; k < 32; k += 8) {
@@ -110,20 +120,22 @@ __global__ void __launch_bounds__(256) k_get(double* __restrict__ dst, int64_t l
 }
 
 cudaError_t launch_put(const double* src, int64_t lda, int64_t row0, double* pool, int64_t slot_elems,
-                       const int32_t* slot_of, int b, int bp, int64_t tri_lo, int64_t ntiles, cudaStream_t st) {
+                       const int32_t* slot_of, int b, int bp, int64_t tri_lo, int64_t ntiles, cudaStream_t st,
+                       int64_t T1, int64_t mstride) {
   if (ntiles <= 0) return cudaSuccess;
   dim3 grid((unsigned)ntiles, (unsigned)((bp + 7) / 8));
-  k_put<<<grid, 256, 0, st>>>(src, lda, row0, pool, slot_elems, slot_of, b, bp, tri_lo);
+  k_put<<<grid, 256, 0, st>>>(src, lda, row0, pool, slot_elems, slot_of, b, bp, tri_lo, T1, mstride);
   return cudaGetLastError();
 }
 
 cudaError_t launch_get(double* dst, int64_t ldd, int64_t row0, const double* pool, int64_t slot_elems,
                        const int32_t* slot_of, int b, int bp, int t, int panel_i, int64_t tile_lo,
-                       int64_t ntiles, int symmetrize, cudaStream_t st) {
+                       int64_t ntiles, int symmetrize, cudaStream_t st, int64_t T1, int64_t mstride) {
   if (ntiles <= 0) return cudaSuccess;
   const int nsb = (b + 31) / 32;
   dim3 grid((unsigned)ntiles, (unsigned)(nsb * nsb));
-  k_get<<<grid, 256, 0, st>>>(dst, ldd, row0, pool, slot_elems, slot_of, b, bp, t, panel_i, tile_lo, symmetrize);
+  k_get<<<grid, 256, 0, st>>>(dst, ldd, row0, pool, slot_elems, slot_of, b, bp, t, panel_i, tile_lo, symmetrize, T1,
+                              mstride);
   return cudaGetLastError();
 }
 
