@@ -42,19 +42,56 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--n", type=int, default=32768)
-    p.add_argument("--nb", type=int, default=512)
+    p.add_argument("--workload", default="c3", choices=["c1", "c2", "c3", "c4"],
+                   help="BASELINE.json config (c3 = the headline metric's n=32768, nb=512)")
+    p.add_argument("--n", type=int, default=None)
+    p.add_argument("--nb", type=int, default=None)
+    p.add_argument("--batch", type=int, default=None)
     p.add_argument("--placement", default="out", choices=["in", "out"])
     p.add_argument("--loops", default="UDU")
     p.add_argument("--barriered", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--cpu-sample-n", type=int, default=8192)
+    p.add_argument("--cpu-sample-n", type=int, default=None)
     p.add_argument("--cpu-worker", action="store_true", help=argparse.SUPPRESS)
     return p.parse_args()
 
 
 # --------------------------------------------------------------------- CPU side
+def _one_matrix(args):
+    """Pool task for the batched CPU baseline: one matrix through the oracle."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import tileinv_oracle as O
+    a, nb, loops, oop = args
+    with threadpool_limits(1, "blas"):
+        return O.invert(a, nb, loops, oop, True).shape[0]
+
+
+def cpu_worker_batch(n, nb, batch, steps, warmup, placement, loops):
+    """Batched CPU baseline: a process pool with one process per host core, each
+    inverting whole matrices (the reference's t=1 stream per matrix)."""
+    import multiprocessing as mp
+
+    import numpy as np
+    cores = len(os.sched_getaffinity(0))
+    sample = min(batch, 4 * cores)
+    rng = np.random.default_rng(0)
+    g = rng.standard_normal((sample, n, n))
+    a = g @ g.transpose(0, 2, 1) / n + np.eye(n)
+    work = [(a[k], nb, loops, placement == "out") for k in range(sample)]
+    times = []
+    with mp.get_context("fork").Pool(cores) as pool:
+        pool.map(_one_matrix, work[:cores])
+        for k in range(warmup + steps):
+            t0 = time.perf_counter()
+            pool.map(_one_matrix, work, chunksize=1)
+            if k >= warmup:
+                times.append(time.perf_counter() - t0)
+    print(json.dumps({"times": times, "cores": cores, "cpu": "", "flops": float(sample) * n ** 3,
+                      "sample": sample}))
+
+
 def cpu_worker(n, nb, steps, warmup, placement, loops, pipelined):
     """Runs in a subprocess with OPENBLAS_NUM_THREADS=1: the reference's CPU
     algorithm (oracle port) with one worker thread per host core."""
@@ -82,12 +119,13 @@ def cpu_worker(n, nb, steps, warmup, placement, loops, pipelined):
     print(json.dumps({"times": times, "cores": cores, "cpu": model, "flops": float(n) ** 3}))
 
 
-def run_cpu(n, nb, steps, warmup, placement, loops, pipelined):
+def run_cpu(n, nb, steps, warmup, placement, loops, pipelined, batch=1):
     env = dict(os.environ)
     for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
         env.pop(k, None)
     cmd = [sys.executable, os.path.abspath(__file__), "--cpu-worker", "--n", str(n), "--nb", str(nb),
-           "--steps", str(steps), "--warmup", str(warmup), "--placement", placement, "--loops", loops]
+           "--steps", str(steps), "--warmup", str(warmup), "--placement", placement, "--loops", loops,
+           "--batch", str(batch)]
     if not pipelined:
         cmd.append("--barriered")
     out = subprocess.run(cmd, env=env, capture_output=True, text=True, check=True).stdout
@@ -145,20 +183,31 @@ class Clocks:
 def main():
     args = parse()
     if args.cpu_worker:
-        cpu_worker(args.n, args.nb, args.steps, args.warmup, args.placement, args.loops, not args.barriered)
+        if (args.batch or 1) > 1:
+            cpu_worker_batch(args.n, args.nb, args.batch, args.steps, args.warmup, args.placement, args.loops)
+        else:
+            cpu_worker(args.n, args.nb, args.steps, args.warmup, args.placement, args.loops, not args.barriered)
         return
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    n, nb = args.n, args.nb
+    wl = {"c1": (1024, 128, 1), "c2": (8192, 256, 1), "c3": (32768, 512, 1), "c4": (256, 256, 8192)}[args.workload]
+    n = args.n or wl[0]
+    nb = args.nb or wl[1]
+    batch = args.batch or wl[2]
+    if args.cpu_sample_n is None:
+        args.cpu_sample_n = min(n, 8192) if batch == 1 else n
     t = n // nb
     pipelined = not args.barriered
-    flops = float(n) ** 3
-    config = {"workload": f"BASELINE config 3: n={n}, nb={nb}, FP64 SPD inversion "
+    flops = float(batch) * float(n) ** 3
+    in_bytes = batch * n * n * 8
+    desc = (f"{batch} x " if batch > 1 else "") + f"n={n}, nb={nb}"
+    config = {"workload": f"BASELINE config {args.workload[1]}: {desc}, FP64 SPD inversion "
                           f"({args.placement}-of-place, {args.loops}, {'pipelined' if pipelined else 'barriered'})",
-              "n": n, "nb": nb, "t": t, "placement": args.placement, "loops": args.loops,
+              "n": n, "nb": nb, "t": t, "batch": batch, "placement": args.placement, "loops": args.loops,
               "pipelined": pipelined, "input": "A = G G^T/n + I, G iid N(0,1) seed 0",
-              "l2": "inputs 8.6 GB >> 126 MB L2 (no flush needed)",
+              "l2": (f"inputs {in_bytes / 1e9:.1f} GB >> 126 MB L2 (no flush needed)" if in_bytes > 4e8
+                     else "L2 flushed between steps (256 MB write)"),
               "parallelism": "1 GPU" if world == 1 else f"replicas x{world} (independent matrices)"}
 
     if args.impl == "reference":
@@ -166,12 +215,16 @@ def main():
             return
         steps = max(1, args.steps)
         warm = max(0, min(args.warmup, 1))
-        r = run_cpu(args.cpu_sample_n, nb, steps, warm, args.placement, args.loops, pipelined)
+        r = run_cpu(args.cpu_sample_n, nb, steps, warm, args.placement, args.loops, pipelined, batch)
         ts = r["times"]
         med = statistics.median(ts)
         v = r["flops"] / med / 1e9
-        sample = (f"n={args.cpu_sample_n}, nb={nb} (t={args.cpu_sample_n // nb}) full inversion per step, "
-                  f"same variant; median of {len(ts)}")
+        if batch > 1:
+            sample = (f"{r['sample']} of the {batch} n={n} matrices per step, process pool of {r['cores']} "
+                      f"(one process per core, BLAS 1 thread); median of {len(ts)}")
+        else:
+            sample = (f"n={args.cpu_sample_n}, nb={nb} (t={args.cpu_sample_n // nb}) full inversion per step, "
+                      f"same variant; median of {len(ts)}")
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": v, "unit": "Gflop/s", "n_gpus": args.gpus,
             "steps": steps, "warmup": warm, "ms_per_step": med * 1e3, "higher_is_better": True,
@@ -208,16 +261,26 @@ def main():
 
     # input on the device
     gen = torch.Generator(device="cuda").manual_seed(rank)
-    g = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=gen)
-    a = torch.matmul(g, g.T)
-    del g
-    a.div_(n)
-    a.diagonal().add_(1.0)
-    a = torch.tril(a) + torch.tril(a, -1).T
+    if batch == 1:
+        g = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=gen)
+        a = torch.matmul(g, g.T)
+        del g
+        a.div_(n)
+        a.diagonal().add_(1.0)
+        a = torch.tril(a) + torch.tril(a, -1).T
+    else:
+        g = torch.randn(batch, n, n, dtype=torch.float64, device="cuda", generator=gen)
+        a = torch.bmm(g, g.transpose(1, 2))
+        del g
+        a.div_(n)
+        a.diagonal(dim1=1, dim2=2).add_(1.0)
+        a = torch.tril(a) + torch.tril(a, -1).transpose(1, 2)
+        pipelined = True  # a batched store runs the per-matrix chains without barriers
     x = torch.empty_like(a)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda") if in_bytes <= 4e8 else None
 
     stream = torch.cuda.current_stream()
-    ctx = _native.Context(n, nb, local)
+    ctx = _native.Context(n, nb, local, batch=batch)
     ctx.set_stream(stream.cuda_stream)
     s = P.gen_inversion(t, P.VariantConfig(P.Placement(args.placement), args.loops, pipelined))
     table = s.table()
@@ -240,15 +303,17 @@ def main():
     for _ in range(args.warmup):
         step()
     kern_ms.clear()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with Clocks(local) as clk:
         barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
+        for e0, e1 in evs:
+            if flush is not None:  # inputs smaller than L2: flush it between steps (outside the timed spans)
+                flush.fill_(1.0)
+            e0.record(stream)
             step()
-        ev1.record(stream)
+            e1.record(stream)
         barrier()
-    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_total = max_over_ranks(sum(e0.elapsed_time(e1) for e0, e1 in evs))
     ms_step = ms_total / args.steps
     value = world * flops / (ms_step * 1e-3) / 1e9
     kern_avg = statistics.mean(kern_ms)
@@ -256,21 +321,22 @@ def main():
 
     # numerical check of the last step (outside the timed region)
     eye = torch.eye(n, dtype=torch.float64, device="cuda")
-    r = eye - a @ x
-    res = float(torch.linalg.matrix_norm(r, 1) / (n * torch.linalg.matrix_norm(a, 1)
-                                                   * torch.linalg.matrix_norm(x, 1) * 2.220446049250313e-16))
-    sym_err = float((x - x.T).abs().max())
-    del r, eye
+    ac, xc = (a, x) if batch == 1 else (a[:16], x[:16])
+    r = eye - ac @ xc
+    res = float((torch.linalg.matrix_norm(r, 1) / (n * torch.linalg.matrix_norm(ac, 1)
+                                                    * torch.linalg.matrix_norm(xc, 1) * 2.220446049250313e-16)).max())
+    sym_err = float((xc - xc.transpose(-1, -2)).abs().max())
+    del r, eye, ac, xc
 
     # end to end through the C-ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        ha = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        ha = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
         ha.copy_(a)
-        hx = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        hx = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
         del a, x
         torch.cuda.empty_cache()
-        ha_np, hx_np = ha.numpy(), hx.numpy()
+        ha_np, hx_np = ha.numpy().reshape(-1, n), hx.numpy().reshape(-1, n)
         ctx.set_stream(0)
         plan.close()
 
@@ -294,17 +360,19 @@ def main():
         e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / k)
         T = t * (t + 1) // 2
         e2e = {"value": world * flops / (e2e_ms * 1e-3) / 1e9, "unit": "Gflop/s",
-               "h2d_bytes_per_step": T * nb * nb * 8, "d2h_bytes_per_step": n * n * 8,
+               "h2d_bytes_per_step": T * nb * nb * 8 if batch == 1 else in_bytes, "d2h_bytes_per_step": in_bytes,
                "ms_per_step": e2e_ms, "steps": k,
                "path": "gen_stream + put_dense(pinned host) + plan_create + plan_exec + get_dense(symmetrize, pinned host)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        r = run_cpu(args.cpu_sample_n, nb, 1, 0, args.placement, args.loops, pipelined)
+        r = run_cpu(args.cpu_sample_n, nb, 1, 0, args.placement, args.loops, pipelined, batch)
         cpu = {"value": r["flops"] / statistics.median(r["times"]) / 1e9, "unit": "Gflop/s", "cores": r["cores"],
                "kind": "port", "cpu": r["cpu"],
-               "sample": f"n={args.cpu_sample_n}, nb={nb} full inversion (oracle port of tileinv: numpy kernels, "
-                         f"threaded hazard-DAG executor, {r['cores']} workers, BLAS 1 thread)"}
+               "sample": (f"{r['sample']} of the {batch} n={n} matrices, process pool of {r['cores']} "
+                          "(oracle port of tileinv, BLAS 1 thread)") if batch > 1 else
+                         (f"n={args.cpu_sample_n}, nb={nb} full inversion (oracle port of tileinv: numpy kernels, "
+                          f"threaded hazard-DAG executor, {r['cores']} workers, BLAS 1 thread)")}
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "exec_c3_traffic.json")

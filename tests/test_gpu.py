@@ -268,3 +268,31 @@ def test_layout_roundtrip_and_trace(tmp_path):
     for r in rows[1:]:
         tid, kind, idx, w, s, e = r.split(",")
         assert 0 <= int(s) <= int(e)
+
+
+# ---------------------------------------------------------------- BASELINE config 4 (batched)
+@pytest.mark.parametrize("nb", [256, 128])
+def test_batched_inversion_vs_oracle(nb):
+    rng = np.random.default_rng(4)
+    batch, n = 24, 256
+    g = rng.standard_normal((batch, n, n))
+    a = g @ g.transpose(0, 2, 1) / n + np.eye(n)
+    a = np.tril(a) + np.transpose(np.tril(a, -1), (0, 2, 1))
+    x = P.invert_batched(a, nb)
+    for k in range(0, batch, 5):
+        ref = O.invert(a[k], nb)
+        assert rel(x[k], ref) <= 1e-10 * np.linalg.cond(a[k])
+        assert O.residual(a[k], x[k]) < 10
+
+
+def test_batched_failure_reports_matrix():
+    rng = np.random.default_rng(5)
+    batch, n = 6, 128
+    g = rng.standard_normal((batch, n, n))
+    a = g @ g.transpose(0, 2, 1) / n + np.eye(n)
+    a[3, 40, 40] = -2.0
+    with pytest.raises(P.ExecutionError) as ei:
+        P.invert_batched(a, 64)
+    assert ei.value.matrix == 3
+    assert isinstance(ei.value.cause, P.NotPositiveDefiniteError)
+    assert ei.value.task.kind is P.KernelKind.POTRF

@@ -171,3 +171,12 @@ def test_no_cpu_fallback_without_device():
     tm = P.from_dense(np.eye(4) * 4.0, 2)
     with pytest.raises(_native.NativeError):
         P.execute(P.gen_inversion(2, P.VariantConfig()), tm)
+
+
+def test_batched_validation():
+    with pytest.raises(P.InvalidSizeError):
+        P.invert_batched(np.zeros((2, 4, 5)), 2)
+    with pytest.raises(P.InvalidSizeError):
+        P.invert_batched(np.zeros((2, 6, 6)), 4)
+    with pytest.raises(ValueError):
+        P.invert_batched(np.full((1, 2, 2), np.inf), 2)
