@@ -135,6 +135,22 @@ int tinv_gen_stream(int32_t t, int32_t steps, const char* loops, int32_t out_of_
 int tinv_dag_edges(const int32_t* table, int64_t ntasks, const int64_t* barriers, int64_t nbar,
                    int32_t* src, int32_t* dst, int8_t* kind, int64_t cap, int64_t* nedges);
 
+/* Distribution over a P x Q device grid (2D block-cyclic owner-computes,
+ * SURVEY.md §8(e)): owner(i, j) = (i mod P) * Q + (j mod Q) for every tile of
+ * every label; a task runs on the owner of its output tile. The distributed
+ * stream holds every task of `table` with reads of remotely owned tiles
+ * redirected to receive tiles, plus one transfer per (tile version, consumer
+ * rank): a COPY from the owner's tile into a fresh receive tile (label >=
+ * TINV_RECV_LABEL0, so a receiver never waits on anti-dependences), emitted
+ * right after the producing task (initial versions first). owner[k]: rank that
+ * executes out task k (transfers: the sender); dest[k]: receiving rank of a
+ * transfer, -1 otherwise; ref[k]: source task id, -1 for transfers. Executed
+ * as one stream it is the loopback form of the distributed run; its per-rank
+ * slices are the per-GPU streams. table NULL: count only. */
+#define TINV_RECV_LABEL0 64
+int tinv_dist_stream(const int32_t* table, int64_t ntasks, int32_t t, int32_t P, int32_t Q, int32_t* out,
+                     int64_t cap, int64_t* nout, int32_t* owner, int32_t* dest, int32_t* ref);
+
 /* Plan = the device-resident executable form of a stream on a context
  * (hazard DAG, renaming slots, priorities, ready queues). Reusable. */
 int tinv_plan_create(tinv_ctx* ctx, const int32_t* table, int64_t ntasks, int32_t stream_t,

@@ -24,7 +24,7 @@ DENSE_LOWER, DENSE_SYMMETRIZE = 0, 1
 EXPORTS = (
     "tinv_abi_version", "tinv_device_count", "tinv_last_error", "tinv_create", "tinv_create_batch", "tinv_destroy",
     "tinv_shape", "tinv_set_stream", "tinv_put_dense", "tinv_get_dense", "tinv_put_dense_device", "tinv_get_dense_device",
-    "tinv_put_tile", "tinv_get_tile", "tinv_gen_stream", "tinv_dag_edges", "tinv_plan_create",
+    "tinv_put_tile", "tinv_get_tile", "tinv_gen_stream", "tinv_dag_edges", "tinv_dist_stream", "tinv_plan_create",
     "tinv_plan_exec", "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
 )
 
@@ -79,6 +79,7 @@ def lib():
                             ctypes.c_int),
         "tinv_dag_edges": ([_I32P, _I64, _I64P, _I64, _I32P, _I32P, ctypes.POINTER(ctypes.c_int8), _I64, _I64P],
                            ctypes.c_int),
+        "tinv_dist_stream": ([_I32P, _I64, _I32, _I32, _I32, _I32P, _I64, _I64P, _I32P, _I32P, _I32P], ctypes.c_int),
         "tinv_plan_create": ([_P, _I32P, _I64, _I32, _I64P, _I64, _U32, ctypes.POINTER(_P),
                               ctypes.POINTER(TinvErr)], ctypes.c_int),
         "tinv_plan_exec": ([_P, ctypes.POINTER(TinvErr), ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
@@ -151,6 +152,21 @@ def dag_edges(table, barriers):
     check(L.tinv_dag_edges(_ip(table), len(table), _lp(bars), len(bars), _ip(src), _ip(dst),
                            kind.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)), ne.value, ctypes.byref(ne)))
     return src, dst, kind
+
+
+def dist_stream(table, t, P, Q):
+    """Native distribution transform -> (table, owner, dest, ref) (include/tileinv_b200.h)."""
+    L = lib()
+    table = np.ascontiguousarray(table, dtype=np.int32)
+    nout = ctypes.c_int64()
+    check(L.tinv_dist_stream(_ip(table), len(table), t, P, Q, None, 0, ctypes.byref(nout), None, None, None))
+    out = np.empty((nout.value, TASK_FIELDS), dtype=np.int32)
+    owner = np.empty(nout.value, np.int32)
+    dest = np.empty(nout.value, np.int32)
+    ref = np.empty(nout.value, np.int32)
+    check(L.tinv_dist_stream(_ip(table), len(table), t, P, Q, _ip(out), nout.value, ctypes.byref(nout), _ip(owner),
+                             _ip(dest), _ip(ref)))
+    return out, owner, dest, ref
 
 
 class Context:

@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -523,7 +524,7 @@ void scoreboard(int64_t n, const std::vector<std::vector<Acc>>& acc, const std::
   }
 }
 
-int64_t tile_key(int label, int r, int c) { return ((int64_t)label << 40) | ((int64_t)r << 20) | (int64_t)c; }
+int64_t tile_key(int label, int r, int c) { return ((int64_t)label << 36) | ((int64_t)r << 18) | (int64_t)c; }
 
 void ref_accesses(const int32_t* table, int64_t n, std::vector<std::vector<Acc>>& acc) {
   acc.resize(n);
@@ -651,6 +652,104 @@ int tinv_dag_edges(const int32_t* table, int64_t n, const int64_t* barriers, int
   return TINV_OK;
 }
 
+int tinv_dist_stream(const int32_t* table, int64_t n, int32_t t, int32_t P, int32_t Q, int32_t* out, int64_t cap,
+                     int64_t* nout, int32_t* owner, int32_t* dest, int32_t* ref) {
+  if ((!table && n > 0) || t < 1 || P < 1 || Q < 1 || P * Q > 64)
+    return fail(nullptr, TINV_ERR_BAD_ARG, "bad dist_stream arguments");
+  auto own = [&](int r, int c) { return (r % P) * Q + (c % Q); };
+  auto key = [&](const int32_t* f, int which) -> int64_t {  // which: 0 out, 1 r0, 2 r1
+    const int o = which == 0 ? F_OL : (which == 1 ? F_R0L : F_R1L);
+    return tile_key(f[o], f[o + 1], f[o + 2]);
+  };
+  // pass 1: consumer ranks of every (tile, version), version = writer task (-1: initial)
+  std::unordered_map<int64_t, int32_t> last;
+  std::unordered_map<int64_t, uint64_t> need;  // (tile key, version) -> rank mask
+  std::vector<int64_t> init_order;             // tiles whose initial version travels, first-use order
+  auto vkey = [](int64_t tk, int32_t ver) { return (tk * 1000003ll) ^ ((int64_t)(ver + 1) << 1); };
+  std::unordered_map<int64_t, std::pair<int64_t, int32_t>> vinfo;  // vkey -> (tile key, version)
+  for (int64_t v = 0; v < n; ++v) {
+    const int32_t* f = table + v * TINV_TASK_FIELDS;
+    const int rv = own(f[F_OR], f[F_OC]);
+    for (int x = 0; x < f[F_NR] && x < 2; ++x) {
+      const int o = x == 0 ? F_R0L : F_R1L;
+      if (own(f[o + 1], f[o + 2]) == rv) continue;
+      const int64_t tk = key(f, x + 1);
+      auto it = last.find(tk);
+      const int32_t ver = it == last.end() ? -1 : it->second;
+      const int64_t vk = vkey(tk, ver);
+      if (!vinfo.count(vk)) {
+        vinfo[vk] = {tk, ver};
+        if (ver < 0) init_order.push_back(tk);
+      }
+      need[vk] |= 1ull << rv;
+    }
+    last[key(f, 0)] = (int32_t)v;
+  }
+  // pass 2: emit
+  std::vector<Tk> res;
+  std::vector<int32_t> ow, de, rf;
+  std::unordered_map<int64_t, int32_t> recv_label;  // vkey * 64 + rank -> label
+  int32_t next_label = 64;
+  std::unordered_map<int64_t, std::array<int32_t, 3>> tile_of;  // tile key -> (label, row, col)
+  auto emit_sends = [&](int64_t tk, int32_t ver, int lab, int r, int c) {
+    auto it = need.find(vkey(tk, ver));
+    if (it == need.end()) return;
+    for (int d = 0; d < 64; ++d)
+      if (it->second >> d & 1) {
+        const int32_t lbl = next_label++;
+        recv_label[vkey(tk, ver) * 64 + d] = lbl;
+        Tk cp = {{TINV_COPY, TINV_STEP_COPY, r, c, -1, lbl, r, c, 2, 1, lab, r, c, -1, -1, -1}};
+        res.push_back(cp);
+        ow.push_back(own(r, c));
+        de.push_back(d);
+        rf.push_back(-1);
+      }
+  };
+  for (int64_t v = 0; v < n; ++v) {  // tiles referenced, for the initial sends
+    const int32_t* f = table + v * TINV_TASK_FIELDS;
+    for (int x = 0; x < 3; ++x) {
+      const int o = x == 0 ? F_OL : (x == 1 ? F_R0L : F_R1L);
+      if (x > 0 && f[F_NR] < x) continue;
+      tile_of[tile_key(f[o], f[o + 1], f[o + 2])] = {f[o], f[o + 1], f[o + 2]};
+    }
+  }
+  for (int64_t tk : init_order) {
+    const auto& tl = tile_of[tk];
+    emit_sends(tk, -1, tl[0], tl[1], tl[2]);
+  }
+  last.clear();
+  for (int64_t v = 0; v < n; ++v) {
+    Tk task;
+    memcpy(task.f, table + v * TINV_TASK_FIELDS, sizeof(task.f));
+    int32_t* f = task.f;
+    const int rv = own(f[F_OR], f[F_OC]);
+    for (int x = 0; x < f[F_NR] && x < 2; ++x) {
+      const int o = x == 0 ? F_R0L : F_R1L;
+      if (own(f[o + 1], f[o + 2]) == rv) continue;
+      const int64_t tk = tile_key(f[o], f[o + 1], f[o + 2]);
+      auto it = last.find(tk);
+      const int32_t ver = it == last.end() ? -1 : it->second;
+      f[o] = recv_label.at(vkey(tk, ver) * 64 + rv);
+    }
+    res.push_back(task);
+    ow.push_back(rv);
+    de.push_back(-1);
+    rf.push_back((int32_t)v);
+    const int64_t otk = tile_key(f[F_OL], f[F_OR], f[F_OC]);
+    last[otk] = (int32_t)v;
+    emit_sends(otk, (int32_t)v, f[F_OL], f[F_OR], f[F_OC]);
+  }
+  if (nout) *nout = (int64_t)res.size();
+  if (out) {
+    if (cap < (int64_t)res.size()) return fail(nullptr, TINV_ERR_BAD_ARG, "dist_stream capacity too small");
+    memcpy(out, res.data(), res.size() * sizeof(Tk));
+    memcpy(owner, ow.data(), ow.size() * 4);
+    memcpy(dest, de.data(), de.size() * 4);
+    memcpy(ref, rf.data(), rf.size() * 4);
+  }
+  return TINV_OK;
+}
+
 int tinv_plan_destroy(tinv_plan* p) {
   if (!p) return TINV_OK;
   cudaSetDevice(p->ctx->device);
@@ -695,14 +794,15 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
   std::vector<char> written_dyn;                 // per non-matrix logical: written so far
   int64_t next_logical = T;
   int64_t mm = 0;  // matrix of a batched store the task is replicated for
+  const int64_t nm = c->nmat;  // batched store: the stream is replicated per matrix (no cross edges)
   auto get_logical = [&](int label, int r, int cc, bool is_read, int64_t task, int32_t& id) -> bool {
     if (label == 0) {
       if (r < 0 || r >= t || cc < 0 || cc > r) return false;
       id = (int32_t)(mm * c->T1 + tri_index(r, cc));
       return true;
     }
-    if (label < 0 || label >= 1024 || r < 0 || r >= t || cc < 0 || cc >= t) return false;
-    const int64_t key = tile_key(label, r, cc) | (mm << 50);
+    if (label < 0 || label >= (nm > 1 ? (1 << 14) : (1 << 26)) || r < 0 || r >= t || cc < 0 || cc >= t) return false;
+    const int64_t key = tile_key((int)(mm * (1 << 14) + label), r, cc);  // < 2^27 labels x 2^18 x 2^18
     auto it = logical.find(key);
     if (it == logical.end()) {
       if (is_read) return false;  // reference: store KeyError (never written)
@@ -721,7 +821,6 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
   struct XT {
     int kind, step, out, in0, in1, mode, ref;
   };
-  const int64_t nm = c->nmat;  // batched store: the stream is replicated per matrix (no cross edges)
   if (nm > 1 && barriers && nbar > 0) {
     tinv_plan_destroy(p);
     return fail(c, TINV_ERR_BAD_ARG, "barriers are not supported on a batched store");

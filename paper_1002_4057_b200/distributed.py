@@ -1,0 +1,101 @@
+"""Multi-GPU distribution of the tile inversion.
+
+2D block-cyclic owner-computes over a P x Q grid of B200s: tile (i, j) of
+every array lives on rank (i mod P) * Q + (j mod Q) and each task runs on the
+owner of its output tile. `tinv_dist_stream` (csrc/api.cu) turns a stream into
+the distributed stream: remote reads are redirected to receive tiles, and each
+tile version a rank consumes from another owner becomes one explicit transfer
+(a write-only COPY into a fresh receive tile, so receivers never carry
+anti-dependences on in-flight data) placed right after its producer.
+
+* `execute_distributed(stream, a, grid)` runs the distributed stream with a
+  loopback transport on one B200: every rank's tasks and transfers in one
+  executor launch. Results are bitwise identical to `execute` (transfers are
+  exact copies, every tile sees the same kernel sequence), which pins the
+  transform on the hardware we have.
+* `rank_slice(dist, r)` is the stream a rank executes in a multi-process run
+  (its tasks, its outgoing transfers, its incoming receive points); the
+  message schedule is exercised with real processes and gloo in
+  tests/test_distributed.py.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .taskgen import TaskStream
+
+# flop weights in b^3 units per kind code (COPY, POTRF, TRSM, SYRK_SUB, SYRK_ADD_T,
+# GEMM, TRTRI, TRMM_LEFT, TRMM_RIGHT_NEG, TRMM_LEFT_T, LAUUM)
+_W = np.array([0.0, 1 / 3, 1.0, 1.0, 1.0, 2.0, 1 / 3, 1.0, 1.0, 1.0, 1 / 3])
+
+
+@dataclass
+class DistStream:
+    table: np.ndarray   # (m, 16) int32 distributed stream
+    owner: np.ndarray   # rank executing each task (transfers: sender)
+    dest: np.ndarray    # receiving rank of a transfer, -1 otherwise
+    ref: np.ndarray     # source task id, -1 for transfers
+    grid: tuple
+    t: int
+
+    @property
+    def world(self):
+        return self.grid[0] * self.grid[1]
+
+    def stats(self, b=1):
+        """Per-rank load (flops in b^3 units), tasks, transfers in/out, bytes in."""
+        kinds = self.table[:, 0]
+        is_x = self.dest >= 0
+        out = []
+        for r in range(self.world):
+            mine = (self.owner == r) & ~is_x
+            out.append({"rank": r, "tasks": int(mine.sum()), "flops_b3": float(_W[kinds[mine]].sum()),
+                        "sends": int(((self.owner == r) & is_x).sum()), "recvs": int((self.dest == r).sum()),
+                        "bytes_in": int((self.dest == r).sum()) * b * b * 8})
+        loads = np.array([o["flops_b3"] for o in out])
+        return {"ranks": out, "load_max_over_mean": float(loads.max() / loads.mean()) if loads.mean() else 1.0,
+                "transfers": int(is_x.sum())}
+
+
+def distribute(stream: TaskStream, grid=(1, 2), matrix_label: str = "A") -> DistStream:
+    P, Q = grid
+    table, owner, dest, ref = _native.dist_stream(stream.table(matrix_label), stream.t, P, Q)
+    return DistStream(table, owner, dest, ref, (P, Q), stream.t)
+
+
+def rank_slice(d: DistStream, r: int):
+    """Positions of the distributed stream rank r takes part in, with its role:
+    'run' (its task), 'send' (transfer it sends), 'recv' (transfer it receives)."""
+    pos = []
+    for k in range(len(d.table)):
+        if d.dest[k] >= 0:
+            if d.owner[k] == r:
+                pos.append((k, "send"))
+            elif d.dest[k] == r:
+                pos.append((k, "recv"))
+        elif d.owner[k] == r:
+            pos.append((k, "run"))
+    return pos
+
+
+def execute_distributed(stream: TaskStream, a, grid=(1, 2), trace_path=None):
+    """Run `stream` as distributed over `grid`, loopback transport on one B200.
+    Same results and errors as `execute` (task ids refer to `stream`)."""
+    from .scheduler import InvalidStreamError, _run
+    if a.t != stream.t:
+        raise InvalidStreamError(f"stream generated for t={stream.t} cannot run on a t={a.t} matrix")
+    d = distribute(stream, grid, a.label)
+    ref = np.where(d.ref >= 0, d.ref, 0)
+    bars = np.array(sorted(stream.barriers), dtype=np.int64)
+    if len(bars):  # barrier positions refer to source tasks: move them to distributed positions
+        first = {}
+        for k, v in enumerate(d.ref):
+            if v >= 0 and v not in first:
+                first[int(v)] = k
+        bars = np.array([first.get(int(p), len(d.table)) for p in bars], dtype=np.int64)
+    _run(stream, a, d.table, bars, 0, ref_ids=ref, trace_path=None)
+    return d

@@ -296,3 +296,19 @@ def test_batched_failure_reports_matrix():
     assert ei.value.matrix == 3
     assert isinstance(ei.value.cause, P.NotPositiveDefiniteError)
     assert ei.value.task.kind is P.KernelKind.POTRF
+
+
+# ---------------------------------------------------------------- multi-GPU distribution (loopback)
+@pytest.mark.parametrize("grid", [(1, 2), (2, 2), (2, 4)])
+def test_distributed_loopback_bitwise(grid):
+    from paper_1002_4057_b200.distributed import execute_distributed
+    n, b = 1024, 128
+    a = O.spd_matrix(n, 6, 0.5)
+    for cfg in (P.VariantConfig(P.Placement.OUT_OF_PLACE), P.VariantConfig(P.Placement.IN_PLACE, "UUU", False)):
+        s = P.gen_inversion(n // b, cfg)
+        ref = P.from_dense(a, b)
+        P.execute(s, ref)
+        tm = P.from_dense(a, b)
+        d = execute_distributed(s, tm, grid)
+        assert np.array_equal(P.to_dense(tm), P.to_dense(ref))
+        assert d.stats(b)["transfers"] > 0
