@@ -156,6 +156,15 @@ int tinv_dist_stream(const int32_t* table, int64_t ntasks, int32_t t, int32_t P,
 int tinv_plan_create(tinv_ctx* ctx, const int32_t* table, int64_t ntasks, int32_t stream_t,
                      const int64_t* barriers, int64_t nbar, uint32_t flags, tinv_plan** plan,
                      tinv_err* err);
+/* Plan with transfer pseudo-tasks (multi-GPU): kind 12 =
+ * SEND (reads r0: the tile version; a CTA copies it into the receiver's pool
+ * slot 2T + seq through peer memory and sets the receiver's inbox[seq]),
+ * kind 13 = RECV (writes its receive tile, pinned at slot 2T + seq; completed
+ * by the inbox poller when the data has arrived). aux[2k], aux[2k+1] = (dest
+ * rank, seq) of task k; nrecv = inbox length. Without peers attached the
+ * transfers loop back into this context (one-GPU execution of every rank). */
+int tinv_plan_create_xfer(tinv_ctx* ctx, const int32_t* table, int64_t ntasks, int32_t stream_t,
+                          const int32_t* aux, int64_t nrecv, uint32_t flags, tinv_plan** plan, tinv_err* err);
 /* run the plan on the context's matrix; blocks. ms (optional) = device time
  * of the executor launch measured with CUDA events. */
 int tinv_plan_exec(tinv_plan* plan, tinv_err* err, double* ms);

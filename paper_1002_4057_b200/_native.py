@@ -25,7 +25,7 @@ EXPORTS = (
     "tinv_abi_version", "tinv_device_count", "tinv_last_error", "tinv_create", "tinv_create_batch", "tinv_destroy",
     "tinv_shape", "tinv_set_stream", "tinv_put_dense", "tinv_get_dense", "tinv_put_dense_device", "tinv_get_dense_device",
     "tinv_put_tile", "tinv_get_tile", "tinv_gen_stream", "tinv_dag_edges", "tinv_dist_stream", "tinv_plan_create",
-    "tinv_plan_exec", "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
+    "tinv_plan_create_xfer", "tinv_plan_exec", "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
 )
 
 
@@ -82,6 +82,8 @@ def lib():
         "tinv_dist_stream": ([_I32P, _I64, _I32, _I32, _I32, _I32P, _I64, _I64P, _I32P, _I32P, _I32P], ctypes.c_int),
         "tinv_plan_create": ([_P, _I32P, _I64, _I32, _I64P, _I64, _U32, ctypes.POINTER(_P),
                               ctypes.POINTER(TinvErr)], ctypes.c_int),
+        "tinv_plan_create_xfer": ([_P, _I32P, _I64, _I32, _I32P, _I64, _U32, ctypes.POINTER(_P),
+                                   ctypes.POINTER(TinvErr)], ctypes.c_int),
         "tinv_plan_exec": ([_P, ctypes.POINTER(TinvErr), ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
         "tinv_plan_destroy": ([_P], ctypes.c_int),
         "tinv_plan_stats": ([_P, _I64P, _I64P, _I64P], ctypes.c_int),
@@ -236,6 +238,21 @@ class Plan:
                                 len(self.barriers), flags, ctypes.byref(self.h), ctypes.byref(self.err))
         self.rc = rc
         self.msg = last_error(ctx.h) if rc != OK else ""
+
+    @classmethod
+    def xfer(cls, ctx, table, t, aux, nrecv, flags=0):
+        """Plan with SEND / RECV transfer pseudo-tasks (tinv_plan_create_xfer)."""
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        self.table = np.ascontiguousarray(table, dtype=np.int32)
+        self.barriers = np.zeros(0, np.int64)
+        self.aux = np.ascontiguousarray(aux, dtype=np.int32)
+        self.h = _P()
+        self.err = TinvErr()
+        self.rc = lib().tinv_plan_create_xfer(ctx.h, _ip(self.table), len(self.table), t, _ip(self.aux), nrecv, flags,
+                                              ctypes.byref(self.h), ctypes.byref(self.err))
+        self.msg = last_error(ctx.h) if self.rc != OK else ""
+        return self
 
     def run(self):
         """-> (rc, TinvErr, device ms)."""

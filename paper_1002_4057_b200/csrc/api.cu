@@ -39,6 +39,8 @@ struct tinv_ctx {
   int64_t n = 0, b = 0, t = 0, bp = 0, R = 0, T = 0;
   int64_t nmat = 1, T1 = 0;  // batched store: nmat matrices of T1 lower tiles each (T = nmat * T1)
   double* bstage = nullptr;  // batched host transfers: whole-batch device staging
+  double* peer_pool[MAX_RANKS] = {};     // multi-GPU: peer-mapped pools (null: loopback)
+  int32_t* peer_inbox[MAX_RANKS] = {};
   int device = 0, nsm = 0;
   cudaStream_t st = nullptr, st2 = nullptr, own = nullptr;
   double* pool = nullptr;
@@ -542,6 +544,7 @@ int expected_reads(int kind) {
     case TINV_POTRF:
     case TINV_TRTRI:
     case TINV_LAUUM:
+    case KIND_RECV:
       return 0;
     case TINV_GEMM:
       return 2;
@@ -592,6 +595,9 @@ struct tinv_plan {
   int32_t* d_tsm = nullptr;
   int32_t *d_snap_from = nullptr, *d_snap_to = nullptr;
   unsigned long long* d_phase = nullptr;
+  int64_t nrecv = 0;
+  std::vector<int32_t> recv_task_h;
+  int32_t *d_recv_task = nullptr, *d_inbox = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<unsigned long long> h_ts, h_te;
   std::vector<int32_t> h_tsm;
@@ -755,7 +761,7 @@ int tinv_plan_destroy(tinv_plan* p) {
   cudaSetDevice(p->ctx->device);
   void* ptrs[] = {p->d_tasks, p->d_succ, p->d_indeg, p->d_done, p->d_cur,      p->d_alt,       p->d_queue, p->d_head,
                   p->d_tail,  p->d_ctr,  p->d_err,   p->d_progress, p->d_ts, p->d_te, p->d_tsm, p->d_snap_from,
-                  p->d_snap_to, p->d_phase};
+                  p->d_snap_to, p->d_phase, p->d_recv_task, p->d_inbox};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->ev0) cudaEventDestroy(p->ev0);
@@ -772,8 +778,12 @@ static void set_err(tinv_err* err, int32_t task, int32_t kind, int32_t code, int
   err->index = index;
 }
 
-int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, const int64_t* barriers,
-                     int64_t nbar, uint32_t flags, tinv_plan** out, tinv_err* err) {
+// aux (n x 2, or null): per-task (dest rank, receive sequence) of transfer
+// pseudo-tasks (KIND_SEND / KIND_RECV, allowed only when aux is given);
+// nrecv: inbox length (receive tiles pinned at slots 2T + seq).
+static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, const int64_t* barriers,
+                      int64_t nbar, uint32_t flags, tinv_plan** out, tinv_err* err, const int32_t* aux,
+                      int64_t nrecv) {
   set_err(err, -1, -1, TINV_OK, -1);
   if (!c || !out || (!table && n > 0)) return fail(c, TINV_ERR_BAD_ARG, "bad plan arguments");
   *out = nullptr;
@@ -819,8 +829,9 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
   last_writer_exec.assign(T, -1);
   std::unordered_map<int64_t, int32_t> inv_cache;  // (L logical << 32 | version+1) -> aux logical
   struct XT {
-    int kind, step, out, in0, in1, mode, ref;
+    int kind, step, out, in0, in1, mode, ref, aux0, aux1;
   };
+  std::unordered_map<int32_t, int32_t> recv_pin;  // receive tile -> sequence number
   if (nm > 1 && barriers && nbar > 0) {
     tinv_plan_destroy(p);
     return fail(c, TINV_ERR_BAD_ARG, "barriers are not supported on a batched store");
@@ -843,33 +854,48 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
       tinv_plan_destroy(p);
       return fail(c, TINV_ERR_STREAM, "task " + std::to_string(v) + ": " + why);
     };
-    if (kind < TINV_COPY || kind > TINV_LAUUM) return bad("unknown kernel kind");
+    const bool xfer = aux && (kind == KIND_SEND || kind == KIND_RECV);
+    if ((kind < TINV_COPY || kind > TINV_LAUUM) && !xfer) return bad("unknown kernel kind");
     if (kind == TINV_GEMM && (f[F_STEP] < 1 || f[F_STEP] > 3)) return bad("unsupported gemm shape");
     const int nr = f[F_NR];
     if (nr != expected_reads(kind)) return bad("wrong number of operands");
     int32_t in0 = -1, in1 = -1, o = -1;
     if (nr >= 1 && !get_logical(f[F_R0L], f[F_R0R], f[F_R0C], true, v, in0)) return bad("read of a missing tile");
     if (nr >= 2 && !get_logical(f[F_R1L], f[F_R1R], f[F_R1C], true, v, in1)) return bad("read of a missing tile");
+    const int32_t ax0 = aux ? aux[2 * (rv % n)] : -1, ax1 = aux ? aux[2 * (rv % n) + 1] : -1;
+    if (kind == KIND_SEND) {  // reads its tile version, writes nothing locally
+      xs.push_back({kind, 0, -1, in0, -1, 0, (int)v, ax0, ax1});
+      continue;
+    }
     if (!get_logical(f[F_OL], f[F_OR], f[F_OC], false, v, o)) return bad("output tile outside the matrix");
+    if (kind == KIND_RECV) {
+      if (ax1 < 0 || ax1 >= nrecv) return bad("receive sequence out of range");
+      recv_pin[o] = ax1;
+      written_dyn[o - T] = 1;
+      if ((int64_t)last_writer_exec.size() < next_logical) last_writer_exec.resize(next_logical, -1);
+      last_writer_exec[o] = (int32_t)xs.size();
+      xs.push_back({kind, 0, o, -1, -1, 2, (int)v, ax0, ax1});
+      continue;
+    }
     if (kind != TINV_COPY && f[F_OL] != 0 && o >= T && !written_dyn[o - T]) return bad("kernel on an unwritten tile");
     if ((int64_t)last_writer_exec.size() < next_logical) last_writer_exec.resize(next_logical, -1);
     if (kind == TINV_TRSM) {
       const int64_t key = ((int64_t)in0 << 32) | (int64_t)(last_writer_exec[in0] + 1);
       auto it = inv_cache.find(key);
-      int32_t aux;
+      int32_t inv_t;
       if (it == inv_cache.end()) {
-        aux = (int32_t)next_logical++;
+        inv_t = (int32_t)next_logical++;
         written_dyn.push_back(1);
         is_aux.resize(next_logical - T, 0);
-        is_aux[aux - T] = 1;
+        is_aux[inv_t - T] = 1;
         last_writer_exec.resize(next_logical, -1);
-        last_writer_exec[aux] = (int32_t)xs.size();
-        xs.push_back({KIND_INV, f[F_STEP], aux, in0, -1, 1, (int)v});
-        inv_cache[key] = aux;
+        last_writer_exec[inv_t] = (int32_t)xs.size();
+        xs.push_back({KIND_INV, f[F_STEP], inv_t, in0, -1, 1, (int)v, -1, -1});
+        inv_cache[key] = inv_t;
       } else {
-        aux = it->second;
+        inv_t = it->second;
       }
-      in0 = aux;
+      in0 = inv_t;
     }
     if (kind == TINV_POTRF) {  // private aux tile: inverses of the diagonal blocks of L
       in0 = (int32_t)next_logical++;
@@ -878,7 +904,7 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
     }
     if (o >= T) written_dyn[o - T] = 1;
     last_writer_exec[o] = (int32_t)xs.size();
-    xs.push_back({kind, f[F_STEP], o, in0, in1, f[F_OM] == 2 ? 2 : 1, (int)v});
+    xs.push_back({kind, f[F_STEP], o, in0, in1, f[F_OM] == 2 ? 2 : 1, (int)v, -1, -1});
   }
   first_exec_of_ref[n * nm] = (int32_t)xs.size();
   p->nexec = (int64_t)xs.size();
@@ -891,7 +917,7 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
     for (int64_t v = 0; v < nx; ++v) {
       if (xs[v].in0 >= 0 && xs[v].kind != TINV_POTRF) acc[v].push_back({xs[v].in0, 0});
       if (xs[v].in1 >= 0) acc[v].push_back({xs[v].in1, 0});
-      acc[v].push_back({xs[v].out, xs[v].mode});
+      if (xs[v].out >= 0) acc[v].push_back({xs[v].out, xs[v].mode});
     }
     std::vector<int64_t> bars;
     for (int64_t x = 0; x < (barriers ? nbar : 0); ++x) {
@@ -947,6 +973,8 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
     d.in0 = x.in0;
     d.in1 = x.in1;
     d.ref_id = x.ref;
+    d.aux0 = x.aux0;
+    d.aux1 = x.aux1;
     d.nitems = total_items(x.kind, R);
     d.nphases = (int16_t)phases_of(x.kind, R);
     d.pad = 0;
@@ -958,6 +986,7 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
       d.flags |= TF_RENAMED;
       renamed_tile[x.out] = 1;
     }
+    if (x.kind == KIND_RECV) d.flags |= TF_EXTERNAL;
     int lev = blmax > 0 ? (int)std::floor(NLEV * (1.0 - bl[u] / blmax)) : 0;
     lev = std::min(NLEV - 1, std::max(0, lev));
     d.level = (int8_t)lev;
@@ -970,7 +999,7 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
   p->tail0.assign(NLEV, 0);
   p->q_init.assign(p->q_off[NLEV], 0ull);
   for (int64_t u = 0; u < nx; ++u)
-    if (p->indeg0[u] == 0) {
+    if (p->indeg0[u] == 0 && !(p->tasks[u].flags & TF_EXTERNAL)) {
       const TaskDev& d = p->tasks[u];
       for (int i = 0; i < phase_items(d.kind, R, 0); ++i)
         p->q_init[p->q_off[d.level] + p->tail0[d.level]++] = ((unsigned long long)(u + 1) << 32) | (unsigned)i;
@@ -979,12 +1008,21 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
   // ---- slots of the non-matrix logical tiles: [2T, 2T + dyn)
   p->cur0.assign(p->nlogical, -1);
   p->alt0.assign(p->nlogical, -1);
-  int64_t next_slot = 2 * T;
+  int64_t next_slot = 2 * T + nrecv;  // receive tiles pinned at 2T + seq (same on every rank)
   for (int64_t l = T; l < p->nlogical; ++l) {
+    auto pin = recv_pin.find((int32_t)l);
+    if (pin != recv_pin.end()) {
+      p->cur0[l] = p->alt0[l] = (int32_t)(2 * T + pin->second);
+      continue;
+    }
     p->cur0[l] = (int32_t)next_slot++;
     p->alt0[l] = renamed_tile[l] ? (int32_t)next_slot++ : p->cur0[l];
   }
   p->dyn_slots = next_slot - 2 * T;
+  p->nrecv = nrecv;
+  p->recv_task_h.assign(std::max<int64_t>(nrecv, 1), -1);
+  for (int64_t u = 0; u < nx; ++u)
+    if (xs[u].kind == KIND_RECV) p->recv_task_h[xs[u].aux1] = (int32_t)u;
 
   // ---- device buffers
   auto ckm = [&](void** ptr, size_t bytes) { return cudaMalloc(ptr, std::max<size_t>(bytes, 16)); };
@@ -1011,6 +1049,11 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
       return fail(c, TINV_ERR_CUDA, "snapshot allocation failed");
     }
   }
+  if (ckm((void**)&p->d_recv_task, p->recv_task_h.size() * 4) || ckm((void**)&p->d_inbox, p->recv_task_h.size() * 4)) {
+    tinv_plan_destroy(p);
+    return fail(c, TINV_ERR_CUDA, "inbox allocation failed");
+  }
+  cudaMemcpy(p->d_recv_task, p->recv_task_h.data(), p->recv_task_h.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(p->d_tasks, p->tasks.data(), nx * sizeof(TaskDev), cudaMemcpyHostToDevice);
   if (!p->succ.empty()) cudaMemcpy(p->d_succ, p->succ.data(), p->succ.size() * 4, cudaMemcpyHostToDevice);
   if (cudaGetLastError() != cudaSuccess) {
@@ -1019,6 +1062,17 @@ int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t strea
   }
   *out = p;
   return TINV_OK;
+}
+
+int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, const int64_t* barriers,
+                     int64_t nbar, uint32_t flags, tinv_plan** out, tinv_err* err) {
+  return plan_build(c, table, n, stream_t, barriers, nbar, flags, out, err, nullptr, 0);
+}
+
+int tinv_plan_create_xfer(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, const int32_t* aux,
+                          int64_t nrecv, uint32_t flags, tinv_plan** out, tinv_err* err) {
+  if (!aux) return fail(c, TINV_ERR_BAD_ARG, "transfer plans need the aux table");
+  return plan_build(c, table, n, stream_t, nullptr, 0, flags, out, err, aux, nrecv);
 }
 
 int tinv_plan_stats(const tinv_plan* p, int64_t* exec_tasks, int64_t* items, int64_t* edges) {
@@ -1102,6 +1156,15 @@ int tinv_plan_exec(tinv_plan* p, tinv_err* err, double* ms) {
   P.trace_end = p->d_te;
   P.trace_sm = p->d_tsm;
   P.t0 = 0;
+  P.nrecv = (int32_t)p->nrecv;
+  P.recv_base = (int32_t)(2 * T);
+  P.recv_task = p->d_recv_task;
+  P.inbox = p->d_inbox;
+  for (int r = 0; r < MAX_RANKS; ++r) {  // peers: IPC-mapped pools of the other ranks, or this pool (loopback)
+    P.peer_pool[r] = c->peer_pool[r] ? c->peer_pool[r] : c->pool;
+    P.peer_inbox[r] = c->peer_inbox[r] ? c->peer_inbox[r] : p->d_inbox;
+  }
+  CK(c, cudaMemsetAsync(p->d_inbox, 0, p->recv_task_h.size() * 4, st));
   if (getenv("TINV_PHASE_PROFILE")) {
     if (!p->d_phase) CK(c, cudaMalloc(&p->d_phase, (size_t)c->nsm * NPHASE * 8));
     CK(c, cudaMemsetAsync(p->d_phase, 0, (size_t)c->nsm * NPHASE * 8, st));

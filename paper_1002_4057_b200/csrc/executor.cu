@@ -103,6 +103,14 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_acquire_sys_s32(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_s32(int32_t* p, int v) {
+  asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_release_cta_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
@@ -134,12 +142,13 @@ __device__ __forceinline__ int rho(int x) { return (x >> 1) | ((x & 1) << 2); }
 // ---------------------------------------------------------------- jobs
 enum Variant : int8_t { V_NT = 0, V_NN = 1, V_TN = 2 };
 enum JobType : int8_t { J_GEMM = 0, J_SPECIAL = 1 };
-enum Special : int8_t { SP_BPOTRF = 0, SP_BTRTRI = 1, SP_COPY_ROWS = 2 };
+enum Special : int8_t { SP_BPOTRF = 0, SP_BTRTRI = 1, SP_COPY_ROWS = 2, SP_SEND = 3 };
 
 struct ItemInfo {
   int32_t task, item, phase, kind, step;
   int32_t out_s, alt_s, in0_s, in1_s, scr_s;
   int32_t ref_id, nitems, njobs, flags;
+  int32_t aux0, aux1;
 };
 
 struct Job {
@@ -244,6 +253,10 @@ __device__ void get_job(const ItemInfo& it, int n, int R, Job& j) {
   }
   if (kind == TINV_COPY) {
     special_job(j, SP_COPY_ROWS, it.item, x, o);
+    return;
+  }
+  if (kind == KIND_SEND) {
+    special_job(j, SP_SEND, 0, x, -1);
     return;
   }
   int r, c;
@@ -896,6 +909,15 @@ __device__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams&
       }
       break;
     }
+    case SP_SEND: {  // tile version -> receiver's pool (peer memory), then its inbox flag
+      const double2* src = reinterpret_cast<const double2*>(P.pool + (int64_t)jb.src_s * P.slot_elems);
+      double2* out = reinterpret_cast<double2*>(P.peer_pool[it.aux0] + (int64_t)(P.recv_base + it.aux1) * P.slot_elems);
+      for (int64_t e = threadIdx.x; e < P.slot_elems / 2; e += 256) out[e] = __ldcg(src + e);
+      __threadfence_system();
+      cons_bar();
+      if (threadIdx.x == 0) st_release_sys_s32(P.peer_inbox[it.aux0] + it.aux1, 1);
+      break;
+    }
     case SP_COPY_ROWS: {
       const double* src = P.pool + (int64_t)jb.src_s * P.slot_elems + (int64_t)d * BLK * bp;
       double* out = dst + (int64_t)d * BLK * bp;
@@ -912,6 +934,7 @@ __device__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams&
 // ---------------------------------------------------------------- scheduler (device side)
 __device__ __forceinline__ void push_task(const ExecParams& P, int s, int phase) {
   const TaskDev& t = P.tasks[s];
+  if (t.flags & TF_EXTERNAL) return;  // RECV: completed by the inbox poller
   const int lev = t.level;
   const int n = phase_items(t.kind, P.R, phase);
   const int pos = atomicAdd(&P.q_tail[lev], n);
@@ -1092,6 +1115,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       return;
     }
+    if (warp == NCONS_WARPS + 2) {
+      // ============================ inbox poller (one per launch): completes RECV tasks
+      if (blockIdx.x != 0 || P.nrecv == 0) return;
+      for (;;) {
+        if (ld_relaxed_s32(P.abort_flag) || ld_relaxed_s32(P.remaining) <= 0) break;
+        bool any = false;
+        for (int base = 0; base < P.nrecv; base += 32) {
+          const int i = base + lane;
+          const int found = (i < P.nrecv && P.recv_task[i] >= 0 && ld_acquire_sys_s32(P.inbox + i) == 1) ? 1 : 0;
+          unsigned m = __ballot_sync(FULL, found);
+          while (m) {
+            const int idx = base + __ffs(m) - 1;
+            m &= m - 1;
+            if (lane == 0) P.inbox[idx] = 2;
+            __syncwarp();
+            complete_item(P, Rec{R_ITEM_END, P.recv_task[idx], 1, -1, 0, 0, 0, 0});
+            any = true;
+          }
+        }
+        if (!any) __nanosleep(256);
+      }
+      return;
+    }
     if (warp != NCONS_WARPS || lane != 0) return;
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmM)) : "memory");
@@ -1117,11 +1163,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       it.ref_id = t.ref_id;
       it.nitems = t.nitems;
       it.flags = t.flags;
-      it.out_s = __ldcg(P.cur_slot + t.out);
+      it.out_s = t.out >= 0 ? __ldcg(P.cur_slot + t.out) : -1;
       it.alt_s = (t.flags & TF_RENAMED) ? __ldcg(P.alt_slot + t.out) : -1;
       it.in0_s = t.in0 >= 0 ? __ldcg(P.cur_slot + t.in0) : -1;
       it.in1_s = t.in1 >= 0 ? __ldcg(P.cur_slot + t.in1) : -1;
       it.scr_s = P.scratch_base + blockIdx.x;
+      it.aux0 = t.aux0;
+      it.aux1 = t.aux1;
       it.njobs = job_count(it);
       fence_proxy_async();  // tiles written by other SMs (generic proxy) -> TMA reads
       ctl.items[slot] = it;

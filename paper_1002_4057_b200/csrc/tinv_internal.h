@@ -31,9 +31,16 @@ constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + EXTRA_SMEM + 2048;
 // shared by every TRSM reading that version of L (TRSM then runs as a
 // DMMA triangular multiply by the inverse).
 constexpr int KIND_INV = 11;
+// Multi-GPU transfer pseudo-tasks (csrc/api.cu tinv_plan_create_dist):
+// SEND copies a tile version into the receiver's pool (peer memory) and sets
+// the receiver's inbox flag; RECV is completed by the receiver's inbox poller.
+constexpr int KIND_SEND = 12;
+constexpr int KIND_RECV = 13;
+constexpr int MAX_RANKS = 8;
 
 enum TaskFlags : int32_t {
-  TF_RENAMED = 1,  // output written to the alternate slot, slots swapped at completion
+  TF_RENAMED = 1,   // output written to the alternate slot, slots swapped at completion
+  TF_EXTERNAL = 2,  // never queued: completed by the inbox poller (RECV)
 };
 
 struct TaskDev {
@@ -50,6 +57,8 @@ struct TaskDev {
   int32_t ref_id;  // reference task id (errors / trace)
   int32_t succ_begin;
   int32_t succ_end;
+  int32_t aux0;    // SEND: destination rank
+  int32_t aux1;    // SEND / RECV: receive sequence number (inbox index, slot recv_base + seq)
 };
 
 struct ExecParams {
@@ -78,6 +87,13 @@ struct ExecParams {
   int32_t* trace_sm;
   unsigned long long t0;           // globaltimer at launch (trace base)
   unsigned long long* phase;       // optional per-CTA phase cycle counters (NPHASE each)
+  // multi-GPU transfers
+  double* peer_pool[MAX_RANKS];    // pools of the ranks (peer-mapped; the local pool for self)
+  int32_t* peer_inbox[MAX_RANKS];  // inbox flag arrays of the ranks
+  int32_t* inbox;                  // this rank's inbox flags (1 = arrived, 2 = consumed)
+  const int32_t* recv_task;        // inbox index -> exec task id (-1: not received here)
+  int32_t nrecv;                   // inbox length
+  int32_t recv_base;               // slot of receive sequence number 0 (same on every rank)
 };
 constexpr int NPHASE = 20;  // item-wait, mainloop, epilogue, job-end, item-end, completion, items, jobs,
                             // special: load, factor, inverse, store
@@ -98,6 +114,7 @@ inline int64_t tri_index(int64_t i, int64_t j) { return i * (i + 1) / 2 + j; }
 //    s >= 1: X[r][r-s] for r = s..R-1 (R-s items, two block GEMMs each).
 //  everything else: one phase.
 TINV_HD int phases_of(int kind, int R) {
+  if (kind == KIND_SEND || kind == KIND_RECV) return 1;
   if (kind == TINV_POTRF) return 3 * R - 2;
   if (kind == TINV_TRTRI || kind == KIND_INV) return R;
   return 1;
@@ -117,6 +134,9 @@ TINV_HD int phase_items(int kind, int R, int p) {
       return R * (R + 1) / 2;
     case TINV_COPY:
       return R;
+    case KIND_SEND:
+    case KIND_RECV:
+      return 1;
     default:
       return R * R;
   }

@@ -13,6 +13,12 @@ anti-dependences on in-flight data) placed right after its producer.
   executor launch. Results are bitwise identical to `execute` (transfers are
   exact copies, every tile sees the same kernel sequence), which pins the
   transform on the hardware we have.
+* `transfer_plan(dist, rank)` turns transfers into device SEND / RECV
+  pseudo-tasks: a CTA copies the version into the receiver's pool (peer
+  memory over NVLink) and sets its inbox flag with a system-scope release; the
+  receiver's inbox poller completes the RECV. `execute_distributed(...,
+  transport="device")` runs every rank's plan in one launch with the local
+  pool standing in for the peers -- the exact device protocol, on one GPU.
 * `rank_slice(dist, r)` is the stream a rank executes in a multi-process run
   (its tasks, its outgoing transfers, its incoming receive points); the
   message schedule is exercised with real processes and gloo in
@@ -82,13 +88,71 @@ def rank_slice(d: DistStream, r: int):
     return pos
 
 
-def execute_distributed(stream: TaskStream, a, grid=(1, 2), trace_path=None):
-    """Run `stream` as distributed over `grid`, loopback transport on one B200.
-    Same results and errors as `execute` (task ids refer to `stream`)."""
-    from .scheduler import InvalidStreamError, _run
+def transfer_plan(d: DistStream, rank: int = -1):
+    """Table + aux (dest, seq) + inbox length with SEND / RECV pseudo-tasks.
+
+    rank -1: every rank's tasks (one-GPU execution, sequence = transfer index);
+    rank r: the tasks of rank r, sequence numbers counted per receiver."""
+    rows, aux, src = [], [], []
+    per_dest = {}
+    nrecv = 0
+    for k in range(len(d.table)):
+        f = d.table[k]
+        if d.dest[k] < 0:
+            if rank < 0 or d.owner[k] == rank:
+                rows.append(f)
+                aux.append((-1, -1))
+                src.append(int(d.ref[k]))
+            continue
+        dst, snd = int(d.dest[k]), int(d.owner[k])
+        if rank < 0:
+            seq = nrecv
+        else:
+            seq = per_dest.get(dst, 0)
+            per_dest[dst] = seq + 1
+        send = np.full(16, -1, np.int32)
+        send[0], send[1], send[8], send[9] = 12, 0, 0, 1
+        send[10:13] = f[10:13]
+        recv = np.full(16, -1, np.int32)
+        recv[0], recv[1], recv[8], recv[9] = 13, 0, 2, 0
+        recv[5:8] = f[5:8]
+        if rank < 0 or snd == rank:
+            rows.append(send)
+            aux.append((dst, seq))
+            src.append(-1)
+        if rank < 0 or dst == rank:
+            rows.append(recv)
+            aux.append((dst, seq))
+            src.append(-1)
+        if rank < 0 or dst == rank:
+            nrecv = max(nrecv, seq + 1)
+    return np.array(rows, np.int32), np.array(aux, np.int32), nrecv, np.array(src, np.int64)
+
+
+def execute_distributed(stream: TaskStream, a, grid=(1, 2), transport="loopback"):
+    """Run `stream` as distributed over `grid` on one B200: transport
+    "loopback" (transfers as device copies) or "device" (the SEND / RECV
+    protocol with the local pool standing in for peers). Same results and
+    errors as `execute` (task ids refer to `stream`)."""
+    from .scheduler import ExecutionError, InvalidStreamError, _cause, _run
+    from .tile_matrix import _DEVICE
     if a.t != stream.t:
         raise InvalidStreamError(f"stream generated for t={stream.t} cannot run on a t={a.t} matrix")
     d = distribute(stream, grid, a.label)
+    if transport == "device":
+        table, aux, nrecv, src = transfer_plan(d, -1)
+        ctx = a._device()
+        plan = _native.Plan.xfer(ctx, table, stream.t, aux, nrecv)
+        rc, err, _ = plan.run()
+        msg = plan.msg
+        plan.close()
+        if rc != _native.OK:
+            if err.task_id < 0 or src[err.task_id] < 0:
+                raise _native.NativeError(rc, msg)
+            cause = _cause(err, msg)
+            raise ExecutionError(stream.tasks[int(src[err.task_id])], cause) from cause
+        a._state = _DEVICE
+        return d
     ref = np.where(d.ref >= 0, d.ref, 0)
     bars = np.array(sorted(stream.barriers), dtype=np.int64)
     if len(bars):  # barrier positions refer to source tasks: move them to distributed positions

@@ -312,3 +312,18 @@ def test_distributed_loopback_bitwise(grid):
         d = execute_distributed(s, tm, grid)
         assert np.array_equal(P.to_dense(tm), P.to_dense(ref))
         assert d.stats(b)["transfers"] > 0
+
+
+@pytest.mark.parametrize("grid", [(1, 2), (2, 2), (2, 4)])
+def test_distributed_device_transport_bitwise(grid):
+    # SEND (CTA copy into the receiver's pool + system-scope inbox flag) and
+    # RECV (completed by the inbox poller), every rank in one launch
+    from paper_1002_4057_b200.distributed import execute_distributed
+    n, b = 1024, 128
+    a = O.spd_matrix(n, 7, 0.5)
+    s = P.gen_inversion(n // b, P.VariantConfig(P.Placement.OUT_OF_PLACE))
+    ref = P.from_dense(a, b)
+    P.execute(s, ref)
+    tm = P.from_dense(a, b)
+    execute_distributed(s, tm, grid, transport="device")
+    assert np.array_equal(P.to_dense(tm), P.to_dense(ref))
