@@ -260,7 +260,7 @@ def main():
         return float(v.item())
 
     # input on the device
-    gen = torch.Generator(device="cuda").manual_seed(rank)
+    gen = torch.Generator(device="cuda").manual_seed(rank if world > 1 and batch > 1 else 0)
     if batch == 1:
         g = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=gen)
         a = torch.matmul(g, g.T)
@@ -285,7 +285,27 @@ def main():
     s = P.gen_inversion(t, P.VariantConfig(P.Placement(args.placement), args.loops, pipelined))
     table = s.table()
     bars = np.array(sorted(s.barriers), dtype=np.int64)
-    plan = _native.Plan(ctx, table, t, bars)
+
+    # N > 1: one matrix distributed over all ranks (2D block-cyclic, tile
+    # versions sent GPU to GPU through peer memory) -- strong scaling. If the
+    # distributed setup fails, fall back to independent replicas and say why.
+    mg = None
+    scaling = "weak"
+    if world > 1 and batch == 1:
+        try:
+            from paper_1002_4057_b200.distributed import MultiGPU, owned_mask
+            if pipelined is False:
+                raise RuntimeError("the distributed run is pipelined only")
+            mg = MultiGPU(s, ctx)
+            scaling = "strong"
+            st = mg.dist.stats(nb)
+            config["parallelism"] = f"2d-block-cyclic {mg.grid[0]}x{mg.grid[1]} (tile versions over NVLink peer memory)"
+            config["load_max_over_mean"] = st["load_max_over_mean"]
+            config["transfers"] = st["transfers"]
+        except Exception as exc:  # noqa: BLE001 -- report and fall back
+            mg = None
+            config["parallelism"] = f"replicas x{world} (distributed setup failed: {type(exc).__name__}: {exc})"[:300]
+    plan = mg.plan if mg is not None else _native.Plan(ctx, table, t, bars)
     if plan.rc != 0:
         raise RuntimeError(plan.msg)
     stats = plan.stats()
@@ -294,11 +314,11 @@ def main():
 
     def step():
         ctx.put_dense_device(a.data_ptr(), n)
-        rc, err, ms = plan.run()
+        rc, err, ms = mg.run() if mg is not None else plan.run()
         if rc != 0:
             raise RuntimeError(f"executor failed: {plan.msg} task {err.task_id}")
         kern_ms.append(ms)
-        ctx.get_dense_device(x.data_ptr(), n, _native.DENSE_SYMMETRIZE)
+        ctx.get_dense_device(x.data_ptr(), n, _native.DENSE_LOWER if mg is not None else _native.DENSE_SYMMETRIZE)
 
     for _ in range(args.warmup):
         step()
@@ -315,9 +335,15 @@ def main():
         barrier()
     ms_total = max_over_ranks(sum(e0.elapsed_time(e1) for e0, e1 in evs))
     ms_step = ms_total / args.steps
-    value = world * flops / (ms_step * 1e-3) / 1e9
-    kern_avg = statistics.mean(kern_ms)
-    achieved = flops / (kern_avg * 1e-3) / 1e12
+    jobs = 1 if mg is not None else world  # distributed: all ranks share one matrix per step
+    value = jobs * flops / (ms_step * 1e-3) / 1e9
+    kern_avg = max_over_ranks(statistics.mean(kern_ms))
+    achieved = flops / (world if mg is not None else 1) / (kern_avg * 1e-3) / 1e12
+    if mg is not None:  # gather the owned tiles for the check below
+        x *= owned_mask(n, nb, mg.grid, rank, "cuda")
+        import torch.distributed as tdist
+        tdist.all_reduce(x)
+        x = torch.tril(x) + torch.tril(x, -1).T
 
     # numerical check of the last step (outside the timed region)
     eye = torch.eye(n, dtype=torch.float64, device="cuda")
@@ -330,7 +356,10 @@ def main():
 
     # end to end through the C-ABI with pinned host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and mg is not None:
+        e2e = {"value": None, "unit": "Gflop/s", "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+               "note": "not measured for the distributed run (plans are bound to the exported stores)"}
+    elif not args.no_e2e:
         ha = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
         ha.copy_(a)
         hx = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
@@ -383,7 +412,7 @@ def main():
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "Gflop/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / DMMA_PEAK_TFLOPS, "traffic": traffic,
@@ -393,7 +422,7 @@ def main():
                          "algorithmic": f"n^3 = {flops:.3e} flop per launch",
                          "peak_source": "measured FP64 DMMA peak (tools/fp64_peak.cu); cuBLAS DGEMM "
                                         f"{DGEMM_TFLOPS} TF/s for context; MEASURED_PEAKS.json has no FP64 entry"},
-            "pct_fp64_peak": 100.0 * value / world / 1e3 / DMMA_PEAK_TFLOPS,
+            "pct_fp64_peak": 100.0 * value / world / 1e3 / DMMA_PEAK_TFLOPS,  # per GPU
             "kernel_ms": kern_avg, "plan": stats,
             "residual": res, "symmetry_err": sym_err,
             "gpu_launches": 3 * args.steps,

@@ -165,6 +165,15 @@ int tinv_plan_create(tinv_ctx* ctx, const int32_t* table, int64_t ntasks, int32_
  * transfers loop back into this context (one-GPU execution of every rank). */
 int tinv_plan_create_xfer(tinv_ctx* ctx, const int32_t* table, int64_t ntasks, int32_t stream_t,
                           const int32_t* aux, int64_t nrecv, uint32_t flags, tinv_plan** plan, tinv_err* err);
+/* Multi-process runs (one rank per B200 of a node): size the store for
+ * `plan` and export this rank's pool and inbox as CUDA IPC handles (64 bytes
+ * each); after the exchange, map every peer (handles in rank order). Call
+ * tinv_ipc_reset on every rank, then a barrier across ranks, before each
+ * tinv_plan_exec of a transfer plan. The store cannot grow once exported. */
+int tinv_ipc_export(tinv_ctx* ctx, tinv_plan* plan, void* pool_handle, void* inbox_handle);
+int tinv_ipc_open(tinv_ctx* ctx, int32_t rank, int32_t world, const void* pool_handles,
+                  const void* inbox_handles);
+int tinv_ipc_reset(tinv_ctx* ctx);
 /* run the plan on the context's matrix; blocks. ms (optional) = device time
  * of the executor launch measured with CUDA events. */
 int tinv_plan_exec(tinv_plan* plan, tinv_err* err, double* ms);

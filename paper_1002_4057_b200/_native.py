@@ -25,7 +25,8 @@ EXPORTS = (
     "tinv_abi_version", "tinv_device_count", "tinv_last_error", "tinv_create", "tinv_create_batch", "tinv_destroy",
     "tinv_shape", "tinv_set_stream", "tinv_put_dense", "tinv_get_dense", "tinv_put_dense_device", "tinv_get_dense_device",
     "tinv_put_tile", "tinv_get_tile", "tinv_gen_stream", "tinv_dag_edges", "tinv_dist_stream", "tinv_plan_create",
-    "tinv_plan_create_xfer", "tinv_plan_exec", "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
+    "tinv_plan_create_xfer", "tinv_ipc_export", "tinv_ipc_open", "tinv_ipc_reset", "tinv_plan_exec",
+    "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
 )
 
 
@@ -84,6 +85,9 @@ def lib():
                               ctypes.POINTER(TinvErr)], ctypes.c_int),
         "tinv_plan_create_xfer": ([_P, _I32P, _I64, _I32, _I32P, _I64, _U32, ctypes.POINTER(_P),
                                    ctypes.POINTER(TinvErr)], ctypes.c_int),
+        "tinv_ipc_export": ([_P, _P, ctypes.c_char_p, ctypes.c_char_p], ctypes.c_int),
+        "tinv_ipc_open": ([_P, _I32, _I32, ctypes.c_char_p, ctypes.c_char_p], ctypes.c_int),
+        "tinv_ipc_reset": ([_P], ctypes.c_int),
         "tinv_plan_exec": ([_P, ctypes.POINTER(TinvErr), ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
         "tinv_plan_destroy": ([_P], ctypes.c_int),
         "tinv_plan_stats": ([_P, _I64P, _I64P, _I64P], ctypes.c_int),
@@ -199,6 +203,12 @@ class Context:
         """Launch on a caller-owned cudaStream_t (int handle); 0 -> own stream."""
         check(lib().tinv_set_stream(self.h, ctypes.c_void_p(stream_ptr or None)), self.h)
 
+    def ipc_open(self, rank, world, pool_handles, inbox_handles):
+        check(lib().tinv_ipc_open(self.h, rank, world, b"".join(pool_handles), b"".join(inbox_handles)), self.h)
+
+    def ipc_reset(self):
+        check(lib().tinv_ipc_reset(self.h), self.h)
+
     def put_dense(self, m):
         m = np.ascontiguousarray(m, dtype=np.float64)
         check(lib().tinv_put_dense(self.h, _dp(m), m.shape[-1]), self.h)
@@ -262,6 +272,13 @@ class Plan:
         rc = lib().tinv_plan_exec(self.h, ctypes.byref(self.err), ctypes.byref(ms))
         self.msg = last_error(self.ctx.h) if rc != OK else ""
         return rc, self.err, ms.value
+
+    def ipc_export(self):
+        """-> (pool handle, inbox handle), 64 bytes each (CUDA IPC)."""
+        hp = ctypes.create_string_buffer(64)
+        hi = ctypes.create_string_buffer(64)
+        check(lib().tinv_ipc_export(self.ctx.h, self.h, hp, hi), self.ctx.h)
+        return hp.raw, hi.raw
 
     def stats(self):
         a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()

@@ -41,6 +41,10 @@ struct tinv_ctx {
   double* bstage = nullptr;  // batched host transfers: whole-batch device staging
   double* peer_pool[MAX_RANKS] = {};     // multi-GPU: peer-mapped pools (null: loopback)
   int32_t* peer_inbox[MAX_RANKS] = {};
+  int32_t* inbox = nullptr;              // exported inbox (multi-process)
+  int64_t inbox_len = 0;
+  bool exported = false;                 // pool mapped by peers: must not move
+  int rank = -1, world = 0;
   int device = 0, nsm = 0;
   cudaStream_t st = nullptr, st2 = nullptr, own = nullptr;
   double* pool = nullptr;
@@ -107,6 +111,7 @@ static int make_maps(tinv_ctx* c) {
 // grow the slot pool to at least `slots`, keeping the matrix region [0, 2T)
 static int ensure_pool(tinv_ctx* c, int64_t slots) {
   if (slots <= c->pool_slots) return TINV_OK;
+  if (c->exported) return fail(c, TINV_ERR_BAD_ARG, "tile store is mapped by peer ranks and cannot grow");
   CK(c, cudaSetDevice(c->device));
   double* np = nullptr;
   CK(c, cudaMalloc(&np, (size_t)slots * c->slot_elems * 8));
@@ -199,6 +204,12 @@ int tinv_destroy(tinv_ctx* c) {
   if (c->pool) cudaFree(c->pool);
   if (c->d_a_slot) cudaFree(c->d_a_slot);
   if (c->bstage) cudaFree(c->bstage);
+  for (int r = 0; r < MAX_RANKS; ++r) {
+    if (r == c->rank) continue;
+    if (c->peer_pool[r]) cudaIpcCloseMemHandle(c->peer_pool[r]);
+    if (c->peer_inbox[r]) cudaIpcCloseMemHandle(c->peer_inbox[r]);
+  }
+  if (c->inbox) cudaFree(c->inbox);
   for (auto& s : c->staging)
     if (s) cudaFree(s);
   if (c->own) cudaStreamDestroy(c->own);
@@ -1075,6 +1086,61 @@ int tinv_plan_create_xfer(tinv_ctx* c, const int32_t* table, int64_t n, int32_t 
   return plan_build(c, table, n, stream_t, nullptr, 0, flags, out, err, aux, nrecv);
 }
 
+int tinv_ipc_export(tinv_ctx* c, tinv_plan* p, void* pool_handle, void* inbox_handle) {
+  if (!c || !p || !pool_handle || !inbox_handle) return fail(c, TINV_ERR_BAD_ARG, "bad ipc_export arguments");
+  CK(c, cudaSetDevice(c->device));
+  const int64_t need = 2 * c->T + p->dyn_slots + c->nsm + ((p->flags & TINV_KEEP_ON_FAILURE) ? c->T : 0);
+  int rc = ensure_pool(c, need);
+  if (rc) return rc;
+  if (!c->inbox || c->inbox_len < std::max<int64_t>(p->nrecv, 1)) {
+    if (c->exported) return fail(c, TINV_ERR_BAD_ARG, "inbox already exported");
+    if (c->inbox) cudaFree(c->inbox);
+    c->inbox_len = std::max<int64_t>(p->nrecv, 1);
+    CK(c, cudaMalloc(&c->inbox, c->inbox_len * 4));
+    CK(c, cudaMemset(c->inbox, 0, c->inbox_len * 4));
+  }
+  cudaIpcMemHandle_t hp, hi;
+  CK(c, cudaIpcGetMemHandle(&hp, c->pool));
+  CK(c, cudaIpcGetMemHandle(&hi, c->inbox));
+  memcpy(pool_handle, &hp, sizeof(hp));
+  memcpy(inbox_handle, &hi, sizeof(hi));
+  c->exported = true;
+  return TINV_OK;
+}
+
+int tinv_ipc_open(tinv_ctx* c, int32_t rank, int32_t world, const void* pool_handles, const void* inbox_handles) {
+  if (!c || rank < 0 || world < 1 || world > MAX_RANKS || rank >= world || !pool_handles || !inbox_handles)
+    return fail(c, TINV_ERR_BAD_ARG, "bad ipc_open arguments");
+  if (!c->exported) return fail(c, TINV_ERR_BAD_ARG, "export this rank's store first");
+  CK(c, cudaSetDevice(c->device));
+  c->rank = rank;
+  c->world = world;
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) {
+      c->peer_pool[r] = c->pool;
+      c->peer_inbox[r] = c->inbox;
+      continue;
+    }
+    cudaIpcMemHandle_t hp, hi;
+    memcpy(&hp, (const char*)pool_handles + r * sizeof(hp), sizeof(hp));
+    memcpy(&hi, (const char*)inbox_handles + r * sizeof(hi), sizeof(hi));
+    void *pp = nullptr, *pi = nullptr;
+    CK(c, cudaIpcOpenMemHandle(&pp, hp, cudaIpcMemLazyEnablePeerAccess));
+    CK(c, cudaIpcOpenMemHandle(&pi, hi, cudaIpcMemLazyEnablePeerAccess));
+    c->peer_pool[r] = (double*)pp;
+    c->peer_inbox[r] = (int32_t*)pi;
+  }
+  return TINV_OK;
+}
+
+int tinv_ipc_reset(tinv_ctx* c) {
+  if (!c || !c->inbox) return fail(c, TINV_ERR_BAD_ARG, "no exported inbox");
+  CK(c, cudaSetDevice(c->device));
+  CK(c, cudaMemset(c->inbox, 0, c->inbox_len * 4));
+  CK(c, cudaDeviceSynchronize());
+  return TINV_OK;
+}
+
 int tinv_plan_stats(const tinv_plan* p, int64_t* exec_tasks, int64_t* items, int64_t* edges) {
   if (!p) return TINV_ERR_BAD_ARG;
   if (exec_tasks) *exec_tasks = p->nexec;
@@ -1160,11 +1226,16 @@ int tinv_plan_exec(tinv_plan* p, tinv_err* err, double* ms) {
   P.recv_base = (int32_t)(2 * T);
   P.recv_task = p->d_recv_task;
   P.inbox = p->d_inbox;
+  if (c->inbox) {  // multi-process: the exported inbox, zeroed by tinv_ipc_reset before the ranks' barrier
+    if (c->inbox_len < p->nrecv) return fail(c, TINV_ERR_BAD_ARG, "exported inbox smaller than the plan's");
+    P.inbox = c->inbox;
+  } else {
+    CK(c, cudaMemsetAsync(p->d_inbox, 0, p->recv_task_h.size() * 4, st));
+  }
   for (int r = 0; r < MAX_RANKS; ++r) {  // peers: IPC-mapped pools of the other ranks, or this pool (loopback)
     P.peer_pool[r] = c->peer_pool[r] ? c->peer_pool[r] : c->pool;
-    P.peer_inbox[r] = c->peer_inbox[r] ? c->peer_inbox[r] : p->d_inbox;
+    P.peer_inbox[r] = c->peer_inbox[r] ? c->peer_inbox[r] : P.inbox;
   }
-  CK(c, cudaMemsetAsync(p->d_inbox, 0, p->recv_task_h.size() * 4, st));
   if (getenv("TINV_PHASE_PROFILE")) {
     if (!p->d_phase) CK(c, cudaMalloc(&p->d_phase, (size_t)c->nsm * NPHASE * 8));
     CK(c, cudaMemsetAsync(p->d_phase, 0, (size_t)c->nsm * NPHASE * 8, st));

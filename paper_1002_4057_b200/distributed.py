@@ -163,3 +163,107 @@ def execute_distributed(stream: TaskStream, a, grid=(1, 2), transport="loopback"
         bars = np.array([first.get(int(p), len(d.table)) for p in bars], dtype=np.int64)
     _run(stream, a, d.table, bars, 0, ref_ids=ref, trace_path=None)
     return d
+
+
+def default_grid(world: int):
+    """P x Q with P <= Q, as square as possible (1x2, 2x2, 2x4, ...)."""
+    p = int(np.sqrt(world))
+    while world % p:
+        p -= 1
+    return (p, world // p)
+
+
+def owned_mask(n, b, grid, rank, device):
+    """(n, n) float mask of the lower tiles rank owns (2D block-cyclic)."""
+    import torch
+    t = n // b
+    P, Q = grid
+    m = torch.zeros((t, t), dtype=torch.float64, device=device)
+    for i in range(t):
+        for j in range(i + 1):
+            if (i % P) * Q + (j % Q) == rank:
+                m[i, j] = 1.0
+    return m.repeat_interleave(b, 0).repeat_interleave(b, 1)
+
+
+class MultiGPU:
+    """One rank of a multi-process run (torch.distributed, one B200 per rank).
+
+    Builds the rank's transfer plan from the distributed stream, exports its
+    tile store and inbox (CUDA IPC) and maps every peer's, so SEND work items
+    write tile versions straight into the receivers' pools over NVLink."""
+
+    def __init__(self, stream: TaskStream, ctx, grid=None, matrix_label="A"):
+        import torch.distributed as dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.grid = grid or default_grid(self.world)
+        if self.grid[0] * self.grid[1] != self.world:
+            raise ValueError(f"grid {self.grid} does not match world size {self.world}")
+        self.stream, self.ctx = stream, ctx
+        self.dist = distribute(stream, self.grid, matrix_label)
+        table, aux, nrecv, self.src = transfer_plan(self.dist, self.rank)
+        self.plan = _native.Plan.xfer(ctx, table, stream.t, aux, nrecv)
+        ok = _agree(self.plan.rc == _native.OK)
+        if not ok:
+            raise _native.NativeError(self.plan.rc, self.plan.msg or "plan failed on a peer rank")
+        hp, hi = self.plan.ipc_export()
+        hs = [None] * self.world
+        dist.all_gather_object(hs, (hp, hi))
+        ctx.ipc_open(self.rank, self.world, [h[0] for h in hs], [h[1] for h in hs])
+
+    def run(self):
+        """Every rank: reset inbox, barrier, execute. -> (rc, err, device ms)."""
+        import torch.distributed as dist
+        self.ctx.ipc_reset()
+        dist.barrier()
+        return self.plan.run()
+
+
+def _agree(flag: bool) -> bool:
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    v = torch.tensor([0 if flag else 1], device=dev)
+    dist.all_reduce(v)
+    return int(v.item()) == 0
+
+
+def execute_multi_gpu(stream: TaskStream, a, grid=None):
+    """`execute` over all ranks of the default process group (one B200 each):
+    every rank passes the same stream and matrix; on return every rank's `a`
+    holds the full result (owned tiles all-reduced over NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    from .scheduler import ExecutionError, InvalidStreamError, _cause
+    from .tile_matrix import _NONE
+    if a.t != stream.t:
+        raise InvalidStreamError(f"stream generated for t={stream.t} cannot run on a t={a.t} matrix")
+    dev = torch.cuda.current_device()
+    ctx = a._device(dev)
+    mg = MultiGPU(stream, ctx, grid, a.label)
+    rc, err, _ = mg.run()
+    src_id = int(mg.src[err.task_id]) if rc != _native.OK and 0 <= err.task_id < len(mg.src) else -1
+    info = torch.tensor([src_id if src_id >= 0 else 2 ** 62, err.code, err.index, rc], dtype=torch.int64,
+                        device="cuda")
+    allinfo = [torch.zeros_like(info) for _ in range(mg.world)]
+    dist.all_gather(allinfo, info)
+    fails = [x.tolist() for x in allinfo if x[3] != 0]
+    if fails:
+        a._state = _NONE
+        tid, code, index, r = min(fails)
+        if tid >= 2 ** 62:
+            raise _native.NativeError(r, "multi-GPU execution failed")
+        e = _native.TinvErr(int(tid), -1, int(code), int(index))
+        cause = _cause(e, "")
+        raise ExecutionError(stream.tasks[int(tid)], cause) from cause
+    x = torch.zeros((a.n, a.n), dtype=torch.float64, device="cuda")
+    ctx.get_dense_device(x.data_ptr(), a.n, _native.DENSE_LOWER)
+    x *= owned_mask(a.n, a.b, mg.grid, mg.rank, "cuda")
+    dist.all_reduce(x)
+    full = x.cpu().numpy()
+    b = a.b
+    for i in range(a.t):  # lower tiles only: the strictly-upper tiles keep the stale input (tile_matrix.py:30-33)
+        a._host[i * b:(i + 1) * b, :(i + 1) * b] = full[i * b:(i + 1) * b, :(i + 1) * b]
+    a._state = _NONE
+    return a
