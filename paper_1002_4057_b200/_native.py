@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libtileinv_b200.so")
+LIB_PATH = os.environ.get("TINV_LIB") or os.path.join(_PKG, "libtileinv_b200.so")
 
 TASK_FIELDS = 16
 OK, ERR_NOT_SPD, ERR_SINGULAR, ERR_BAD_ARG, ERR_CUDA, ERR_STREAM, ERR_NO_DEVICE, ERR_INTERNAL = range(8)

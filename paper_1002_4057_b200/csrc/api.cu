@@ -840,7 +840,7 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
   last_writer_exec.assign(T, -1);
   std::unordered_map<int64_t, int32_t> inv_cache;  // (L logical << 32 | version+1) -> aux logical
   struct XT {
-    int kind, step, out, in0, in1, mode, ref, aux0, aux1;
+    int kind, step, out, in0, in1, mode, ref, aux0, aux1, flags;
   };
   std::unordered_map<int32_t, int32_t> recv_pin;  // receive tile -> sequence number
   if (nm > 1 && barriers && nbar > 0) {
@@ -875,7 +875,7 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
     if (nr >= 2 && !get_logical(f[F_R1L], f[F_R1R], f[F_R1C], true, v, in1)) return bad("read of a missing tile");
     const int32_t ax0 = aux ? aux[2 * (rv % n)] : -1, ax1 = aux ? aux[2 * (rv % n) + 1] : -1;
     if (kind == KIND_SEND) {  // reads its tile version, writes nothing locally
-      xs.push_back({kind, 0, -1, in0, -1, 0, (int)v, ax0, ax1});
+      xs.push_back({kind, 0, -1, in0, -1, 0, (int)v, ax0, ax1, 0});
       continue;
     }
     if (!get_logical(f[F_OL], f[F_OR], f[F_OC], false, v, o)) return bad("output tile outside the matrix");
@@ -885,11 +885,31 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
       written_dyn[o - T] = 1;
       if ((int64_t)last_writer_exec.size() < next_logical) last_writer_exec.resize(next_logical, -1);
       last_writer_exec[o] = (int32_t)xs.size();
-      xs.push_back({kind, 0, o, -1, -1, 2, (int)v, ax0, ax1});
+      xs.push_back({kind, 0, o, -1, -1, 2, (int)v, ax0, ax1, 0});
       continue;
     }
     if (kind != TINV_COPY && f[F_OL] != 0 && o >= T && !written_dyn[o - T]) return bad("kernel on an unwritten tile");
     if ((int64_t)last_writer_exec.size() < next_logical) last_writer_exec.resize(next_logical, -1);
+    int xflags = 0;
+    // the factor's diagonal-block inverses computed by POTRF (its aux tile)
+    auto potrf_aux = [&](int32_t tile) -> int32_t {
+      const int32_t w = last_writer_exec[tile];
+      return (w >= 0 && xs[w].kind == TINV_POTRF) ? xs[w].in0 : -1;
+    };
+    if (kind == TINV_TRTRI) {  // TRTRI of an unchanged factor: reuse INV's inverse, or POTRF's diagonal blocks
+      const int64_t key = ((int64_t)o << 32) | (int64_t)(last_writer_exec[o] + 1);
+      auto it = inv_cache.find(key);
+      if (it != inv_cache.end()) {
+        last_writer_exec[o] = (int32_t)xs.size();
+        xs.push_back({TINV_COPY, TINV_STEP_COPY, o, it->second, -1, 1, (int)v, -1, -1, 0});
+        continue;
+      }
+      const int32_t pa = potrf_aux(o);
+      if (pa >= 0) {
+        in1 = pa;
+        xflags = TF_DIAG_FROM_AUX;
+      }
+    }
     if (kind == TINV_TRSM) {
       const int64_t key = ((int64_t)in0 << 32) | (int64_t)(last_writer_exec[in0] + 1);
       auto it = inv_cache.find(key);
@@ -901,7 +921,8 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
         is_aux[inv_t - T] = 1;
         last_writer_exec.resize(next_logical, -1);
         last_writer_exec[inv_t] = (int32_t)xs.size();
-        xs.push_back({KIND_INV, f[F_STEP], inv_t, in0, -1, 1, (int)v, -1, -1});
+        const int32_t pa = potrf_aux(in0);
+        xs.push_back({KIND_INV, f[F_STEP], inv_t, in0, pa, 1, (int)v, -1, -1, pa >= 0 ? TF_DIAG_FROM_AUX : 0});
         inv_cache[key] = inv_t;
       } else {
         inv_t = it->second;
@@ -915,7 +936,7 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
     }
     if (o >= T) written_dyn[o - T] = 1;
     last_writer_exec[o] = (int32_t)xs.size();
-    xs.push_back({kind, f[F_STEP], o, in0, in1, f[F_OM] == 2 ? 2 : 1, (int)v, -1, -1});
+    xs.push_back({kind, f[F_STEP], o, in0, in1, f[F_OM] == 2 ? 2 : 1, (int)v, -1, -1, xflags});
   }
   first_exec_of_ref[n * nm] = (int32_t)xs.size();
   p->nexec = (int64_t)xs.size();
@@ -987,9 +1008,9 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
     d.aux0 = x.aux0;
     d.aux1 = x.aux1;
     d.nitems = total_items(x.kind, R);
-    d.nphases = (int16_t)phases_of(x.kind, R);
+    d.nphases = (int16_t)ngroups(x.kind, R);
     d.pad = 0;
-    d.flags = 0;
+    d.flags = (int8_t)x.flags;
     const bool alias = (x.in0 == x.out || x.in1 == x.out);
     if (x.kind == TINV_TRMM_LEFT || x.kind == TINV_TRMM_RIGHT_NEG || x.kind == TINV_TRMM_LEFT_T ||
         x.kind == TINV_LAUUM || x.kind == TINV_TRSM || x.kind == TINV_TRTRI ||
@@ -1012,7 +1033,7 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
   for (int64_t u = 0; u < nx; ++u)
     if (p->indeg0[u] == 0 && !(p->tasks[u].flags & TF_EXTERNAL)) {
       const TaskDev& d = p->tasks[u];
-      for (int i = 0; i < phase_items(d.kind, R, 0); ++i)
+      for (int i = 0; i < group_items(d.kind, R, 0); ++i)
         p->q_init[p->q_off[d.level] + p->tail0[d.level]++] = ((unsigned long long)(u + 1) << 32) | (unsigned)i;
     }
 

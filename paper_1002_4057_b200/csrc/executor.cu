@@ -142,10 +142,11 @@ __device__ __forceinline__ int rho(int x) { return (x >> 1) | ((x & 1) << 2); }
 // ---------------------------------------------------------------- jobs
 enum Variant : int8_t { V_NT = 0, V_NN = 1, V_TN = 2 };
 enum JobType : int8_t { J_GEMM = 0, J_SPECIAL = 1 };
-enum Special : int8_t { SP_BPOTRF = 0, SP_BTRTRI = 1, SP_COPY_ROWS = 2, SP_SEND = 3 };
+enum Special : int8_t { SP_BPOTRF = 0, SP_BTRTRI = 1, SP_COPY_ROWS = 2, SP_SEND = 3, SP_BCOPYINV = 4 };
 
 struct ItemInfo {
-  int32_t task, item, phase, kind, step;
+  int32_t task, item, phase, kind, step;  // phase: phase group index (queue entry)
+  int32_t ph0, nph, grp;                  // first phase, fused single-item phases, phase group
   int32_t out_s, alt_s, in0_s, in1_s, scr_s;
   int32_t ref_id, nitems, njobs, flags;
   int32_t aux0, aux1;
@@ -166,10 +167,15 @@ __device__ __forceinline__ void lower_pair(int i, int& r, int& c) {
   c = i - r * (r + 1) / 2;
 }
 
-// jobs of one work item: two for the off-diagonal items of TRTRI / INV
+// jobs of one item of phase p: two for the off-diagonal items of TRTRI / INV
 // phases >= 1, one otherwise
+__device__ __forceinline__ int phase_jobs(int kind, int p) {
+  return ((kind == TINV_TRTRI || kind == KIND_INV) && p > 0) ? 2 : 1;
+}
 __device__ __forceinline__ int job_count(const ItemInfo& it) {
-  return ((it.kind == TINV_TRTRI || it.kind == KIND_INV) && it.phase > 0) ? 2 : 1;
+  int n = 0;
+  for (int p = it.ph0; p < it.ph0 + it.nph; ++p) n += phase_jobs(it.kind, p);
+  return n;
 }
 
 __device__ __forceinline__ void gemm_job(Job& j, int8_t v, int a_s, int a_fix, int a_k0, int b_s, int b_fix,
@@ -208,7 +214,30 @@ __device__ __forceinline__ void special_job(Job& j, int8_t sp, int d, int src, i
   j.o_s = dst;
 }
 
+__device__ void get_job_phase(const ItemInfo& it, int n, int R, Job& j);
+
+// job n of an item: walk the fused phases of its group; the first job of a
+// fused phase after the first depends on everything before it
 __device__ void get_job(const ItemInfo& it, int n, int R, Job& j) {
+  if (it.nph == 1) {
+    get_job_phase(it, n, R, j);
+    return;
+  }
+  ItemInfo sub = it;
+  for (int p = it.ph0; p < it.ph0 + it.nph; ++p) {
+    const int nj = phase_jobs(it.kind, p);
+    if (n < nj) {
+      sub.phase = p;
+      sub.item = 0;
+      get_job_phase(sub, n, R, j);
+      if (n == 0 && p > it.ph0) j.dep = 1;
+      return;
+    }
+    n -= nj;
+  }
+}
+
+__device__ void get_job_phase(const ItemInfo& it, int n, int R, Job& j) {
   const int o = it.out_s, a = it.alt_s, x = it.in0_s, y = it.in1_s;
   const int kind = it.kind;
   if (kind == TINV_POTRF) {  // in place on o; inverses of the diagonal blocks kept in aux tile x
@@ -237,7 +266,10 @@ __device__ void get_job(const ItemInfo& it, int n, int R, Job& j) {
     const int src = kind == KIND_INV ? x : o;
     const int dst = kind == KIND_INV ? o : a;
     if (it.phase == 0) {
-      special_job(j, SP_BTRTRI, it.item, src, dst);
+      if (it.flags & TF_DIAG_FROM_AUX)  // inverse diagonal blocks already computed by POTRF
+        special_job(j, SP_BCOPYINV, it.item, y, dst);
+      else
+        special_job(j, SP_BTRTRI, it.item, src, dst);
       return;
     }
     const int r = it.phase + it.item, d = r - it.phase;
@@ -597,10 +629,42 @@ __device__ __forceinline__ void run_gemm(const Job& jb, const ExecParams& P, Sme
 // A 128x128 diagonal block in shared memory uses row stride 129 doubles.
 constexpr int SLD = BLK + 1;
 
+// global -> global copy of n2 double2 by the 256 consumer threads, 8 loads in
+// flight per thread (a dependent load->store loop is latency-bound)
+__device__ __forceinline__ void copy_d2(double2* __restrict__ out, const double2* __restrict__ src, int64_t n2) {
+  int64_t e = threadIdx.x;
+  for (; e + 7 * 256 < n2; e += 8 * 256) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + e + u * 256);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) out[e + u * 256] = v[u];
+  }
+  for (; e < n2; e += 256) out[e] = __ldcg(src + e);
+}
+// 128x128 block (row stride bp) -> S, lower part only, 8 row-pairs in flight per thread
+__device__ __forceinline__ void load_block_lower(double* S, const double* blk, int64_t bp) {
+  const int c2 = threadIdx.x & 63, r0 = threadIdx.x >> 6;  // each thread: columns 2*c2, 2*c2+1 of 32 rows
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcg(reinterpret_cast<const double2*>(blk + (r0 + 4 * (8 * g + u)) * bp) + c2);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = r0 + 4 * (8 * g + u), j = 2 * c2;
+      S[i * SLD + j] = j <= i ? v[u].x : 0.0;
+      S[i * SLD + j + 1] = j + 1 <= i ? v[u].y : 0.0;
+    }
+  }
+}
+
 __device__ void store_block_lower(const double* S, double* dst, int64_t bp) {
-  for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
-    const int i = e >> 7, j = e & 127;
-    dst[i * bp + j] = (j <= i) ? S[i * SLD + j] : 0.0;
+  const int c2 = threadIdx.x & 63;
+  for (int i = threadIdx.x >> 6; i < BLK; i += 4) {
+    const int j = 2 * c2;
+    reinterpret_cast<double2*>(dst + i * bp)[c2] =
+        make_double2(j <= i ? S[i * SLD + j] : 0.0, j + 1 <= i ? S[i * SLD + j + 1] : 0.0);
   }
 }
 // zero the blocks (d, c > d) of a tile (upper part of block row d)
@@ -842,10 +906,7 @@ __device__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams&
     case SP_BPOTRF: {  // factor block (d,d) of dst in place; inverse -> aux block (d,d)
       long long t0 = clock64();
       double* blk = dst + (int64_t)d * BLK * bp + d * BLK;
-      for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
-        const int i = e >> 7, j = e & 127;
-        S[i * SLD + j] = (j <= i) ? __ldcg(blk + i * bp + j) : 0.0;
-      }
+      load_block_lower(S, blk, bp);
       cons_bar();
       long long t1 = clock64();
       const int f = block_potrf(S, ctl);
@@ -881,10 +942,7 @@ __device__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams&
     case SP_BTRTRI: {  // dst block (d,d) <- inv(tril(src block (d,d))); zero dst blocks (d, c>d)
       const double* sb = P.pool + (int64_t)jb.src_s * P.slot_elems + (int64_t)d * BLK * bp + d * BLK;
       if (threadIdx.x == 0) ctl.scan_min = 1 << 30;
-      for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
-        const int i = e >> 7, j = e & 127;
-        S[i * SLD + j] = (j <= i) ? __ldcg(sb + i * bp + j) : 0.0;
-      }
+      load_block_lower(S, sb, bp);
       cons_bar();
       if (threadIdx.x < BLK && d * BLK + threadIdx.x < b && S[threadIdx.x * SLD + threadIdx.x] == 0.0)
         atomicMin(&ctl.scan_min, threadIdx.x);  // kernels.py:125-127: zero diagonal
@@ -912,18 +970,25 @@ __device__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams&
     case SP_SEND: {  // tile version -> receiver's pool (peer memory), then its inbox flag
       const double2* src = reinterpret_cast<const double2*>(P.pool + (int64_t)jb.src_s * P.slot_elems);
       double2* out = reinterpret_cast<double2*>(P.peer_pool[it.aux0] + (int64_t)(P.recv_base + it.aux1) * P.slot_elems);
-      for (int64_t e = threadIdx.x; e < P.slot_elems / 2; e += 256) out[e] = __ldcg(src + e);
+      copy_d2(out, src, P.slot_elems / 2);
       __threadfence_system();
       cons_bar();
       if (threadIdx.x == 0) st_release_sys_s32(P.peer_inbox[it.aux0] + it.aux1, 1);
       break;
     }
+    case SP_BCOPYINV: {  // dst block (d,d) <- aux block (d,d) (lower, zero upper); zero dst blocks (d, c>d)
+      const double* sb = P.pool + (int64_t)jb.src_s * P.slot_elems + (int64_t)d * BLK * bp + d * BLK;
+      double* db = dst + (int64_t)d * BLK * bp + d * BLK;
+      for (int i = threadIdx.x >> 6; i < BLK; i += 4)
+        reinterpret_cast<double2*>(db + i * bp)[threadIdx.x & 63] =
+            __ldcg(reinterpret_cast<const double2*>(sb + i * bp) + (threadIdx.x & 63));
+      zero_upper_row(dst, d, R, bp);
+      break;
+    }
     case SP_COPY_ROWS: {
       const double* src = P.pool + (int64_t)jb.src_s * P.slot_elems + (int64_t)d * BLK * bp;
       double* out = dst + (int64_t)d * BLK * bp;
-      const int64_t n2 = (int64_t)BLK * bp / 2;
-      for (int64_t e = threadIdx.x; e < n2; e += 256)
-        reinterpret_cast<double2*>(out)[e] = __ldcg(reinterpret_cast<const double2*>(src) + e);
+      copy_d2(reinterpret_cast<double2*>(out), reinterpret_cast<const double2*>(src), (int64_t)BLK * bp / 2);
       break;
     }
     default:
@@ -936,7 +1001,7 @@ __device__ __forceinline__ void push_task(const ExecParams& P, int s, int phase)
   const TaskDev& t = P.tasks[s];
   if (t.flags & TF_EXTERNAL) return;  // RECV: completed by the inbox poller
   const int lev = t.level;
-  const int n = phase_items(t.kind, P.R, phase);
+  const int n = group_items(t.kind, P.R, phase);
   const int pos = atomicAdd(&P.q_tail[lev], n);
   unsigned long long* q = P.queue + P.q_off[lev] + pos;
   for (int i = 0; i < n; ++i)
@@ -945,41 +1010,64 @@ __device__ __forceinline__ void push_task(const ExecParams& P, int s, int phase)
 
 constexpr unsigned long long POP_EXIT = ~0ull;
 
+// Warp-cooperative pop (all 32 lanes of the producer warp): lane l inspects
+// priority level l, the lowest non-empty level is claimed with a CAS on its head.
 __device__ unsigned long long pop_item(const ExecParams& P) {
+  static_assert(NLEV <= 32, "one lane per priority level");
+  const int lane = threadIdx.x & 31;
   unsigned last_prog = ld_relaxed_u32(P.progress);
   unsigned long long t_last = globaltimer();
   unsigned spin = 0;
   while (true) {
-    if (ld_relaxed_s32(P.abort_flag)) return POP_EXIT;
-    if (ld_relaxed_s32(P.remaining) <= 0) return POP_EXIT;
-    for (int lev = 0; lev < NLEV; ++lev) {
-      int h = ld_relaxed_s32(P.q_head + lev);
-      const int t = ld_relaxed_s32(P.q_tail + lev);
-      while (h < t) {
+    int stop = 0;
+    if (lane == 0) stop = ld_relaxed_s32(P.abort_flag) || ld_relaxed_s32(P.remaining) <= 0;
+    if (__shfl_sync(0xffffffffu, stop, 0)) return POP_EXIT;
+    int h = 0, t = 0;
+    if (lane < NLEV) {
+      h = ld_relaxed_s32(P.q_head + lane);
+      t = ld_relaxed_s32(P.q_tail + lane);
+    }
+    unsigned m = __ballot_sync(0xffffffffu, h < t);
+    while (m) {
+      const int lev = __ffs(m) - 1;
+      unsigned long long v = 0;
+      int got = 0;
+      if (lane == lev) {
         const int prev = atomicCAS(P.q_head + lev, h, h + 1);
         if (prev == h) {
           const unsigned long long* slot = P.queue + P.q_off[lev] + h;
-          unsigned long long v;
           while ((v = ld_acquire_u64(slot)) == 0ull) {
           }
-          return v;
+          got = 1;
+        } else {
+          h = prev;  // lost the race: retry this level if still non-empty
         }
-        h = prev;
       }
+      const unsigned won = __ballot_sync(0xffffffffu, got);
+      if (won) {
+        const int src = __ffs(won) - 1;
+        return __shfl_sync(0xffffffffu, v, src);
+      }
+      if (lane == lev && h >= t) m &= ~(1u << lev);
+      m = __shfl_sync(0xffffffffu, m, lev);
     }
     __nanosleep(spin < 64 ? 32 : 256);
     ++spin;
     if ((spin & 255) == 0) {  // watchdog: no item completed anywhere for 30 s
-      const unsigned pr = ld_relaxed_u32(P.progress);
-      const unsigned long long now = globaltimer();
-      if (pr != last_prog) {
-        last_prog = pr;
-        t_last = now;
-      } else if (now - t_last > 30ull * 1000000000ull) {
-        atomicMin(P.err, ((unsigned long long)0x7fffffffu << 32) | ((unsigned long long)TINV_ERR_INTERNAL << 24));
-        atomicExch(P.abort_flag, 1);
-        return POP_EXIT;
+      int quit = 0;
+      if (lane == 0) {
+        const unsigned pr = ld_relaxed_u32(P.progress);
+        const unsigned long long now = globaltimer();
+        if (pr != last_prog) {
+          last_prog = pr;
+          t_last = now;
+        } else if (now - t_last > 30ull * 1000000000ull) {
+          atomicMin(P.err, ((unsigned long long)0x7fffffffu << 32) | ((unsigned long long)TINV_ERR_INTERNAL << 24));
+          atomicExch(P.abort_flag, 1);
+          quit = 1;
+        }
       }
+      if (__shfl_sync(0xffffffffu, quit, 0)) return POP_EXIT;
     }
   }
 }
@@ -1000,7 +1088,7 @@ __device__ void complete_item(const ExecParams& P, const Rec& r) {
     } else {
       const TaskDev& t = P.tasks[task];
       const int old = atomicAdd(P.done + task, 1);
-      if (old == phase_items(t.kind, P.R, phase) - 1) {  // phase complete
+      if (old == group_items(t.kind, P.R, phase) - 1) {  // phase group complete
         if (phase + 1 < t.nphases) {
           P.done[task] = 0;  // every item of this phase has finished: no concurrent update
           __threadfence();
@@ -1036,6 +1124,84 @@ __device__ void complete_item(const ExecParams& P, const Rec& r) {
     }
   }
   if (lane == 0) atomicAdd(P.progress, 1u);
+}
+
+// Producer lane 0: publish one popped work item to the consumers and stream
+// the operand chunks of its GEMM jobs through the TMA ring.
+__device__ __forceinline__ void produce_item(unsigned long long e, int slot, const ExecParams& P, SmemCtl& ctl,
+                                             char* ring, const CUtensorMap& tmK, const CUtensorMap& tmM, int R,
+                                             unsigned& ks, unsigned& issued) {
+      ItemInfo it;
+      if (e == POP_EXIT) {
+        it.task = -1;
+        ctl.items[slot] = it;
+        mbar_arrive(&ctl.item_full[slot]);
+        return;
+      }
+      it.task = (int)(e >> 32) - 1;
+      const int grp = (int)((e >> 16) & 0xffffu);
+      it.item = (int)(e & 0xffffu);
+      const TaskDev t = P.tasks[it.task];
+      it.kind = t.kind;
+      it.ph0 = group_first(t.kind, R, grp);
+      it.nph = group_phases(t.kind, R, it.ph0);
+      it.phase = it.ph0;  // phase of the first job; the group index travels in `grp`
+      it.grp = grp;
+      it.step = t.step;
+      it.ref_id = t.ref_id;
+      it.nitems = t.nitems;
+      it.flags = t.flags;
+      it.out_s = t.out >= 0 ? __ldcg(P.cur_slot + t.out) : -1;
+      it.alt_s = (t.flags & TF_RENAMED) ? __ldcg(P.alt_slot + t.out) : -1;
+      it.in0_s = t.in0 >= 0 ? __ldcg(P.cur_slot + t.in0) : -1;
+      it.in1_s = t.in1 >= 0 ? __ldcg(P.cur_slot + t.in1) : -1;
+      it.scr_s = P.scratch_base + blockIdx.x;
+      it.aux0 = t.aux0;
+      it.aux1 = t.aux1;
+      it.njobs = job_count(it);
+      fence_proxy_async();  // tiles written by other SMs (generic proxy) -> TMA reads
+      ctl.items[slot] = it;
+      mbar_arrive(&ctl.item_full[slot]);
+      for (int jn = 0; jn < it.njobs; ++jn, ++issued) {
+        Job jb;
+        get_job(it, jn, R, jb);
+        if (jb.type == J_SPECIAL) {
+          while (ld_acquire_cta_u32(&ctl.jobs_done) < issued + 1) {
+          }
+          fence_proxy_async();
+          continue;
+        }
+        if (jb.dep) {
+          while (ld_acquire_cta_u32(&ctl.jobs_done) < issued) {
+          }
+          fence_proxy_async();
+        }
+        if (jb.c_s >= 0)  // warm L2 with the C block for the epilogue
+          for (int x = 0; x < BLK; x += 16) tma_prefetch3(&tmK, jb.o_c * BLK + x, jb.o_r * BLK, jb.c_s);
+        const bool aK = (jb.variant != V_TN), bK = (jb.variant == V_NT);
+        for (int kb = jb.k0; kb < jb.k1; ++kb) {
+          const int ka = jb.a_k0 + (kb - jb.k0), kbb = jb.b_k0 + (kb - jb.k0);
+          for (int ch = 0; ch < BLK / KCH; ++ch, ++ks) {
+            const int st = ks % NSTAGE;
+            mbar_wait(&ctl.empty[st], ((ks / NSTAGE) & 1) ^ 1);
+            char* sA = ring + st * STAGE_BYTES;
+            char* sB = sA + STAGE_BYTES / 2;
+            mbar_arrive_tx(&ctl.full[st], STAGE_BYTES);
+            if (aK) {
+              tma_load3(&tmK, sA, &ctl.full[st], ka * BLK + ch * KCH, jb.a_fix * BLK, jb.a_s);
+            } else {
+              for (int q = 0; q < 8; ++q)
+                tma_load3(&tmM, sA + q * 2048, &ctl.full[st], jb.a_fix * BLK + 16 * q, ka * BLK + ch * KCH, jb.a_s);
+            }
+            if (bK) {
+              tma_load3(&tmK, sB, &ctl.full[st], kbb * BLK + ch * KCH, jb.b_fix * BLK, jb.b_s);
+            } else {
+              for (int q = 0; q < 8; ++q)
+                tma_load3(&tmM, sB + q * 2048, &ctl.full[st], jb.b_fix * BLK + 16 * q, kbb * BLK + ch * KCH, jb.b_s);
+            }
+          }
+        }
+      }
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -1138,82 +1304,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       return;
     }
-    if (warp != NCONS_WARPS || lane != 0) return;
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
+    if (warp != NCONS_WARPS) return;
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmK)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmM)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmE)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmE)) : "memory");
+    }
     unsigned ks = 0, issued = 0;
     for (unsigned itn = 0;; ++itn) {
       const int slot = itn & 1;
       mbar_wait(&ctl.item_empty[slot], ((itn >> 1) & 1) ^ 1);
-      const unsigned long long e = pop_item(P);
-      ItemInfo it;
-      if (e == POP_EXIT) {
-        it.task = -1;
-        ctl.items[slot] = it;
-        mbar_arrive(&ctl.item_full[slot]);
-        break;
-      }
-      it.task = (int)(e >> 32) - 1;
-      it.phase = (int)((e >> 16) & 0xffffu);
-      it.item = (int)(e & 0xffffu);
-      const TaskDev t = P.tasks[it.task];
-      it.kind = t.kind;
-      it.step = t.step;
-      it.ref_id = t.ref_id;
-      it.nitems = t.nitems;
-      it.flags = t.flags;
-      it.out_s = t.out >= 0 ? __ldcg(P.cur_slot + t.out) : -1;
-      it.alt_s = (t.flags & TF_RENAMED) ? __ldcg(P.alt_slot + t.out) : -1;
-      it.in0_s = t.in0 >= 0 ? __ldcg(P.cur_slot + t.in0) : -1;
-      it.in1_s = t.in1 >= 0 ? __ldcg(P.cur_slot + t.in1) : -1;
-      it.scr_s = P.scratch_base + blockIdx.x;
-      it.aux0 = t.aux0;
-      it.aux1 = t.aux1;
-      it.njobs = job_count(it);
-      fence_proxy_async();  // tiles written by other SMs (generic proxy) -> TMA reads
-      ctl.items[slot] = it;
-      mbar_arrive(&ctl.item_full[slot]);
-      for (int jn = 0; jn < it.njobs; ++jn, ++issued) {
-        Job jb;
-        get_job(it, jn, R, jb);
-        if (jb.type == J_SPECIAL) {
-          while (ld_acquire_cta_u32(&ctl.jobs_done) < issued + 1) {
-          }
-          fence_proxy_async();
-          continue;
-        }
-        if (jb.dep) {
-          while (ld_acquire_cta_u32(&ctl.jobs_done) < issued) {
-          }
-          fence_proxy_async();
-        }
-        if (jb.c_s >= 0)  // warm L2 with the C block for the epilogue
-          for (int x = 0; x < BLK; x += 16) tma_prefetch3(&tmK, jb.o_c * BLK + x, jb.o_r * BLK, jb.c_s);
-        const bool aK = (jb.variant != V_TN), bK = (jb.variant == V_NT);
-        for (int kb = jb.k0; kb < jb.k1; ++kb) {
-          const int ka = jb.a_k0 + (kb - jb.k0), kbb = jb.b_k0 + (kb - jb.k0);
-          for (int ch = 0; ch < BLK / KCH; ++ch, ++ks) {
-            const int st = ks % NSTAGE;
-            mbar_wait(&ctl.empty[st], ((ks / NSTAGE) & 1) ^ 1);
-            char* sA = ring + st * STAGE_BYTES;
-            char* sB = sA + STAGE_BYTES / 2;
-            mbar_arrive_tx(&ctl.full[st], STAGE_BYTES);
-            if (aK) {
-              tma_load3(&tmK, sA, &ctl.full[st], ka * BLK + ch * KCH, jb.a_fix * BLK, jb.a_s);
-            } else {
-              for (int q = 0; q < 8; ++q)
-                tma_load3(&tmM, sA + q * 2048, &ctl.full[st], jb.a_fix * BLK + 16 * q, ka * BLK + ch * KCH, jb.a_s);
-            }
-            if (bK) {
-              tma_load3(&tmK, sB, &ctl.full[st], kbb * BLK + ch * KCH, jb.b_fix * BLK, jb.b_s);
-            } else {
-              for (int q = 0; q < 8; ++q)
-                tma_load3(&tmM, sB + q * 2048, &ctl.full[st], jb.b_fix * BLK + 16 * q, kbb * BLK + ch * KCH, jb.b_s);
-            }
-          }
-        }
-      }
+      const unsigned long long e = pop_item(P);  // all 32 lanes
+      if (lane == 0) produce_item(e, slot, P, ctl, ring, tmK, tmM, R, ks, issued);
+      __syncwarp();
+      if (e == POP_EXIT) break;
     }
     return;
   }
@@ -1274,7 +1378,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     tick(4);
     if (tid == 0) {
-      push_rec(ctl, es.rec, Rec{R_ITEM_END, it.task, it.nitems, it.ref_id, ctl.fail_code, ctl.fail_index, it.phase, 0});
+      push_rec(ctl, es.rec, Rec{R_ITEM_END, it.task, it.nitems, it.ref_id, ctl.fail_code, ctl.fail_index, it.grp, 0});
       ctl.fail_code = 0;
       ctl.fail_index = -1;
     }

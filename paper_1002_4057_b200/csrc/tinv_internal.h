@@ -10,7 +10,7 @@ namespace tinv {
 // The sub-tile ("block") every device job works on: 128 x 128 FP64.
 constexpr int BLK = 128;
 // Work-item queue priority levels (0 = most critical).
-constexpr int NLEV = 8;
+constexpr int NLEV = 32;
 // Executor CTA: two consumer warpgroups (8 DMMA warps) + one producer
 // warpgroup (warp 8 = scheduler + TMA issue); registers are rebalanced with
 // setmaxnreg (producer 56, consumers 224).
@@ -41,6 +41,7 @@ constexpr int MAX_RANKS = 8;
 enum TaskFlags : int32_t {
   TF_RENAMED = 1,   // output written to the alternate slot, slots swapped at completion
   TF_EXTERNAL = 2,  // never queued: completed by the inbox poller (RECV)
+  TF_DIAG_FROM_AUX = 4,  // TRTRI / INV: diagonal-block inverses copied from the POTRF aux tile (in1)
 };
 
 struct TaskDev {
@@ -48,7 +49,7 @@ struct TaskDev {
   int8_t step;
   int8_t flags;
   int8_t level;
-  int16_t nphases;  // diagonal tasks run as chains of parallel block phases
+  int16_t nphases;  // phase groups (queue round trips) of the task
   int16_t pad;
   int32_t nitems;   // items over all phases
   int32_t out;     // logical tile ids
@@ -141,9 +142,40 @@ TINV_HD int phase_items(int kind, int R, int p) {
       return R * R;
   }
 }
+// Phase groups: a run of consecutive single-item phases is fused into one
+// work item (its jobs run back to back on one CTA, no queue round trip); a
+// phase with several items is a group of its own.
+// group_first(kind, R, g) -> first phase of group g; -1 past the end.
+TINV_HD int group_first(int kind, int R, int g) {
+  const int np = phases_of(kind, R);
+  int p = 0;
+  for (int k = 0; k < g && p < np; ++k) {
+    if (phase_items(kind, R, p) > 1) {
+      ++p;
+    } else {
+      while (p < np && phase_items(kind, R, p) == 1) ++p;
+    }
+  }
+  return p < np ? p : -1;
+}
+TINV_HD int group_phases(int kind, int R, int first) {  // phases in the group starting at `first`
+  if (phase_items(kind, R, first) > 1) return 1;
+  int p = first;
+  while (p < phases_of(kind, R) && phase_items(kind, R, p) == 1) ++p;
+  return p - first;
+}
+TINV_HD int ngroups(int kind, int R) {
+  int g = 0;
+  while (group_first(kind, R, g) >= 0) ++g;
+  return g;
+}
+TINV_HD int group_items(int kind, int R, int g) {
+  const int f = group_first(kind, R, g);
+  return f < 0 ? 0 : phase_items(kind, R, f);
+}
 TINV_HD int total_items(int kind, int R) {
   int n = 0;
-  for (int p = 0; p < phases_of(kind, R); ++p) n += phase_items(kind, R, p);
+  for (int g = 0; g < ngroups(kind, R); ++g) n += group_items(kind, R, g);
   return n;
 }
 

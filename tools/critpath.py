@@ -1,0 +1,52 @@
+"""Trace-based critical path of one inversion: walk back from the last task
+through the predecessor that finished last; report time per kind and gaps."""
+import sys
+from collections import defaultdict
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+import paper_1002_4057_b200 as P
+from paper_1002_4057_b200 import _native
+
+n, b = int(sys.argv[1]), int(sys.argv[2])
+pl = sys.argv[3] if len(sys.argv) > 3 else "out"
+t = n // b
+g = torch.randn(n, n, dtype=torch.float64, device="cuda")
+a = g @ g.T / n
+a.diagonal().add_(1.0)
+ctx = _native.Context(n, b)
+s = P.gen_inversion(t, P.VariantConfig(P.Placement(pl)))
+table = s.table()
+plan = _native.Plan(ctx, table, t, np.zeros(0, np.int64), _native.TRACE)
+for _ in range(2):
+    ctx.put_dense_device(a.data_ptr(), n)
+    rc, err, ms = plan.run()
+st, en, sm = plan.trace()
+src, dst, kind = _native.dag_edges(table, np.zeros(0, np.int64))
+pred = defaultdict(list)
+for u, v in zip(src.tolist(), dst.tolist()):
+    pred[v].append(u)
+names = ["COPY", "POTRF", "TRSM", "SYRK_SUB", "SYRK_ADD_T", "GEMM", "TRTRI", "TRMM_L", "TRMM_RN", "TRMM_LT", "LAUUM"]
+v = int(np.argmax(en))
+path = []
+while True:
+    path.append(v)
+    ps = pred[v]
+    if not ps:
+        break
+    v = max(ps, key=lambda u: en[u])
+path.reverse()
+busy = defaultdict(float)
+cnt = defaultdict(int)
+gap = 0.0
+prev_end = 0
+for v in path:
+    k = names[table[v, 0]]
+    busy[k] += (en[v] - st[v]) / 1e3
+    cnt[k] += 1
+    gap += max(0, st[v] - prev_end) / 1e3
+    prev_end = en[v]
+print(f"n={n} b={b} {pl}: exec {ms:.2f} ms, critical path {len(path)} tasks, span {(en.max() - st.min()) / 1e6:.2f} ms")
+print(f"  gaps (ready->start, dispatch) {gap / 1e3:.2f} ms")
+for k in sorted(busy, key=lambda x: -busy[x]):
+    print(f"  {k:10s} n={cnt[k]:5d} busy {busy[k] / 1e3:8.2f} ms  mean {busy[k] / cnt[k]:8.1f} us")
