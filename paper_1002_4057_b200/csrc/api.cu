@@ -34,6 +34,9 @@ cudaError_t launch_copy_slots(double* pool, int64_t slot_elems, const int32_t* f
 using namespace tinv;
 
 static std::string g_err;
+// executor: next-item claim ahead of time only from levels with at least this
+// many ready items (TINV_PREFETCH_MIN overrides; 0 disables)
+static const int kPrefetchMin = 0;  // measured: hurts C2 (critical path), neutral on C3
 
 struct tinv_ctx {
   int64_t n = 0, b = 0, t = 0, bp = 0, R = 0, T = 0;
@@ -1257,6 +1260,10 @@ int tinv_plan_exec(tinv_plan* p, tinv_err* err, double* ms) {
     P.peer_pool[r] = c->peer_pool[r] ? c->peer_pool[r] : c->pool;
     P.peer_inbox[r] = c->peer_inbox[r] ? c->peer_inbox[r] : P.inbox;
   }
+  {
+    const char* pf = getenv("TINV_PREFETCH_MIN");
+    P.prefetch_min = pf ? atoi(pf) : kPrefetchMin;
+  }
   if (getenv("TINV_PHASE_PROFILE")) {
     if (!p->d_phase) CK(c, cudaMalloc(&p->d_phase, (size_t)c->nsm * NPHASE * 8));
     CK(c, cudaMemsetAsync(p->d_phase, 0, (size_t)c->nsm * NPHASE * 8, st));
@@ -1297,6 +1304,12 @@ int tinv_plan_exec(tinv_plan* p, tinv_err* err, double* ms) {
             tot[7], tot[8], tot[9], tot[10], tot[11]);
     fprintf(stderr, "[tinv phase] potrf factor %.0f subst %.0f trailing %.0f | trtri base %.0f l16 %.0f l32 %.0f l64 %.0f\n",
             tot[12], tot[13], tot[14], tot[15], tot[16], tot[17], tot[18]);
+    const double pops = tot[23] > 0 ? tot[23] : 1;
+    fprintf(stderr,
+            "[tinv phase] producer per pop: slot-wait %.0f pop %.0f produce %.0f (pops %.0f) | storer per item: "
+            "quarters %.0f job-end %.0f item-end %.0f idle %.0f\n",
+            tot[20] / pops, tot[21] / pops, tot[22] / pops, tot[23], tot[24] / items, tot[25] / items,
+            tot[26] / items, tot[27] / items);
   }
   if (ekey != ~0ull || ctr_out[0] != 0) {
     if (keep) {

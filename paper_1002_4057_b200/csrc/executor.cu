@@ -93,6 +93,12 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ int ld_relaxed_s32(const int32_t* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -214,30 +220,7 @@ __device__ __forceinline__ void special_job(Job& j, int8_t sp, int d, int src, i
   j.o_s = dst;
 }
 
-__device__ void get_job_phase(const ItemInfo& it, int n, int R, Job& j);
-
-// job n of an item: walk the fused phases of its group; the first job of a
-// fused phase after the first depends on everything before it
-__device__ void get_job(const ItemInfo& it, int n, int R, Job& j) {
-  if (it.nph == 1) {
-    get_job_phase(it, n, R, j);
-    return;
-  }
-  ItemInfo sub = it;
-  for (int p = it.ph0; p < it.ph0 + it.nph; ++p) {
-    const int nj = phase_jobs(it.kind, p);
-    if (n < nj) {
-      sub.phase = p;
-      sub.item = 0;
-      get_job_phase(sub, n, R, j);
-      if (n == 0 && p > it.ph0) j.dep = 1;
-      return;
-    }
-    n -= nj;
-  }
-}
-
-__device__ void get_job_phase(const ItemInfo& it, int n, int R, Job& j) {
+__device__ __forceinline__ void get_job_phase(const ItemInfo& it, int n, int R, Job& j) {
   const int o = it.out_s, a = it.alt_s, x = it.in0_s, y = it.in1_s;
   const int kind = it.kind;
   if (kind == TINV_POTRF) {  // in place on o; inverses of the diagonal blocks kept in aux tile x
@@ -347,6 +330,27 @@ __device__ void get_job_phase(const ItemInfo& it, int n, int R, Job& j) {
   }
 }
 
+// job n of an item: walk the fused phases of its group; the first job of a
+// fused phase after the first depends on everything before it
+__device__ __forceinline__ void get_job(const ItemInfo& it, int n, int R, Job& j) {
+  if (it.nph == 1) {
+    get_job_phase(it, n, R, j);
+    return;
+  }
+  ItemInfo sub = it;
+  for (int p = it.ph0; p < it.ph0 + it.nph; ++p) {
+    const int nj = phase_jobs(it.kind, p);
+    if (n < nj) {
+      sub.phase = p;
+      sub.item = 0;
+      get_job_phase(sub, n, R, j);
+      if (n == 0 && p > it.ph0) j.dep = 1;
+      return;
+    }
+    n -= nj;
+  }
+}
+
 // ---------------------------------------------------------------- smem
 // consumer -> storer hand-off records
 enum RecType : int32_t { R_QUARTER = 0, R_JOB_END = 1, R_ITEM_END = 2, R_EXIT = 3 };
@@ -354,6 +358,7 @@ struct Rec {
   int32_t type, a, b, c, d, e, f, g;
 };
 constexpr int NREC = 16;
+constexpr int MAXJ = 8;
 
 struct SmemCtl {
   uint64_t full[NSTAGE];
@@ -364,6 +369,8 @@ struct SmemCtl {
   uint64_t rec_empty[NREC];
   uint64_t stg_free[2];
   ItemInfo items[2];
+  Job jobs[2][MAXJ + 2];  // per item slot: its first MAXJ jobs (producer-built); [MAXJ] consumers' and
+                          // [MAXJ + 1] producer's scratch for later ones
   Rec recs[NREC];
   unsigned jobs_done;
   int fail_code;   // per item: 0 none
@@ -895,14 +902,15 @@ __device__ void block_trtri(double* S, unsigned long long* ctl_dbg) {
   }
 }
 
-__device__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams& P, SmemCtl& ctl, double* S,
-                            int b) {
+// jb / it live in shared memory (the item slot)
+__device__ __noinline__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams& P, SmemCtl& ctl,
+                                         double* S, int b) {
+  const int special = jb.special, d = jb.d, src_s = jb.src_s, o_s = jb.o_s, aux0 = it.aux0, aux1 = it.aux1;
   const int64_t bp = P.bp;
   const int R = P.R;
-  const int d = jb.d;
   if (ctl.fail_code) return;  // item already failed: keep the job protocol, skip work
-  double* dst = P.pool + (int64_t)jb.o_s * P.slot_elems;
-  switch (jb.special) {
+  double* dst = P.pool + (int64_t)o_s * P.slot_elems;
+  switch (special) {
     case SP_BPOTRF: {  // factor block (d,d) of dst in place; inverse -> aux block (d,d)
       long long t0 = clock64();
       double* blk = dst + (int64_t)d * BLK * bp + d * BLK;
@@ -930,7 +938,7 @@ __device__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams&
       t1 = clock64();
       block_trtri(S, ctl.dbg2);
       t2 = clock64();
-      double* aux = P.pool + (int64_t)jb.src_s * P.slot_elems;
+      double* aux = P.pool + (int64_t)src_s * P.slot_elems;
       store_block_lower(S, aux + (int64_t)d * BLK * bp + d * BLK, bp);
       cons_bar();
       if (threadIdx.x == 0) {
@@ -940,7 +948,7 @@ __device__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams&
       break;
     }
     case SP_BTRTRI: {  // dst block (d,d) <- inv(tril(src block (d,d))); zero dst blocks (d, c>d)
-      const double* sb = P.pool + (int64_t)jb.src_s * P.slot_elems + (int64_t)d * BLK * bp + d * BLK;
+      const double* sb = P.pool + (int64_t)src_s * P.slot_elems + (int64_t)d * BLK * bp + d * BLK;
       if (threadIdx.x == 0) ctl.scan_min = 1 << 30;
       load_block_lower(S, sb, bp);
       cons_bar();
@@ -968,16 +976,16 @@ __device__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams&
       break;
     }
     case SP_SEND: {  // tile version -> receiver's pool (peer memory), then its inbox flag
-      const double2* src = reinterpret_cast<const double2*>(P.pool + (int64_t)jb.src_s * P.slot_elems);
-      double2* out = reinterpret_cast<double2*>(P.peer_pool[it.aux0] + (int64_t)(P.recv_base + it.aux1) * P.slot_elems);
+      const double2* src = reinterpret_cast<const double2*>(P.pool + (int64_t)src_s * P.slot_elems);
+      double2* out = reinterpret_cast<double2*>(P.peer_pool[aux0] + (int64_t)(P.recv_base + aux1) * P.slot_elems);
       copy_d2(out, src, P.slot_elems / 2);
       __threadfence_system();
       cons_bar();
-      if (threadIdx.x == 0) st_release_sys_s32(P.peer_inbox[it.aux0] + it.aux1, 1);
+      if (threadIdx.x == 0) st_release_sys_s32(P.peer_inbox[aux0] + aux1, 1);
       break;
     }
     case SP_BCOPYINV: {  // dst block (d,d) <- aux block (d,d) (lower, zero upper); zero dst blocks (d, c>d)
-      const double* sb = P.pool + (int64_t)jb.src_s * P.slot_elems + (int64_t)d * BLK * bp + d * BLK;
+      const double* sb = P.pool + (int64_t)src_s * P.slot_elems + (int64_t)d * BLK * bp + d * BLK;
       double* db = dst + (int64_t)d * BLK * bp + d * BLK;
       for (int i = threadIdx.x >> 6; i < BLK; i += 4)
         reinterpret_cast<double2*>(db + i * bp)[threadIdx.x & 63] =
@@ -986,7 +994,7 @@ __device__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams&
       break;
     }
     case SP_COPY_ROWS: {
-      const double* src = P.pool + (int64_t)jb.src_s * P.slot_elems + (int64_t)d * BLK * bp;
+      const double* src = P.pool + (int64_t)src_s * P.slot_elems + (int64_t)d * BLK * bp;
       double* out = dst + (int64_t)d * BLK * bp;
       copy_d2(reinterpret_cast<double2*>(out), reinterpret_cast<const double2*>(src), (int64_t)BLK * bp / 2);
       break;
@@ -1010,47 +1018,73 @@ __device__ __forceinline__ void push_task(const ExecParams& P, int s, int phase)
 
 constexpr unsigned long long POP_EXIT = ~0ull;
 
-// Warp-cooperative pop (all 32 lanes of the producer warp): lane l inspects
-// priority level l, the lowest non-empty level is claimed with a CAS on its head.
-__device__ unsigned long long pop_item(const ExecParams& P) {
+// Claim attempt over the priority levels (all 32 lanes; lane l holds the
+// head / tail snapshot of level l): the lowest non-empty level is claimed with
+// a CAS on its head. The entry is read speculatively alongside the CAS (queue
+// entries are written once per run), then ordered with an acquire fence.
+// Returns 0 when every level is (or turned out) empty.
+__device__ __forceinline__ unsigned long long claim_item(const ExecParams& P, int h, int t, int minback = 1) {
+  const int lane = threadIdx.x & 31;
+  unsigned m = __ballot_sync(0xffffffffu, t - h >= minback);
+  while (m) {
+    const int lev = __ffs(m) - 1;
+    unsigned long long v = 0;
+    int got = 0;
+    if (lane == lev) {
+      const unsigned long long* slot = P.queue + P.q_off[lev] + h;
+      v = ld_relaxed_u64(slot);
+      const int prev = atomicCAS(P.q_head + lev, h, h + 1);
+      if (prev == h) {
+        while (v == 0ull) v = ld_relaxed_u64(slot);  // pusher reserved the slot, store in flight
+        fence_acq_rel_gpu();
+        got = 1;
+      } else {
+        h = prev;  // lost the race: retry this level if still non-empty
+      }
+    }
+    const unsigned won = __ballot_sync(0xffffffffu, got);
+    if (won) return __shfl_sync(0xffffffffu, v, __ffs(won) - 1);
+    if (lane == lev && t - h < minback) m &= ~(1u << lev);
+    m = __shfl_sync(0xffffffffu, m, lev);
+  }
+  return 0ull;
+}
+
+// Non-blocking pop (all 32 lanes): one snapshot of the levels, one claim pass
+// over the levels holding at least P.prefetch_min ready items (a lone ready
+// item is left to the CTAs that are idle right now).
+__device__ __forceinline__ unsigned long long try_pop(const ExecParams& P) {
   static_assert(NLEV <= 32, "one lane per priority level");
+  const int lane = threadIdx.x & 31;
+  int h = 0, t = 0;
+  if (lane < NLEV) {
+    h = ld_relaxed_s32(P.q_head + lane);
+    t = ld_relaxed_s32(P.q_tail + lane);
+  }
+  return claim_item(P, h, t, P.prefetch_min);
+}
+
+// Blocking pop (all 32 lanes): spins until an item is claimed, every task is
+// complete, the run aborted, or the watchdog fires.
+__device__ unsigned long long pop_item(const ExecParams& P) {
   const int lane = threadIdx.x & 31;
   unsigned last_prog = ld_relaxed_u32(P.progress);
   unsigned long long t_last = globaltimer();
   unsigned spin = 0;
   while (true) {
-    int stop = 0;
-    if (lane == 0) stop = ld_relaxed_s32(P.abort_flag) || ld_relaxed_s32(P.remaining) <= 0;
-    if (__shfl_sync(0xffffffffu, stop, 0)) return POP_EXIT;
-    int h = 0, t = 0;
+    // one round trip: queue bounds of every level and the stop flags together
+    int h = 0, t = 0, ab = 0, rem = 1;
     if (lane < NLEV) {
       h = ld_relaxed_s32(P.q_head + lane);
       t = ld_relaxed_s32(P.q_tail + lane);
     }
-    unsigned m = __ballot_sync(0xffffffffu, h < t);
-    while (m) {
-      const int lev = __ffs(m) - 1;
-      unsigned long long v = 0;
-      int got = 0;
-      if (lane == lev) {
-        const int prev = atomicCAS(P.q_head + lev, h, h + 1);
-        if (prev == h) {
-          const unsigned long long* slot = P.queue + P.q_off[lev] + h;
-          while ((v = ld_acquire_u64(slot)) == 0ull) {
-          }
-          got = 1;
-        } else {
-          h = prev;  // lost the race: retry this level if still non-empty
-        }
-      }
-      const unsigned won = __ballot_sync(0xffffffffu, got);
-      if (won) {
-        const int src = __ffs(won) - 1;
-        return __shfl_sync(0xffffffffu, v, src);
-      }
-      if (lane == lev && h >= t) m &= ~(1u << lev);
-      m = __shfl_sync(0xffffffffu, m, lev);
+    if (lane == 0) {
+      ab = ld_relaxed_s32(P.abort_flag);
+      rem = ld_relaxed_s32(P.remaining);
     }
+    if (__shfl_sync(0xffffffffu, ab || rem <= 0, 0)) return POP_EXIT;
+    const unsigned long long v = claim_item(P, h, t);
+    if (v) return v;
     __nanosleep(spin < 64 ? 32 : 256);
     ++spin;
     if ((spin & 255) == 0) {  // watchdog: no item completed anywhere for 30 s
@@ -1126,88 +1160,120 @@ __device__ void complete_item(const ExecParams& P, const Rec& r) {
   if (lane == 0) atomicAdd(P.progress, 1u);
 }
 
-// Producer lane 0: publish one popped work item to the consumers and stream
-// the operand chunks of its GEMM jobs through the TMA ring.
-__device__ __forceinline__ void produce_item(unsigned long long e, int slot, const ExecParams& P, SmemCtl& ctl,
-                                             char* ring, const CUtensorMap& tmK, const CUtensorMap& tmM, int R,
-                                             unsigned& ks, unsigned& issued) {
-      ItemInfo it;
-      if (e == POP_EXIT) {
-        it.task = -1;
-        ctl.items[slot] = it;
-        mbar_arrive(&ctl.item_full[slot]);
-        return;
-      }
-      it.task = (int)(e >> 32) - 1;
-      const int grp = (int)((e >> 16) & 0xffffu);
-      it.item = (int)(e & 0xffffu);
-      const TaskDev t = P.tasks[it.task];
-      it.kind = t.kind;
-      it.ph0 = group_first(t.kind, R, grp);
-      it.nph = group_phases(t.kind, R, it.ph0);
-      it.phase = it.ph0;  // phase of the first job; the group index travels in `grp`
-      it.grp = grp;
-      it.step = t.step;
-      it.ref_id = t.ref_id;
-      it.nitems = t.nitems;
-      it.flags = t.flags;
-      it.out_s = t.out >= 0 ? __ldcg(P.cur_slot + t.out) : -1;
-      it.alt_s = (t.flags & TF_RENAMED) ? __ldcg(P.alt_slot + t.out) : -1;
-      it.in0_s = t.in0 >= 0 ? __ldcg(P.cur_slot + t.in0) : -1;
-      it.in1_s = t.in1 >= 0 ? __ldcg(P.cur_slot + t.in1) : -1;
-      it.scr_s = P.scratch_base + blockIdx.x;
-      it.aux0 = t.aux0;
-      it.aux1 = t.aux1;
-      it.njobs = job_count(it);
-      fence_proxy_async();  // tiles written by other SMs (generic proxy) -> TMA reads
-      ctl.items[slot] = it;
+// Producer warp (all 32 lanes; lane 0 does the stores, arrivals and TMA
+// issues): publish one popped work item to the consumers and stream the
+// operand chunks of its GEMM jobs through the TMA ring. When PREFETCH_AT
+// chunks are left to issue (the ring is full, the consumers have about
+// NSTAGE + PREFETCH_AT chunks of work left), the next item is claimed without
+// blocking, hiding the queue round trips; returns it (0: none claimed).
+constexpr int PREFETCH_AT = 4;
+__device__ __forceinline__ unsigned long long produce_item(unsigned long long e, int slot, const ExecParams& P,
+                                                           SmemCtl& ctl, char* ring, const CUtensorMap& tmK,
+                                                           const CUtensorMap& tmM, int R, unsigned& ks,
+                                                           unsigned& issued) {
+  const int lane = threadIdx.x & 31;
+  ItemInfo& it = ctl.items[slot];  // built in place
+  if (e == POP_EXIT) {
+    if (lane == 0) {
+      it.task = -1;
       mbar_arrive(&ctl.item_full[slot]);
-      for (int jn = 0; jn < it.njobs; ++jn, ++issued) {
-        Job jb;
-        get_job(it, jn, R, jb);
-        if (jb.type == J_SPECIAL) {
-          while (ld_acquire_cta_u32(&ctl.jobs_done) < issued + 1) {
-          }
-          fence_proxy_async();
-          continue;
-        }
-        if (jb.dep) {
-          while (ld_acquire_cta_u32(&ctl.jobs_done) < issued) {
-          }
-          fence_proxy_async();
-        }
-        if (jb.c_s >= 0)  // warm L2 with the C block for the epilogue
-          for (int x = 0; x < BLK; x += 16) tma_prefetch3(&tmK, jb.o_c * BLK + x, jb.o_r * BLK, jb.c_s);
-        const bool aK = (jb.variant != V_TN), bK = (jb.variant == V_NT);
-        for (int kb = jb.k0; kb < jb.k1; ++kb) {
-          const int ka = jb.a_k0 + (kb - jb.k0), kbb = jb.b_k0 + (kb - jb.k0);
-          for (int ch = 0; ch < BLK / KCH; ++ch, ++ks) {
-            const int st = ks % NSTAGE;
-            mbar_wait(&ctl.empty[st], ((ks / NSTAGE) & 1) ^ 1);
-            char* sA = ring + st * STAGE_BYTES;
-            char* sB = sA + STAGE_BYTES / 2;
-            mbar_arrive_tx(&ctl.full[st], STAGE_BYTES);
-            if (aK) {
-              tma_load3(&tmK, sA, &ctl.full[st], ka * BLK + ch * KCH, jb.a_fix * BLK, jb.a_s);
-            } else {
-              for (int q = 0; q < 8; ++q)
-                tma_load3(&tmM, sA + q * 2048, &ctl.full[st], jb.a_fix * BLK + 16 * q, ka * BLK + ch * KCH, jb.a_s);
-            }
-            if (bK) {
-              tma_load3(&tmK, sB, &ctl.full[st], kbb * BLK + ch * KCH, jb.b_fix * BLK, jb.b_s);
-            } else {
-              for (int q = 0; q < 8; ++q)
-                tma_load3(&tmM, sB + q * 2048, &ctl.full[st], jb.b_fix * BLK + 16 * q, kbb * BLK + ch * KCH, jb.b_s);
-            }
-          }
-        }
+    }
+    return 0ull;
+  }
+  if (lane == 0) {
+    it.task = (int)(e >> 32) - 1;
+    const int grp = (int)((e >> 16) & 0xffffu);
+    it.item = (int)(e & 0xffffu);
+    const TaskDev t = P.tasks[it.task];
+    it.kind = t.kind;
+    it.ph0 = group_first(t.kind, R, grp);
+    it.nph = group_phases(t.kind, R, it.ph0);
+    it.phase = it.ph0;  // phase of the first job; the group index travels in `grp`
+    it.grp = grp;
+    it.step = t.step;
+    it.ref_id = t.ref_id;
+    it.nitems = t.nitems;
+    it.flags = t.flags;
+    it.out_s = t.out >= 0 ? __ldcg(P.cur_slot + t.out) : -1;
+    it.alt_s = (t.flags & TF_RENAMED) ? __ldcg(P.alt_slot + t.out) : -1;
+    it.in0_s = t.in0 >= 0 ? __ldcg(P.cur_slot + t.in0) : -1;
+    it.in1_s = t.in1 >= 0 ? __ldcg(P.cur_slot + t.in1) : -1;
+    it.scr_s = P.scratch_base + blockIdx.x;
+    it.aux0 = t.aux0;
+    it.aux1 = t.aux1;
+    it.njobs = job_count(it);
+    for (int jn = 0; jn < it.njobs && jn < MAXJ; ++jn) get_job(it, jn, R, ctl.jobs[slot][jn]);
+    fence_proxy_async();  // tiles written by other SMs (generic proxy) -> TMA reads
+    mbar_arrive(&ctl.item_full[slot]);
+  }
+  __syncwarp();
+  const int njobs = it.njobs;
+  int left = 0;  // chunks left to issue (jobs past MAXJ are not counted: prefetch may come early)
+  for (int jn = 0; jn < njobs && jn < MAXJ; ++jn) {
+    const Job& j = ctl.jobs[slot][jn];
+    if (j.type == J_GEMM) left += (j.k1 - j.k0) * (BLK / KCH);
+  }
+  unsigned long long next = 0ull;
+  bool tried = false;
+  for (int jn = 0; jn < njobs; ++jn, ++issued) {
+    if (jn >= MAXJ) {
+      if (lane == 0) get_job(it, jn, R, ctl.jobs[slot][MAXJ + 1]);
+      __syncwarp();
+    }
+    const Job& jb = ctl.jobs[slot][jn < MAXJ ? jn : MAXJ + 1];
+    if (jb.type == J_SPECIAL) {
+      while (ld_acquire_cta_u32(&ctl.jobs_done) < issued + 1) {
       }
+      fence_proxy_async();
+      continue;
+    }
+    if (jb.dep) {
+      while (ld_acquire_cta_u32(&ctl.jobs_done) < issued) {
+      }
+      fence_proxy_async();
+    }
+    if (lane == 0 && jb.c_s >= 0)  // warm L2 with the C block for the epilogue
+      for (int x = 0; x < BLK; x += 16) tma_prefetch3(&tmK, jb.o_c * BLK + x, jb.o_r * BLK, jb.c_s);
+    // job fields are re-read from smem (LDS) rather than held across the loop:
+    // the producer runs on 56 registers
+    for (int kb = jb.k0; kb < jb.k1; ++kb) {
+      for (int ch = 0; ch < BLK / KCH; ++ch, ++ks, --left) {
+        if (!tried && left <= PREFETCH_AT) {
+          tried = true;
+          if (P.prefetch_min > 0) next = try_pop(P);
+        }
+        const int st = ks % NSTAGE;
+        mbar_wait(&ctl.empty[st], ((ks / NSTAGE) & 1) ^ 1);
+        if (lane == 0) {
+          const int ka = jb.a_k0 + (kb - jb.k0), kbb = jb.b_k0 + (kb - jb.k0);
+          char* sA = ring + st * STAGE_BYTES;
+          char* sB = sA + STAGE_BYTES / 2;
+          mbar_arrive_tx(&ctl.full[st], STAGE_BYTES);
+          if (jb.variant != V_TN) {  // A K-major
+            tma_load3(&tmK, sA, &ctl.full[st], ka * BLK + ch * KCH, jb.a_fix * BLK, jb.a_s);
+          } else {
+            for (int q = 0; q < 8; ++q)
+              tma_load3(&tmM, sA + q * 2048, &ctl.full[st], jb.a_fix * BLK + 16 * q, ka * BLK + ch * KCH, jb.a_s);
+          }
+          if (jb.variant == V_NT) {  // B K-major
+            tma_load3(&tmK, sB, &ctl.full[st], kbb * BLK + ch * KCH, jb.b_fix * BLK, jb.b_s);
+          } else {
+            for (int q = 0; q < 8; ++q)
+              tma_load3(&tmM, sB + q * 2048, &ctl.full[st], jb.b_fix * BLK + 16 * q, kbb * BLK + ch * KCH, jb.b_s);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+  return next;
 }
 
 // ---------------------------------------------------------------- the kernel
+template <bool PROF>
 __global__ void __launch_bounds__(NTHREADS, 1)
     exec_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmM,
-                const __grid_constant__ CUtensorMap tmE, ExecParams P, int b) {
+                const __grid_constant__ CUtensorMap tmE, const __grid_constant__ ExecParams P, int b) {
   extern __shared__ __align__(1024) char dsmem[];
   __shared__ SmemCtl ctl;
   // keep the pointer derived from the __shared__ array (arithmetic through an
@@ -1246,9 +1312,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PROD_REGS));
     if (warp == NCONS_WARPS + 1) {
       // ============================ storer warp: epilogue TMA + completion
+      unsigned long long sph[4] = {0, 0, 0, 0};  // PROF: quarter, job-end, item-end, idle cycles
+      long long stc = clock64();
       for (unsigned idx = 0;; ++idx) {
         const int s = idx % NREC;
         mbar_wait(&ctl.rec_full[s], (idx / NREC) & 1);
+        if constexpr (PROF) {
+          const long long now = clock64();
+          sph[3] += now - stc;
+          stc = now;
+        }
         const Rec r = ctl.recs[s];
         __syncwarp();
         if (r.type == R_EXIT) break;
@@ -1278,6 +1351,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&ctl.rec_empty[s]);
+        if constexpr (PROF) {
+          const long long now = clock64();
+          sph[r.type == R_QUARTER ? 0 : (r.type == R_JOB_END ? 1 : 2)] += now - stc;
+          stc = now;
+        }
+      }
+      if constexpr (PROF) {
+        if (lane == 0 && P.phase)
+          for (int k = 0; k < 4; ++k) P.phase[blockIdx.x * NPHASE + 24 + k] = sph[k];
       }
       return;
     }
@@ -1311,13 +1393,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmE)) : "memory");
     }
     unsigned ks = 0, issued = 0;
+    unsigned long long pph[4] = {0, 0, 0, 0};  // PROF: slot wait, pop, produce cycles, pops
+    long long ptc = clock64();
+    auto ptick = [&](int k) {
+      if constexpr (PROF) {
+        const long long now = clock64();
+        pph[k] += now - ptc;
+        ptc = now;
+      }
+    };
+    unsigned long long next = 0ull;  // item claimed ahead while streaming the previous one
     for (unsigned itn = 0;; ++itn) {
       const int slot = itn & 1;
       mbar_wait(&ctl.item_empty[slot], ((itn >> 1) & 1) ^ 1);
-      const unsigned long long e = pop_item(P);  // all 32 lanes
-      if (lane == 0) produce_item(e, slot, P, ctl, ring, tmK, tmM, R, ks, issued);
-      __syncwarp();
+      ptick(0);
+      const unsigned long long e = next ? next : pop_item(P);  // all 32 lanes
+      ptick(1);
+      next = produce_item(e, slot, P, ctl, ring, tmK, tmM, R, ks, issued);
+      ptick(2);
+      if constexpr (PROF) pph[3] += 1;
       if (e == POP_EXIT) break;
+    }
+    if constexpr (PROF) {
+      if (lane == 0 && P.phase)
+        for (int k = 0; k < 4; ++k) P.phase[blockIdx.x * NPHASE + 20 + k] = pph[k];
     }
     return;
   }
@@ -1329,17 +1428,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   unsigned long long ph[NPHASE] = {};
   long long tc = clock64();
   auto tick = [&](int k) {
-    const long long now = clock64();
-    ph[k] += (unsigned long long)(now - tc);
-    tc = now;
+    if constexpr (PROF) {
+      const long long now = clock64();
+      ph[k] += (unsigned long long)(now - tc);
+      tc = now;
+    }
   };
   for (unsigned itn = 0;; ++itn) {
     const int slot = itn & 1;
     mbar_wait(&ctl.item_full[slot], (itn >> 1) & 1);
     tick(0);
-    const ItemInfo it = ctl.items[slot];
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&ctl.item_empty[slot]);
+    const ItemInfo& it = ctl.items[slot];  // stays in smem: the slot is released at item end
     if (it.task < 0) {
       if (tid == 0) push_rec(ctl, es.rec, Rec{R_EXIT, 0, 0, 0, 0, 0, 0, 0});
       break;
@@ -1347,8 +1446,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (tid == 0 && P.trace_start) atomicMin(P.trace_start + it.task, globaltimer() - P.t0);
     int item_generic = 0;
     for (int jn = 0; jn < it.njobs; ++jn) {
-      Job jb;
-      get_job(it, jn, R, jb);
+      if (jn >= MAXJ) {  // rare: long fused phase groups; build the job in the scratch entry
+        cons_bar();
+        if (tid == 0) get_job(it, jn, R, ctl.jobs[slot][MAXJ]);
+        cons_bar();
+      }
+      const Job& jb = ctl.jobs[slot][jn < MAXJ ? jn : MAXJ];
       es.generic = 0;
       if (jb.type == J_SPECIAL) {
         drain_jobs(ctl, es);
@@ -1382,17 +1485,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       ctl.fail_code = 0;
       ctl.fail_index = -1;
     }
+    if constexpr (PROF) {
+      ph[6] += 1;
+      ph[7] += it.njobs;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ctl.item_empty[slot]);
     es.rec += 1;
     tick(5);
-    ph[6] += 1;
-    ph[7] += it.njobs;
   }
-  if (tid == 0) {
-    for (int k = 0; k < 4; ++k) ph[8 + k] = ctl.dbg[k];
-    for (int k = 0; k < 8; ++k) ph[12 + k] = ctl.dbg2[k];
+  if constexpr (PROF) {
+    if (tid == 0) {
+      for (int k = 0; k < 4; ++k) ph[8 + k] = ctl.dbg[k];
+      for (int k = 0; k < 8; ++k) ph[12 + k] = ctl.dbg2[k];
+      if (P.phase)
+        for (int k = 0; k < 20; ++k) P.phase[blockIdx.x * NPHASE + k] = ph[k];
+    }
   }
-  if (P.phase && tid == 0)
-    for (int k = 0; k < NPHASE; ++k) P.phase[blockIdx.x * NPHASE + k] = ph[k];
 }
 
 // ---------------------------------------------------------------- host launch
@@ -1400,9 +1509,10 @@ int exec_smem_bytes() { return SMEM_BYTES; }
 
 cudaError_t launch_exec(const CUtensorMap& tmK, const CUtensorMap& tmM, const CUtensorMap& tmE, const ExecParams& P,
                         int b, int grid, cudaStream_t stream) {
-  cudaError_t e = cudaFuncSetAttribute(exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  auto kern = P.phase ? exec_kernel<true> : exec_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  exec_kernel<<<grid, NTHREADS, SMEM_BYTES, stream>>>(tmK, tmM, tmE, P, b);
+  kern<<<grid, NTHREADS, SMEM_BYTES, stream>>>(tmK, tmM, tmE, P, b);
   return cudaGetLastError();
 }
 

@@ -88,6 +88,7 @@ struct ExecParams {
   int32_t* trace_sm;
   unsigned long long t0;           // globaltimer at launch (trace base)
   unsigned long long* phase;       // optional per-CTA phase cycle counters (NPHASE each)
+  int prefetch_min;                // claim the next item ahead only from levels with this backlog (0: never)
   // multi-GPU transfers
   double* peer_pool[MAX_RANKS];    // pools of the ranks (peer-mapped; the local pool for self)
   int32_t* peer_inbox[MAX_RANKS];  // inbox flag arrays of the ranks
@@ -96,8 +97,9 @@ struct ExecParams {
   int32_t nrecv;                   // inbox length
   int32_t recv_base;               // slot of receive sequence number 0 (same on every rank)
 };
-constexpr int NPHASE = 20;  // item-wait, mainloop, epilogue, job-end, item-end, completion, items, jobs,
-                            // special: load, factor, inverse, store
+constexpr int NPHASE = 28;  // item-wait, mainloop, epilogue, job-end, item-end, completion, items, jobs,
+                            // special: load, factor, inverse, store; potrf/trtri sub-steps;
+                            // producer: slot-wait, pop, produce, pops; storer: quarters, job-end, item-end, idle
 
 inline int64_t tri_index(int64_t i, int64_t j) { return i * (i + 1) / 2 + j; }
 
