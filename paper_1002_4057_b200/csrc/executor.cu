@@ -1018,6 +1018,20 @@ __device__ __forceinline__ void push_task(const ExecParams& P, int s, int phase)
 
 constexpr unsigned long long POP_EXIT = ~0ull;
 
+// Spin until a claimed queue position holds its entry; POP_EXIT if the run
+// ends or aborts first (only an overshooting ticket can wait that long).
+constexpr int TICKET_BACKLOG = 256;
+__device__ __noinline__ unsigned long long wait_entry(const ExecParams& P, const unsigned long long* slot) {
+  for (unsigned spin = 0;; ++spin) {
+    const unsigned long long v = ld_acquire_u64(slot);
+    if (v) return v;
+    if ((spin & 63) == 63) {
+      if (ld_relaxed_s32(P.abort_flag) || ld_relaxed_s32(P.remaining) <= 0) return POP_EXIT;
+      __nanosleep(128);
+    }
+  }
+}
+
 // Claim attempt over the priority levels (all 32 lanes; lane l holds the
 // head / tail snapshot of level l): the lowest non-empty level is claimed with
 // a CAS on its head. The entry is read speculatively alongside the CAS (queue
@@ -1031,15 +1045,26 @@ __device__ __forceinline__ unsigned long long claim_item(const ExecParams& P, in
     unsigned long long v = 0;
     int got = 0;
     if (lane == lev) {
-      const unsigned long long* slot = P.queue + P.q_off[lev] + h;
-      v = ld_relaxed_u64(slot);
-      const int prev = atomicCAS(P.q_head + lev, h, h + 1);
-      if (prev == h) {
-        while (v == 0ull) v = ld_relaxed_u64(slot);  // pusher reserved the slot, store in flight
-        fence_acq_rel_gpu();
+      if (t - h >= TICKET_BACKLOG) {
+        // deep level: a fetch-and-add ticket always succeeds in one round trip
+        // (148 producers CAS-ing one head convoy at about one claim per round
+        // trip). Overshooting the tail would need hundreds of claims inside
+        // this window; if it happens the ticket still owns a unique position
+        // and waits for its push.
+        const int pos = atomicAdd(P.q_head + lev, 1);
+        v = wait_entry(P, P.queue + P.q_off[lev] + pos);
         got = 1;
       } else {
-        h = prev;  // lost the race: retry this level if still non-empty
+        const unsigned long long* slot = P.queue + P.q_off[lev] + h;
+        v = ld_relaxed_u64(slot);
+        const int prev = atomicCAS(P.q_head + lev, h, h + 1);
+        if (prev == h) {
+          if (v == 0ull) v = wait_entry(P, slot);  // pusher reserved the slot, store in flight
+          fence_acq_rel_gpu();
+          got = 1;
+        } else {
+          h = prev;  // lost the race: retry this level if still non-empty
+        }
       }
     }
     const unsigned won = __ballot_sync(0xffffffffu, got);
@@ -1221,7 +1246,7 @@ __device__ __forceinline__ unsigned long long produce_item(unsigned long long e,
       __syncwarp();
     }
     const Job& jb = ctl.jobs[slot][jn < MAXJ ? jn : MAXJ + 1];
-    if (jb.type == J_SPECIAL) {
+    if (jb.type == J_SPECIAL) {  // it uses the ring as scratch: no loads until it is done
       while (ld_acquire_cta_u32(&ctl.jobs_done) < issued + 1) {
       }
       fence_proxy_async();
