@@ -36,6 +36,7 @@ using namespace tinv;
 static std::string g_err;
 // executor: next-item claim ahead of time only from levels with at least this
 // many ready items (TINV_PREFETCH_MIN overrides; 0 disables)
+static const int kTicketMin = 64;  // fetch-and-add claims on levels with this backlog (TINV_TICKET_MIN)
 static const int kPrefetchMin = 0;  // measured: hurts C2 (critical path), neutral on C3
 
 struct tinv_ctx {
@@ -1263,6 +1264,8 @@ int tinv_plan_exec(tinv_plan* p, tinv_err* err, double* ms) {
   {
     const char* pf = getenv("TINV_PREFETCH_MIN");
     P.prefetch_min = pf ? atoi(pf) : kPrefetchMin;
+    const char* tk = getenv("TINV_TICKET_MIN");
+    P.ticket_min = tk ? std::max(1, atoi(tk)) : kTicketMin;
   }
   if (getenv("TINV_PHASE_PROFILE")) {
     if (!p->d_phase) CK(c, cudaMalloc(&p->d_phase, (size_t)c->nsm * NPHASE * 8));

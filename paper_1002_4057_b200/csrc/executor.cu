@@ -1020,7 +1020,6 @@ constexpr unsigned long long POP_EXIT = ~0ull;
 
 // Spin until a claimed queue position holds its entry; POP_EXIT if the run
 // ends or aborts first (only an overshooting ticket can wait that long).
-constexpr int TICKET_BACKLOG = 256;
 __device__ __noinline__ unsigned long long wait_entry(const ExecParams& P, const unsigned long long* slot) {
   for (unsigned spin = 0;; ++spin) {
     const unsigned long long v = ld_acquire_u64(slot);
@@ -1037,7 +1036,8 @@ __device__ __noinline__ unsigned long long wait_entry(const ExecParams& P, const
 // a CAS on its head. The entry is read speculatively alongside the CAS (queue
 // entries are written once per run), then ordered with an acquire fence.
 // Returns 0 when every level is (or turned out) empty.
-__device__ __forceinline__ unsigned long long claim_item(const ExecParams& P, int h, int t, int minback = 1) {
+__device__ __forceinline__ unsigned long long claim_item(const ExecParams& P, int h, int t, int minback,
+                                                         bool tickets) {
   const int lane = threadIdx.x & 31;
   unsigned m = __ballot_sync(0xffffffffu, t - h >= minback);
   while (m) {
@@ -1045,15 +1045,19 @@ __device__ __forceinline__ unsigned long long claim_item(const ExecParams& P, in
     unsigned long long v = 0;
     int got = 0;
     if (lane == lev) {
-      if (t - h >= TICKET_BACKLOG) {
+      if (tickets && t - h >= P.ticket_min) {
         // deep level: a fetch-and-add ticket always succeeds in one round trip
         // (148 producers CAS-ing one head convoy at about one claim per round
-        // trip). Overshooting the tail would need hundreds of claims inside
-        // this window; if it happens the ticket still owns a unique position
-        // and waits for its push.
+        // trip). Overshooting the tail needs ticket_min claims inside this
+        // window; if it happens the ticket still owns a unique position and
+        // waits for its push (or for the end of the run).
         const int pos = atomicAdd(P.q_head + lev, 1);
-        v = wait_entry(P, P.queue + P.q_off[lev] + pos);
-        got = 1;
+        if (pos < P.q_off[lev + 1] - P.q_off[lev]) {
+          v = wait_entry(P, P.queue + P.q_off[lev] + pos);
+          got = 1;
+        } else {
+          h = t;  // past the level's capacity: no item will ever be pushed there
+        }
       } else {
         const unsigned long long* slot = P.queue + P.q_off[lev] + h;
         v = ld_relaxed_u64(slot);
@@ -1086,7 +1090,8 @@ __device__ __forceinline__ unsigned long long try_pop(const ExecParams& P) {
     h = ld_relaxed_s32(P.q_head + lane);
     t = ld_relaxed_s32(P.q_tail + lane);
   }
-  return claim_item(P, h, t, P.prefetch_min);
+  // CAS only: an overshooting ticket could wait for a push behind this CTA's own item
+  return claim_item(P, h, t, P.prefetch_min, false);
 }
 
 // Blocking pop (all 32 lanes): spins until an item is claimed, every task is
@@ -1108,7 +1113,7 @@ __device__ unsigned long long pop_item(const ExecParams& P) {
       rem = ld_relaxed_s32(P.remaining);
     }
     if (__shfl_sync(0xffffffffu, ab || rem <= 0, 0)) return POP_EXIT;
-    const unsigned long long v = claim_item(P, h, t);
+    const unsigned long long v = claim_item(P, h, t, 1, true);
     if (v) return v;
     __nanosleep(spin < 64 ? 32 : 256);
     ++spin;

@@ -89,6 +89,7 @@ struct ExecParams {
   unsigned long long t0;           // globaltimer at launch (trace base)
   unsigned long long* phase;       // optional per-CTA phase cycle counters (NPHASE each)
   int prefetch_min;                // claim the next item ahead only from levels with this backlog (0: never)
+  int ticket_min;                  // levels with at least this backlog are claimed by fetch-and-add
   // multi-GPU transfers
   double* peer_pool[MAX_RANKS];    // pools of the ranks (peer-mapped; the local pool for self)
   int32_t* peer_inbox[MAX_RANKS];  // inbox flag arrays of the ranks

@@ -251,6 +251,25 @@ def test_variants_and_determinism():
         assert np.array_equal(r, runs[0])
 
 
+@pytest.mark.parametrize("ticket,prefetch", [("1", "0"), ("3", "0"), ("64", "1"), ("1", "2")])
+def test_scheduler_claim_modes_bitwise(monkeypatch, ticket, prefetch):
+    # fetch-and-add tickets on every level (overshooting tails, tickets past a
+    # level's capacity) and ahead-of-time claims must run every item exactly
+    # once: the result is bitwise the default schedule's
+    n, b = 1536, 128
+    a = O.spd_matrix(n, 6, 0.5)
+    cfg = P.VariantConfig(P.Placement.OUT_OF_PLACE)
+    base = P.invert(a, b, cfg)
+    monkeypatch.setenv("TINV_TICKET_MIN", ticket)
+    monkeypatch.setenv("TINV_PREFETCH_MIN", prefetch)
+    for _ in range(2):
+        assert np.array_equal(P.invert(a, b, cfg), base)
+    xb = P.invert_batched(np.stack([a[:256, :256]] * 40), 128)
+    monkeypatch.delenv("TINV_TICKET_MIN")
+    monkeypatch.delenv("TINV_PREFETCH_MIN")
+    assert np.array_equal(xb, P.invert_batched(np.stack([a[:256, :256]] * 40), 128))
+
+
 def test_layout_roundtrip_and_trace(tmp_path):
     n, b = 640, 160
     a = np.random.default_rng(5).standard_normal((n, n))
