@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--placement", default="out", choices=["in", "out"])
     p.add_argument("--loops", default="UDU")
     p.add_argument("--barriered", action="store_true")
+    p.add_argument("--no-steps", action="store_true", help="skip the per-step / barriered breakdown")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-sample-n", type=int, default=None)
@@ -354,6 +355,42 @@ def main():
     sym_err = float((xc - xc.transpose(-1, -2)).abs().max())
     del r, eye, ac, xc
 
+    # per-step device times (each step on the previous one's
+    # output, same store) and pipelined vs barriered full inversion
+    steps_breakdown = None
+    if batch == 1 and mg is None and not args.no_steps:
+        def med_ms(plans, reps=3):
+            out = []
+            for _ in range(reps):
+                ctx.put_dense_device(a.data_ptr(), n)
+                cur = []
+                for pl in plans:
+                    rc, err, ms = pl.run()
+                    if rc != 0:
+                        raise RuntimeError(f"executor failed: {pl.msg}")
+                    cur.append(ms)
+                out.append(cur)
+            return [statistics.median(c[k] for c in out) for k in range(len(plans))]
+
+        plc = P.Placement(args.placement)
+        sps = [P.gen_step1(t, args.loops[0]), P.gen_step2(t, args.loops[1], plc), P.gen_step3(t, args.loops[2], plc)]
+        step_plans = [_native.Plan(ctx, q.table(), t, np.zeros(0, np.int64)) for q in sps]
+        ms1, ms2, ms3 = med_ms(step_plans)
+        for q in step_plans:
+            q.close()
+        other = P.gen_inversion(t, P.VariantConfig(plc, args.loops, not pipelined))
+        op = _native.Plan(ctx, other.table(), t, np.array(sorted(other.barriers), dtype=np.int64))
+        (ms_other,) = med_ms([op])
+        op.close()
+        pipe_ms, bar_ms = (kern_avg, ms_other) if pipelined else (ms_other, kern_avg)
+        steps_breakdown = {
+            "unit": "ms (device, median of 3; kernel only, input resident)",
+            "step1_potrf_ms": ms1, "step2_trtri_ms": ms2, "step3_lauum_ms": ms3, "sum_of_steps_ms": ms1 + ms2 + ms3,
+            "step_gflops": [flops / 3 / (m * 1e-3) / 1e9 for m in (ms1, ms2, ms3)],
+            "pipelined_ms": pipe_ms, "barriered_ms": bar_ms,
+            "pipelining_gain": bar_ms / pipe_ms,
+        }
+
     # end to end through the C-ABI with pinned host buffers
     e2e = None
     if not args.no_e2e and mg is not None:
@@ -429,6 +466,8 @@ def main():
             "clocks": clk.summary(),
             "e2e": e2e, "cpu_baseline": cpu,
         }
+        if steps_breakdown is not None:
+            out["steps_breakdown"] = steps_breakdown
         print(json.dumps(out))
     ctx.close()
     if dist is not None:
