@@ -48,7 +48,10 @@ def parse():
     p.add_argument("--nb", type=int, default=None)
     p.add_argument("--batch", type=int, default=None)
     p.add_argument("--placement", default="out", choices=["in", "out"])
-    p.add_argument("--loops", default="UDU")
+    p.add_argument("--loops", default=None,
+                   help="loop orders of the three steps; default DDU at c3 (result tiles become final "
+                        "progressively, so the device->host copies overlap the run; same kernel time as UDU), "
+                        "UDU (the reference default) elsewhere")
     p.add_argument("--barriered", action="store_true")
     p.add_argument("--no-steps", action="store_true", help="skip the per-step / barriered breakdown")
     p.add_argument("--no-e2e", action="store_true")
@@ -195,6 +198,8 @@ def main():
     wl = {"c1": (1024, 128, 1), "c2": (8192, 256, 1), "c3": (32768, 512, 1), "c4": (256, 256, 8192)}[args.workload]
     n = args.n or wl[0]
     nb = args.nb or wl[1]
+    if args.loops is None:
+        args.loops = "DDU" if args.workload == "c3" else "UDU"
     batch = args.batch or wl[2]
     if args.cpu_sample_n is None:
         args.cpu_sample_n = min(n, 8192) if batch == 1 else n
@@ -397,38 +402,44 @@ def main():
         e2e = {"value": None, "unit": "Gflop/s", "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                "note": "not measured for the distributed run (plans are bound to the exported stores)"}
     elif not args.no_e2e:
+        # the public host-buffer call (invert_host / invert_batched_host): A's
+        # lower tiles stream host -> device while the executor runs, result
+        # tiles stream back (mirrored) as they become final; the compiled plan
+        # is cached by the first (warm-up) call
         ha = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
         ha.copy_(a)
         hx = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
         del a, x
-        torch.cuda.empty_cache()
-        ha_np, hx_np = ha.numpy().reshape(-1, n), hx.numpy().reshape(-1, n)
         ctx.set_stream(0)
         plan.close()
+        ctx.close()
+        torch.cuda.empty_cache()
+        ha_np, hx_np = ha.numpy(), hx.numpy()
+        cfg = P.VariantConfig(P.Placement(args.placement), args.loops, pipelined)
 
         def e2e_step():
-            st = P.gen_inversion(t, P.VariantConfig(P.Placement(args.placement), args.loops, pipelined))
-            ctx.put_dense(ha_np)
-            pl = _native.Plan(ctx, st.table(), t, np.array(sorted(st.barriers), dtype=np.int64))
-            rc, err, _ = pl.run()
-            pl.close()
-            if rc != 0:
-                raise RuntimeError("e2e executor failed")
-            ctx.get_dense(hx_np, _native.DENSE_SYMMETRIZE)
+            if batch == 1:
+                P.invert_host(ha_np, nb, cfg, out=hx_np, device=local)
+            else:
+                P.invert_batched_host(ha_np, nb, cfg, out=hx_np, device=local)
 
         e2e_step()
         barrier()
-        t0 = time.perf_counter()
         k = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
         for _ in range(k):
             e2e_step()
         barrier()
         e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / k)
         T = t * (t + 1) // 2
         e2e = {"value": world * flops / (e2e_ms * 1e-3) / 1e9, "unit": "Gflop/s",
-               "h2d_bytes_per_step": T * nb * nb * 8 if batch == 1 else in_bytes, "d2h_bytes_per_step": in_bytes,
+               "h2d_bytes_per_step": batch * T * nb * nb * 8, "d2h_bytes_per_step": in_bytes,
                "ms_per_step": e2e_ms, "steps": k,
-               "path": "gen_stream + put_dense(pinned host) + plan_create + plan_exec + get_dense(symmetrize, pinned host)"}
+               "path": ("paper_1002_4057_b200.invert_host(pinned A, out=pinned X): lower tiles host->device by the "
+                        "copy engines overlapped with the executor, result tiles device->host (symmetrized) as they "
+                        "become final; plan cached after the warm-up call")}
+        P.clear_plan_cache()
+        ctx = None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -469,7 +480,8 @@ def main():
         if steps_breakdown is not None:
             out["steps_breakdown"] = steps_breakdown
         print(json.dumps(out))
-    ctx.close()
+    if ctx is not None:
+        ctx.close()
     if dist is not None:
         dist.destroy_process_group()
 

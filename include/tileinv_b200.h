@@ -75,6 +75,7 @@ extern "C" {
 #define TINV_SERIAL 1u          /* chain tasks in stream order (run_in_order) */
 #define TINV_TRACE 2u           /* record per-task device timestamps          */
 #define TINV_KEEP_ON_FAILURE 4u /* snapshot the matrix; restore it if a task fails */
+#define TINV_STREAM_IO 8u       /* plan for tinv_plan_exec_host: tile arrivals and departures are tasks */
 
 /* tinv_get_dense modes */
 #define TINV_DENSE_LOWER_TILES 0 /* write only the lower tiles (to_dense on them) */
@@ -177,6 +178,20 @@ int tinv_ipc_reset(tinv_ctx* ctx);
 /* run the plan on the context's matrix; blocks. ms (optional) = device time
  * of the executor launch measured with CUDA events. */
 int tinv_plan_exec(tinv_plan* plan, tinv_err* err, double* ms);
+/* End to end with host buffers, transfers overlapped with the computation
+ * (replaces tinv_put_dense + tinv_plan_exec + tinv_get_dense, i.e.
+ * from_dense -> execute -> [symmetrize_lower(]to_dense[)], tile_matrix.py:84-119
+ * and scheduler.py:261). The plan must be made with TINV_STREAM_IO: the copy
+ * engines move A's lower tiles host -> device in column order while the
+ * executor already runs (a task reading a tile waits for its arrival), and
+ * every result tile is written into `x` by the executor as soon as its last
+ * writer is done (mode TINV_DENSE_*; SYMMETRIZE mirrors on the fly). `a`
+ * should be page-locked for the copies to be asynchronous; `x` must be
+ * page-locked (device-mapped) host memory, else TINV_ERR_BAD_ARG. Batched
+ * stores: matrix m at a + m*n*lda and x + m*n*ldx. `a` is never written; on
+ * failure `x` is unspecified. Not combinable with TINV_KEEP_ON_FAILURE. */
+int tinv_plan_exec_host(tinv_plan* plan, const double* a, int64_t lda, double* x, int64_t ldx, int mode,
+                        tinv_err* err, double* ms);
 int tinv_plan_destroy(tinv_plan* plan);
 /* plan statistics: exec tasks (incl. hidden INV tasks), work items, edges */
 int tinv_plan_stats(const tinv_plan* plan, int64_t* exec_tasks, int64_t* items, int64_t* edges);

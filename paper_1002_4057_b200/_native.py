@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("TINV_LIB") or os.path.join(_PKG, "libtileinv_b200.so"
 
 TASK_FIELDS = 16
 OK, ERR_NOT_SPD, ERR_SINGULAR, ERR_BAD_ARG, ERR_CUDA, ERR_STREAM, ERR_NO_DEVICE, ERR_INTERNAL = range(8)
-SERIAL, TRACE, KEEP_ON_FAILURE = 1, 2, 4
+SERIAL, TRACE, KEEP_ON_FAILURE, STREAM_IO = 1, 2, 4, 8
 DENSE_LOWER, DENSE_SYMMETRIZE = 0, 1
 
 # every symbol include/tileinv_b200.h declares
@@ -26,7 +26,7 @@ EXPORTS = (
     "tinv_shape", "tinv_set_stream", "tinv_put_dense", "tinv_get_dense", "tinv_put_dense_device", "tinv_get_dense_device",
     "tinv_put_tile", "tinv_get_tile", "tinv_gen_stream", "tinv_dag_edges", "tinv_dist_stream", "tinv_plan_create",
     "tinv_plan_create_xfer", "tinv_ipc_export", "tinv_ipc_open", "tinv_ipc_reset", "tinv_plan_exec",
-    "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
+    "tinv_plan_exec_host", "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
 )
 
 
@@ -89,6 +89,8 @@ def lib():
         "tinv_ipc_open": ([_P, _I32, _I32, ctypes.c_char_p, ctypes.c_char_p], ctypes.c_int),
         "tinv_ipc_reset": ([_P], ctypes.c_int),
         "tinv_plan_exec": ([_P, ctypes.POINTER(TinvErr), ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+        "tinv_plan_exec_host": ([_P, _P, _I64, _P, _I64, ctypes.c_int, ctypes.POINTER(TinvErr),
+                                 ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
         "tinv_plan_destroy": ([_P], ctypes.c_int),
         "tinv_plan_stats": ([_P, _I64P, _I64P, _I64P], ctypes.c_int),
         "tinv_plan_trace": ([_P, _I64P, _I64P, _I32P, _I64], ctypes.c_int),
@@ -270,6 +272,17 @@ class Plan:
             return self.rc, self.err, 0.0
         ms = ctypes.c_double()
         rc = lib().tinv_plan_exec(self.h, ctypes.byref(self.err), ctypes.byref(ms))
+        self.msg = last_error(self.ctx.h) if rc != OK else ""
+        return rc, self.err, ms.value
+
+    def run_host(self, a_ptr, lda, x_ptr, ldx, mode=DENSE_SYMMETRIZE):
+        """Streamed end to end (STREAM_IO plans): host input -> executor -> host
+        output, transfers overlapped with the computation. -> (rc, TinvErr, ms)."""
+        if self.rc != OK:
+            return self.rc, self.err, 0.0
+        ms = ctypes.c_double()
+        rc = lib().tinv_plan_exec_host(self.h, a_ptr, lda, x_ptr, ldx, mode, ctypes.byref(self.err),
+                                       ctypes.byref(ms))
         self.msg = last_error(self.ctx.h) if rc != OK else ""
         return rc, self.err, ms.value
 

@@ -29,15 +29,21 @@ cudaError_t launch_get(double* dst, int64_t ldd, int64_t row0, const double* poo
                        int64_t ntiles, int symmetrize, cudaStream_t st, int64_t T1, int64_t mstride);
 cudaError_t launch_copy_slots(double* pool, int64_t slot_elems, const int32_t* from, const int32_t* to,
                               int64_t n, cudaStream_t st);
+cudaError_t launch_pad(double* pool, int64_t slot_elems, const int32_t* slot_of, int b, int bp, int64_t ntiles,
+                       int64_t T1, cudaStream_t st);
 }  // namespace tinv
 
 using namespace tinv;
 
 static std::string g_err;
-// executor: next-item claim ahead of time only from levels with at least this
-// many ready items (TINV_PREFETCH_MIN overrides; 0 disables)
-static const int kTicketMin = 64;  // fetch-and-add claims on levels with this backlog (TINV_TICKET_MIN)
-static const int kPrefetchMin = 0;  // measured: hurts C2 (critical path), neutral on C3
+// executor tunables (environment overrides for experiments):
+// fetch-and-add claims on ready levels with at least this backlog (TINV_TICKET_MIN)
+static const int kTicketMin = 64;
+// next-item claim ahead of time from levels with at least this backlog; 0 = off
+// (TINV_PREFETCH_MIN; measured: hurts C2's critical path, neutral on C3)
+static const int kPrefetchMin = 0;
+// bottom-level weight of a streamed-output departure in b^3 units (TINV_DEPART_WEIGHT)
+static const double kDepartWeight = 0.0;
 
 struct tinv_ctx {
   int64_t n = 0, b = 0, t = 0, bp = 0, R = 0, T = 0;
@@ -51,6 +57,7 @@ struct tinv_ctx {
   int rank = -1, world = 0;
   int device = 0, nsm = 0;
   cudaStream_t st = nullptr, st2 = nullptr, own = nullptr;
+  cudaStream_t dst[8] = {};  // device -> host copy streams of streamed runs
   double* pool = nullptr;
   int64_t pool_slots = 0, slot_elems = 0;
   std::vector<int32_t> a_slot;  // current slot of each lower tile (home k or shadow T+k)
@@ -218,6 +225,8 @@ int tinv_destroy(tinv_ctx* c) {
     if (s) cudaFree(s);
   if (c->own) cudaStreamDestroy(c->own);
   if (c->st2) cudaStreamDestroy(c->st2);
+  for (cudaStream_t s : c->dst)
+    if (s) cudaStreamDestroy(s);
   delete c;
   return TINV_OK;
 }
@@ -579,6 +588,9 @@ double weight_of(int kind) {  // flops in units of b^3 (SURVEY.md §7 hard part 
       return 2.0;
     case TINV_COPY:
       return 0.05;
+    case KIND_ARRIVE:
+    case KIND_DEPART:
+      return 0.0;
     default:
       return 1.0;
   }
@@ -612,6 +624,11 @@ struct tinv_plan {
   unsigned long long* d_phase = nullptr;
   int64_t nrecv = 0;
   std::vector<int32_t> recv_task_h;
+  std::vector<int32_t> arrive_tile;  // TINV_STREAM_IO: logical tile of inbox index k (copy order)
+  std::vector<int32_t> depart_tile;  // matrix tiles in expected completion order (last writer's bottom level)
+  std::vector<uint8_t> rename_parity;  // per matrix tile: odd number of renaming writers (final slot = alt)
+  int32_t *d_depart_group = nullptr, *d_depart_count = nullptr;
+  int32_t *d_depart_seq = nullptr;  // observed completion order of the departures ([T] = counter)
   int32_t *d_recv_task = nullptr, *d_inbox = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<unsigned long long> h_ts, h_te;
@@ -776,7 +793,8 @@ int tinv_plan_destroy(tinv_plan* p) {
   cudaSetDevice(p->ctx->device);
   void* ptrs[] = {p->d_tasks, p->d_succ, p->d_indeg, p->d_done, p->d_cur,      p->d_alt,       p->d_queue, p->d_head,
                   p->d_tail,  p->d_ctr,  p->d_err,   p->d_progress, p->d_ts, p->d_te, p->d_tsm, p->d_snap_from,
-                  p->d_snap_to, p->d_phase, p->d_recv_task, p->d_inbox};
+                  p->d_snap_to, p->d_phase, p->d_recv_task, p->d_inbox, p->d_depart_group, p->d_depart_count,
+                  p->d_depart_seq};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->ev0) cudaEventDestroy(p->ev0);
@@ -851,10 +869,27 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
     tinv_plan_destroy(p);
     return fail(c, TINV_ERR_BAD_ARG, "barriers are not supported on a batched store");
   }
+  const bool sio = (flags & TINV_STREAM_IO) != 0;
+  if (sio && (aux || (flags & TINV_KEEP_ON_FAILURE))) {
+    tinv_plan_destroy(p);
+    return fail(c, TINV_ERR_BAD_ARG, "streamed host I/O excludes transfer plans and TINV_KEEP_ON_FAILURE");
+  }
   p->nref = n * nm;
   p->ref_kind.resize(n * nm);
   std::vector<XT> xs;
-  xs.reserve(nm * (n + n / 8 + 8));
+  xs.reserve(nm * (n + n / 8 + 8 + (sio ? 2 * c->T1 : 0)));
+  if (sio) {  // ARRIVE: every lower tile of every matrix, column order (the order step 1 consumes them)
+    for (int64_t m = 0; m < nm; ++m)
+      for (int j = 0; j < t; ++j)
+        for (int i = j; i < t; ++i) {
+          const int32_t o = (int32_t)(m * c->T1 + tri_index(i, j));
+          const int32_t seq = (int32_t)p->arrive_tile.size();
+          last_writer_exec[o] = (int32_t)xs.size();
+          xs.push_back({KIND_ARRIVE, 0, o, -1, -1, 2, -1, -1, seq, 0});
+          p->arrive_tile.push_back(o);
+        }
+    nrecv = (int64_t)p->arrive_tile.size();
+  }
   std::vector<char> is_aux;
   std::vector<int32_t> first_exec_of_ref(n * nm + 1, 0);
   for (int64_t rv = 0; rv < n * nm; ++rv) {
@@ -943,6 +978,16 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
     xs.push_back({kind, f[F_STEP], o, in0, in1, f[F_OM] == 2 ? 2 : 1, (int)v, -1, -1, xflags});
   }
   first_exec_of_ref[n * nm] = (int32_t)xs.size();
+  std::vector<int32_t> depart_lw;  // last writer of each departing tile
+  if (sio)  // DEPART: every lower tile of every matrix, after its last writer
+    for (int64_t m = 0; m < nm; ++m)
+      for (int i = 0; i < t; ++i)
+        for (int j = 0; j <= i; ++j) {
+          const int32_t o = (int32_t)(m * c->T1 + tri_index(i, j));
+          depart_lw.push_back(last_writer_exec[o]);
+          p->depart_tile.push_back(o);
+          xs.push_back({KIND_DEPART, 0, -1, o, -1, 0, -1, o, (i << 16) | j, 0});
+        }
   p->nexec = (int64_t)xs.size();
   p->nlogical = next_logical;
   const int64_t nx = p->nexec;
@@ -991,13 +1036,18 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
   // ---- items, renaming, priorities (flop-weighted bottom level)
   std::vector<double> bl(nx, 0.0);
   double blmax = 0.0;
+  // streamed output: a departure weighs like `dw` b^3 of work, pulling the
+  // chains that finish result tiles forward so the copy engines overlap them
+  const char* dws = getenv("TINV_DEPART_WEIGHT");
+  const double dw = dws ? atof(dws) : kDepartWeight;
   for (int64_t u = nx - 1; u >= 0; --u) {
     double m = 0.0;
     for (int32_t k = p->tasks[u].succ_begin; k < p->tasks[u].succ_end; ++k) m = std::max(m, bl[p->succ[k]]);
-    bl[u] = weight_of(xs[u].kind) + m;
+    bl[u] = (xs[u].kind == KIND_DEPART ? dw : weight_of(xs[u].kind)) + m;
     blmax = std::max(blmax, bl[u]);
   }
   std::vector<char> renamed_tile(p->nlogical, 0);
+  if (sio) p->rename_parity.assign(T, 0);
   std::vector<int64_t> lev_items(NLEV, 0);
   p->exec_ref.resize(nx);
   for (int64_t u = 0; u < nx; ++u) {
@@ -1021,14 +1071,34 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
         (alias && (x.kind == TINV_GEMM || x.kind == TINV_SYRK_SUB || x.kind == TINV_SYRK_ADD_T))) {
       d.flags |= TF_RENAMED;
       renamed_tile[x.out] = 1;
+      if (sio && x.out < T) p->rename_parity[x.out] ^= 1;
     }
-    if (x.kind == KIND_RECV) d.flags |= TF_EXTERNAL;
+    if (x.kind == KIND_RECV || x.kind == KIND_ARRIVE) d.flags |= TF_EXTERNAL;
     int lev = blmax > 0 ? (int)std::floor(NLEV * (1.0 - bl[u] / blmax)) : 0;
     lev = std::min(NLEV - 1, std::max(0, lev));
+    if (x.kind == KIND_DEPART) lev = 0;  // cheap, and the copy engines wait on it
     d.level = (int8_t)lev;
     lev_items[lev] += d.nitems;
     p->items += d.nitems;
     p->exec_ref[u] = x.ref;
+  }
+  if (sio) {  // departures in predicted completion order: the last writer's top level (earliest finish on
+              // unbounded workers); after a run the observed order replaces it (tinv_plan_exec_host)
+    std::vector<double> tl(nx, 0.0);
+    for (int64_t u = 0; u < nx; ++u) {
+      tl[u] += weight_of(xs[u].kind);
+      for (int32_t k = p->tasks[u].succ_begin; k < p->tasks[u].succ_end; ++k)
+        tl[p->succ[k]] = std::max(tl[p->succ[k]], tl[u]);
+    }
+    std::vector<int32_t> ord(p->depart_tile.size());
+    for (size_t k = 0; k < ord.size(); ++k) ord[k] = (int32_t)k;
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+      const double ax = depart_lw[x] >= 0 ? tl[depart_lw[x]] : 0.0, ay = depart_lw[y] >= 0 ? tl[depart_lw[y]] : 0.0;
+      return ax < ay;
+    });
+    std::vector<int32_t> dt(ord.size());
+    for (size_t k = 0; k < ord.size(); ++k) dt[k] = p->depart_tile[ord[k]];
+    p->depart_tile.swap(dt);
   }
   p->q_off[0] = 0;
   for (int l = 0; l < NLEV; ++l) p->q_off[l + 1] = p->q_off[l] + lev_items[l];
@@ -1058,7 +1128,7 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
   p->nrecv = nrecv;
   p->recv_task_h.assign(std::max<int64_t>(nrecv, 1), -1);
   for (int64_t u = 0; u < nx; ++u)
-    if (xs[u].kind == KIND_RECV) p->recv_task_h[xs[u].aux1] = (int32_t)u;
+    if (xs[u].kind == KIND_RECV || xs[u].kind == KIND_ARRIVE) p->recv_task_h[xs[u].aux1] = (int32_t)u;
 
   // ---- device buffers
   auto ckm = [&](void** ptr, size_t bytes) { return cudaMalloc(ptr, std::max<size_t>(bytes, 16)); };
@@ -1084,6 +1154,11 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
       tinv_plan_destroy(p);
       return fail(c, TINV_ERR_CUDA, "snapshot allocation failed");
     }
+  }
+  if (sio && (ckm((void**)&p->d_depart_group, T * 4) || ckm((void**)&p->d_depart_count, T * 4) ||
+              ckm((void**)&p->d_depart_seq, (T + 1) * 4))) {
+    tinv_plan_destroy(p);
+    return fail(c, TINV_ERR_CUDA, "departure counters allocation failed");
   }
   if (ckm((void**)&p->d_recv_task, p->recv_task_h.size() * 4) || ckm((void**)&p->d_inbox, p->recv_task_h.size() * 4)) {
     tinv_plan_destroy(p);
@@ -1174,16 +1249,151 @@ int tinv_plan_stats(const tinv_plan* p, int64_t* exec_tasks, int64_t* items, int
   return TINV_OK;
 }
 
+// streamed host I/O of one tinv_plan_exec_host call
+struct HostIO {
+  const double* a;
+  int64_t lda;
+  double* xhost;  // page-locked host output
+  int64_t ldx;
+  int mode;
+};
+constexpr int kDepartStreams = 8;
+
+typedef CUresult (*PFN_batchMemOp)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
+
+// Copy engines: A's lower tiles into their slots in inbox order, each followed
+// by its arrival flag (a stream write-value, ordered after the copy). Runs of
+// tiles contiguous on both sides (batched t = 1 stores) move as one copy.
+static int enqueue_arrivals(tinv_ctx* c, tinv_plan* p, const HostIO& io, int32_t* inbox, cudaStream_t st) {
+  static PFN_batchMemOp batch_mem_op = nullptr;
+  if (!batch_mem_op) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(c, cudaGetDriverEntryPoint("cuStreamBatchMemOp", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(c, TINV_ERR_CUDA, "cuStreamBatchMemOp unavailable");
+    batch_mem_op = (PFN_batchMemOp)fn;
+  }
+  const int64_t na = (int64_t)p->arrive_tile.size(), b = c->b, bp = c->bp, n = c->n, T1 = c->T1;
+  const size_t tile_bytes = (size_t)c->slot_elems * 8;
+  std::vector<CUstreamBatchMemOpParams> ops;
+  for (int64_t s0 = 0; s0 < na;) {
+    const int32_t o = p->arrive_tile[s0];
+    const int64_t m = o / T1, k = o % T1;
+    int64_t i = (int64_t)((std::sqrt(8.0 * (double)k + 1.0) - 1.0) * 0.5);
+    while (i * (i + 1) / 2 > k) --i;
+    while ((i + 1) * (i + 2) / 2 <= k) ++i;
+    const int64_t j = k - i * (i + 1) / 2;
+    double* dst = c->pool + (int64_t)c->a_slot[o] * c->slot_elems;
+    const double* src = io.a + m * n * io.lda + i * b * io.lda + j * b;
+    int64_t run = 1;
+    if (T1 == 1 && b == bp && io.lda == n)
+      while (s0 + run < na && run < 64 && p->arrive_tile[s0 + run] == o + run &&
+             c->a_slot[o + run] == c->a_slot[o] + run)
+        ++run;
+    if (run > 1)
+      CK(c, cudaMemcpyAsync(dst, src, tile_bytes * run, cudaMemcpyHostToDevice, st));
+    else
+      CK(c, cudaMemcpy2DAsync(dst, bp * 8, src, io.lda * 8, b * 8, b, cudaMemcpyHostToDevice, st));
+    ops.assign(run, CUstreamBatchMemOpParams{});
+    for (int64_t r = 0; r < run; ++r) {
+      ops[r].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+      ops[r].writeValue.address = (CUdeviceptr)(inbox + s0 + r);
+      ops[r].writeValue.value = 1;
+      ops[r].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+    }
+    const CUresult r = batch_mem_op((CUstream)st, (unsigned)run, ops.data(), 0);
+    if (r != CUDA_SUCCESS) return fail(c, TINV_ERR_CUDA, "arrival flag write failed (CUresult " + std::to_string(r) + ")");
+    s0 += run;
+  }
+  return TINV_OK;
+}
+
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+// Copy engines, device -> host: for each copy group (departure order, spread
+// over kDepartStreams streams) wait until all its tiles departed, then move
+// them: LOWER: the tile's final slot (renaming parity decides cur or alt) to
+// block (i, j); SYMMETRIZE: off-diagonal tiles also their staged transpose to
+// block (j, i), diagonal tiles their staged mirrored form.
+static int enqueue_departures(tinv_ctx* c, tinv_plan* p, const HostIO& io, const std::vector<int32_t>& gfirst,
+                              const std::vector<int32_t>& gsize, int64_t stage_base, cudaEvent_t after) {
+  static PFN_waitValue32 wait_value = nullptr;
+  if (!wait_value) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(c, cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(c, TINV_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+    wait_value = (PFN_waitValue32)fn;
+  }
+  for (int k = 0; k < kDepartStreams; ++k) {
+    if (!c->dst[k]) CK(c, cudaStreamCreateWithFlags(&c->dst[k], cudaStreamNonBlocking));
+    CK(c, cudaStreamWaitEvent(c->dst[k], after, 0));
+  }
+  const int64_t b = c->b, bp = c->bp, n = c->n, T = c->T, T1 = c->T1, ldx = io.ldx;
+  const bool sym = io.mode == TINV_DENSE_SYMMETRIZE;
+  double* X = io.xhost;
+  for (size_t g = 0; g < gfirst.size(); ++g) {
+    cudaStream_t s = c->dst[g % kDepartStreams];
+    if (wait_value((CUstream)s, (CUdeviceptr)(p->d_depart_count + g), (cuuint32_t)gsize[g], CU_STREAM_WAIT_VALUE_GEQ) !=
+        CUDA_SUCCESS)
+      return fail(c, TINV_ERR_CUDA, "departure wait failed");
+    const int64_t k = gfirst[g], m = k / T1, kk = k % T1;
+    int64_t i = (int64_t)((std::sqrt(8.0 * (double)kk + 1.0) - 1.0) * 0.5);
+    while (i * (i + 1) / 2 > kk) --i;
+    while ((i + 1) * (i + 2) / 2 <= kk) ++i;
+    const int64_t j = kk - i * (i + 1) / 2;
+    double* xm = X + m * n * ldx;
+    const double* fin = c->pool + (int64_t)(p->rename_parity[k] ? (c->a_slot[k] < T ? k + T : k) : c->a_slot[k]) *
+                                      c->slot_elems;
+    const double* stg = c->pool + (stage_base + k) * c->slot_elems;
+    if (gsize[g] > 1) {  // contiguous staged diagonal tiles of consecutive matrices
+      CK(c, cudaMemcpyAsync(xm, stg, (size_t)gsize[g] * c->slot_elems * 8, cudaMemcpyDeviceToHost, s));
+      continue;
+    }
+    if (!sym || i != j)
+      CK(c, cudaMemcpy2DAsync(xm + i * b * ldx + j * b, ldx * 8, fin, bp * 8, b * 8, b, cudaMemcpyDeviceToHost, s));
+    if (sym)
+      CK(c, cudaMemcpy2DAsync(xm + j * b * ldx + i * b, ldx * 8, stg, bp * 8, b * 8, b, cudaMemcpyDeviceToHost, s));
+  }
+  return TINV_OK;
+}
+
+static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO* io);
+
 int tinv_plan_exec(tinv_plan* p, tinv_err* err, double* ms) {
   set_err(err, -1, -1, TINV_OK, -1);
   if (!p) return TINV_ERR_BAD_ARG;
+  if (p->flags & TINV_STREAM_IO) return fail(p->ctx, TINV_ERR_BAD_ARG, "a TINV_STREAM_IO plan runs with tinv_plan_exec_host");
+  return plan_exec_impl(p, err, ms, nullptr);
+}
+
+int tinv_plan_exec_host(tinv_plan* p, const double* a, int64_t lda, double* x, int64_t ldx, int mode, tinv_err* err,
+                        double* ms) {
+  set_err(err, -1, -1, TINV_OK, -1);
+  if (!p) return TINV_ERR_BAD_ARG;
+  tinv_ctx* c = p->ctx;
+  if (!(p->flags & TINV_STREAM_IO)) return fail(c, TINV_ERR_BAD_ARG, "plan was not made with TINV_STREAM_IO");
+  if (!a || !x || lda < c->n || ldx < c->n || (mode != TINV_DENSE_LOWER_TILES && mode != TINV_DENSE_SYMMETRIZE))
+    return fail(c, TINV_ERR_BAD_ARG, "bad exec_host arguments");
+  CK(c, cudaSetDevice(c->device));
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, x) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+    cudaGetLastError();
+    return fail(c, TINV_ERR_BAD_ARG, "output must be page-locked host memory");
+  }
+  HostIO io{a, lda, x, ldx, mode};
+  return plan_exec_impl(p, err, ms, &io);
+}
+
+static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO* io) {
   tinv_ctx* c = p->ctx;
   const int64_t T = c->T, nx = p->nexec;
   CK(c, cudaSetDevice(c->device));
   const int64_t scratch_base = 2 * T + p->dyn_slots;
   const bool keep = (p->flags & TINV_KEEP_ON_FAILURE) != 0;
   const int64_t backup_base = scratch_base + c->nsm;
-  int rc = ensure_pool(c, backup_base + (keep ? T : 0));
+  const bool staged_out = io && io->mode == TINV_DENSE_SYMMETRIZE;
+  int rc = ensure_pool(c, backup_base + ((keep || staged_out) ? T : 0));
   if (rc) return rc;
   if (nx == 0) {
     if (ms) *ms = 0.0;
@@ -1261,6 +1471,36 @@ int tinv_plan_exec(tinv_plan* p, tinv_err* err, double* ms) {
     P.peer_pool[r] = c->peer_pool[r] ? c->peer_pool[r] : c->pool;
     P.peer_inbox[r] = c->peer_inbox[r] ? c->peer_inbox[r] : P.inbox;
   }
+  std::vector<int32_t> grp_first, grp_size;  // copy groups of departing tiles (in departure order)
+  if (io) {
+    P.depart_mode = io->mode;
+    P.stage_base = (int32_t)backup_base;  // staging tiles (SYMMETRIZE) use the snapshot region
+    // groups: runs of consecutive staged diagonal tiles that are contiguous in
+    // the host matrix too (batched t = 1 stores) move as one copy
+    std::vector<int32_t> hg(T, 0);
+    const bool runs = io->mode == TINV_DENSE_SYMMETRIZE && c->T1 == 1 && c->b == c->bp && io->ldx == c->n;
+    for (size_t x = 0; x < p->depart_tile.size(); ++x) {
+      const int32_t k = p->depart_tile[x];
+      if (runs && !grp_first.empty() && grp_size.back() < 64 && k == grp_first.back() + grp_size.back()) {
+        grp_size.back()++;
+      } else {
+        grp_first.push_back(k);
+        grp_size.push_back(1);
+      }
+      hg[k] = (int32_t)grp_first.size() - 1;
+    }
+    CK(c, cudaMemcpyAsync(p->d_depart_group, hg.data(), T * 4, cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemsetAsync(p->d_depart_count, 0, T * 4, st));
+    CK(c, cudaMemsetAsync(p->d_depart_seq + T, 0, 4, st));
+    P.depart_group = p->d_depart_group;
+    P.depart_count = p->d_depart_count;
+    P.depart_seq = p->d_depart_seq;
+    P.depart_seq_ctr = p->d_depart_seq + T;
+    if (c->bp != c->b) {  // padding of the arriving tiles (the copies move the b x b part only)
+      CK(c, cudaMemcpyAsync(c->d_a_slot, c->a_slot.data(), c->T * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+      CK(c, launch_pad(c->pool, c->slot_elems, c->d_a_slot, (int)c->b, (int)c->bp, c->T, c->T1, st));
+    }
+  }
   {
     const char* pf = getenv("TINV_PREFETCH_MIN");
     P.prefetch_min = pf ? atoi(pf) : kPrefetchMin;
@@ -1275,7 +1515,23 @@ int tinv_plan_exec(tinv_plan* p, tinv_err* err, double* ms) {
   CK(c, cudaEventRecord(p->ev0, st));
   CK(c, launch_exec(c->tmK, c->tmM, c->tmE, P, (int)c->b, c->nsm, st));
   CK(c, cudaEventRecord(p->ev1, st));
+  if (io)  // executor done (or aborted): release every copy group still waiting
+    CK(c, cudaMemsetAsync(p->d_depart_count, 0x7f, T * 4, st));
+  if (io) {  // copy engines, after the state reset above (ev0), concurrent with the executor
+    CK(c, cudaStreamWaitEvent(c->st2, p->ev0, 0));
+    int rc2 = enqueue_arrivals(c, p, *io, P.inbox, c->st2);
+    if (!rc2) rc2 = enqueue_departures(c, p, *io, grp_first, grp_size, backup_base, p->ev0);
+    if (rc2) {
+      cudaStreamSynchronize(st);
+      cudaDeviceSynchronize();
+      return rc2;
+    }
+  }
   CK(c, cudaStreamSynchronize(st));
+  if (io) {
+    CK(c, cudaStreamSynchronize(c->st2));
+    for (int k = 0; k < kDepartStreams; ++k) CK(c, cudaStreamSynchronize(c->dst[k]));
+  }
   if (ms) {
     float f = 0.f;
     cudaEventElapsedTime(&f, p->ev0, p->ev1);
@@ -1292,6 +1548,20 @@ int tinv_plan_exec(tinv_plan* p, tinv_err* err, double* ms) {
     CK(c, cudaMemcpy(p->h_ts.data(), p->d_ts, nx * 8, cudaMemcpyDeviceToHost));
     CK(c, cudaMemcpy(p->h_te.data(), p->d_te, nx * 8, cudaMemcpyDeviceToHost));
     CK(c, cudaMemcpy(p->h_tsm.data(), p->d_tsm, nx * 4, cudaMemcpyDeviceToHost));
+  }
+  if (p->d_ts && io && getenv("TINV_DEPART_PROFILE")) {  // when do result tiles become final?
+    unsigned long long t0 = ~0ull, t1 = 0;
+    std::vector<unsigned long long> de;
+    for (int64_t u = 0; u < nx; ++u) {
+      if (p->h_ts[u] != ~0ull) t0 = std::min(t0, p->h_ts[u]);
+      t1 = std::max(t1, p->h_te[u]);
+      if (p->tasks[u].kind == KIND_DEPART) de.push_back(p->h_te[u]);
+    }
+    std::sort(de.begin(), de.end());
+    fprintf(stderr, "[tinv depart] run %.1f ms; tiles final at (ms): ", (t1 - t0) * 1e-6);
+    for (double q : {0.1, 0.25, 0.5, 0.75, 0.9, 0.99, 1.0})
+      fprintf(stderr, "q%.2f %.1f ", q, (de[std::min(de.size() - 1, (size_t)(q * de.size()))] - t0) * 1e-6);
+    fprintf(stderr, "\n");
   }
   if (p->d_phase) {
     std::vector<unsigned long long> ph((size_t)c->nsm * NPHASE);
@@ -1337,13 +1607,19 @@ int tinv_plan_exec(tinv_plan* p, tinv_err* err, double* ms) {
   }
   // success: adopt the renamed slots of the matrix tiles
   CK(c, cudaMemcpy(c->a_slot.data(), p->d_cur, T * 4, cudaMemcpyDeviceToHost));
+  if (io && !(c->T1 == 1 && c->b == c->bp)) {  // next run: enqueue departures in the observed order
+    std::vector<int32_t> seq(T);
+    CK(c, cudaMemcpy(seq.data(), p->d_depart_seq, T * 4, cudaMemcpyDeviceToHost));
+    p->depart_tile.swap(seq);
+  }
   return TINV_OK;
 }
 
 int tinv_plan_trace(const tinv_plan* p, int64_t* start_ns, int64_t* end_ns, int32_t* sm, int64_t ntasks) {
   if (!p || ntasks < p->nref || p->h_ts.empty()) return TINV_ERR_BAD_ARG;
   unsigned long long base = ~0ull;
-  for (int64_t u = 0; u < p->nexec; ++u) base = std::min(base, p->h_ts[u]);
+  for (int64_t u = 0; u < p->nexec; ++u)
+    if (p->exec_ref[u] >= 0) base = std::min(base, p->h_ts[u]);
   for (int64_t r = 0; r < p->nref; ++r) {
     start_ns[r] = -1;
     end_ns[r] = -1;
@@ -1351,6 +1627,7 @@ int tinv_plan_trace(const tinv_plan* p, int64_t* start_ns, int64_t* end_ns, int3
   }
   for (int64_t u = 0; u < p->nexec; ++u) {
     const int32_t r = p->exec_ref[u];
+    if (r < 0) continue;  // ARRIVE / DEPART
     const int64_t s = (int64_t)(p->h_ts[u] - base), e = (int64_t)(p->h_te[u] - base);
     if (start_ns[r] < 0 || s < start_ns[r]) start_ns[r] = s;
     if (e > end_ns[r]) {

@@ -114,6 +114,12 @@ __device__ __forceinline__ int ld_acquire_sys_s32(const int32_t* p) {
   asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_relaxed_sys_s32(const int32_t* p) {
+  int v;
+  asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ void st_release_sys_s32(int32_t* p, int v) {
   asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -148,7 +154,7 @@ __device__ __forceinline__ int rho(int x) { return (x >> 1) | ((x & 1) << 2); }
 // ---------------------------------------------------------------- jobs
 enum Variant : int8_t { V_NT = 0, V_NN = 1, V_TN = 2 };
 enum JobType : int8_t { J_GEMM = 0, J_SPECIAL = 1 };
-enum Special : int8_t { SP_BPOTRF = 0, SP_BTRTRI = 1, SP_COPY_ROWS = 2, SP_SEND = 3, SP_BCOPYINV = 4 };
+enum Special : int8_t { SP_BPOTRF = 0, SP_BTRTRI = 1, SP_COPY_ROWS = 2, SP_SEND = 3, SP_BCOPYINV = 4, SP_DEPART = 5 };
 
 struct ItemInfo {
   int32_t task, item, phase, kind, step;  // phase: phase group index (queue entry)
@@ -272,6 +278,10 @@ __device__ __forceinline__ void get_job_phase(const ItemInfo& it, int n, int R, 
   }
   if (kind == KIND_SEND) {
     special_job(j, SP_SEND, 0, x, -1);
+    return;
+  }
+  if (kind == KIND_DEPART) {  // block (item / R, item % R) of the result tile -> host
+    special_job(j, SP_DEPART, it.item, x, -1);
     return;
   }
   int r, c;
@@ -993,6 +1003,41 @@ __device__ __noinline__ void run_special(const Job& jb, const ItemInfo& it, cons
       zero_upper_row(dst, d, R, bp);
       break;
     }
+    case SP_DEPART: {
+      // SYMMETRIZE output: the tile's staging slot receives the transposed
+      // tile (off-diagonal; the copy engines move it to block (j, i) of the
+      // host matrix) or the mirrored full tile (diagonal). LOWER: nothing to
+      // do; the copy engines read the final slot itself once the task is done.
+      if (P.depart_mode != TINV_DENSE_SYMMETRIZE) break;
+      const int br = d / R, bc = d % R;
+      const bool diag = (aux1 >> 16) == (aux1 & 0xffff);
+      if (diag && br < bc) break;  // covered by the transposed copy of block (bc, br)
+      const double* src = P.pool + (int64_t)src_s * P.slot_elems + (int64_t)br * BLK * bp + bc * BLK;
+      double* stg = P.pool + (int64_t)(P.stage_base + aux0) * P.slot_elems;
+      for (int e = threadIdx.x; e < BLK * BLK / 2; e += 256) {
+        const int y = e >> 6, x2 = (e & 63) * 2;
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(src + (int64_t)y * bp + x2));
+        S[y * SLD + x2] = v.x;
+        S[y * SLD + x2 + 1] = v.y;
+      }
+      cons_bar();
+      if (diag) {  // block (br, bc) of the mirrored tile: verbatim (diagonal block: mirrored inside)
+        double* o = stg + (int64_t)br * BLK * bp + bc * BLK;
+        for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
+          const int y = e >> 7, x = e & (BLK - 1);
+          o[(int64_t)y * bp + x] = (br == bc && x > y) ? S[x * SLD + y] : S[y * SLD + x];
+        }
+      }
+      if (!diag || br > bc) {  // transposed block -> (bc, br)
+        double* o = stg + (int64_t)bc * BLK * bp + br * BLK;
+        for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
+          const int x = e >> 7, y = e & (BLK - 1);
+          o[(int64_t)x * bp + y] = S[y * SLD + x];
+        }
+      }
+      cons_bar();
+      break;
+    }
     case SP_COPY_ROWS: {
       const double* src = P.pool + (int64_t)src_s * P.slot_elems + (int64_t)d * BLK * bp;
       double* out = dst + (int64_t)d * BLK * bp;
@@ -1167,6 +1212,11 @@ __device__ void complete_item(const ExecParams& P, const Rec& r) {
           if (P.trace_end) {
             atomicMax(P.trace_end + task, globaltimer() - P.t0);
             P.trace_sm[task] = (int)smid();
+          }
+          if (t.kind == KIND_DEPART) {  // result tile final (and staged): release its copy-engine group
+            P.depart_seq[atomicAdd(P.depart_seq_ctr, 1)] = t.aux0;
+            __threadfence_system();
+            atomicAdd_system(P.depart_count + P.depart_group[t.aux0], 1);
           }
           __threadfence();
         }
@@ -1396,20 +1446,42 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (warp == NCONS_WARPS + 2) {
       // ============================ inbox poller (one per launch): completes RECV tasks
       if (blockIdx.x != 0 || P.nrecv == 0) return;
-      for (;;) {
+      // Entries below `lo` are all consumed. Flags mostly arrive in inbox
+      // order (ARRIVE: copy order; RECV: send order), so each round scans a
+      // window of PWIN entries from `lo` with all loads in flight at once, and
+      // every 64th idle round scans everything beyond it.
+      constexpr int PW = 8, PWIN = PW * 32;
+      int lo = 0;
+      for (unsigned round = 0;; ++round) {
         if (ld_relaxed_s32(P.abort_flag) || ld_relaxed_s32(P.remaining) <= 0) break;
         bool any = false;
-        for (int base = 0; base < P.nrecv; base += 32) {
-          const int i = base + lane;
-          const int found = (i < P.nrecv && P.recv_task[i] >= 0 && ld_acquire_sys_s32(P.inbox + i) == 1) ? 1 : 0;
-          unsigned m = __ballot_sync(FULL, found);
-          while (m) {
-            const int idx = base + __ffs(m) - 1;
-            m &= m - 1;
-            if (lane == 0) P.inbox[idx] = 2;
-            __syncwarp();
-            complete_item(P, Rec{R_ITEM_END, P.recv_task[idx], 1, -1, 0, 0, 0, 0});
-            any = true;
+        const bool full = (round & 63) == 63;
+        for (int base = lo; base < (full ? P.nrecv : min(P.nrecv, lo + PWIN)); base += PWIN) {
+          int fl[PW], tk[PW];
+#pragma unroll
+          for (int k = 0; k < PW; ++k) {
+            const int i = base + k * 32 + lane;
+            tk[k] = i < P.nrecv ? __ldg(P.recv_task + i) : -1;
+            fl[k] = (tk[k] >= 0) ? ld_relaxed_sys_s32(P.inbox + i) : 2;
+          }
+          bool lead = base == lo;  // consumed prefix of the window -> advance lo
+#pragma unroll
+          for (int k = 0; k < PW; ++k) {
+            unsigned m = __ballot_sync(FULL, fl[k] == 1);
+            if (m) fence_acq_rel_sys();
+            while (m) {
+              const int idx = base + k * 32 + __ffs(m) - 1;
+              m &= m - 1;
+              if (lane == 0) P.inbox[idx] = 2;
+              __syncwarp();
+              complete_item(P, Rec{R_ITEM_END, P.recv_task[idx], 1, -1, 0, 0, 0, 0});
+              any = true;
+            }
+            const bool done = __all_sync(FULL, fl[k] != 0);
+            if (lead && done)
+              lo = base + (k + 1) * 32;
+            else
+              lead = false;
           }
         }
         if (!any) __nanosleep(256);

@@ -139,6 +139,29 @@ cudaError_t launch_get(double* dst, int64_t ldd, int64_t row0, const double* poo
   return cudaGetLastError();
 }
 
+// Padding only (streamed arrivals copy the b x b part): rows / columns >= b
+// of every lower tile slot; identity on diagonal tiles, zero elsewhere.
+__global__ void __launch_bounds__(256) k_pad(double* __restrict__ pool, int64_t slot_elems,
+                                            const int32_t* __restrict__ slot_of, int b, int bp, int64_t T1) {
+  int i, j;
+  const int64_t x = blockIdx.x;
+  tri_decode(x % T1, i, j);
+  double* dst = pool + (int64_t)slot_of[x] * slot_elems;
+  const int rr = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (rr >= bp) return;
+  double* drow = dst + (int64_t)rr * bp;
+  for (int cc = (rr < b ? b : 0) + (threadIdx.x & 31); cc < bp; cc += 32)
+    drow[cc] = (i == j && rr == cc) ? 1.0 : 0.0;
+}
+
+cudaError_t launch_pad(double* pool, int64_t slot_elems, const int32_t* slot_of, int b, int bp, int64_t ntiles,
+                       int64_t T1, cudaStream_t st) {
+  if (ntiles <= 0 || b == bp) return cudaSuccess;
+  dim3 grid((unsigned)ntiles, (unsigned)((bp + 7) / 8));
+  k_pad<<<grid, 256, 0, st>>>(pool, slot_elems, slot_of, b, bp, T1);
+  return cudaGetLastError();
+}
+
 // D2D copy of whole slots (snapshot / restore for TINV_KEEP_ON_FAILURE)
 __global__ void k_copy_slots(double* pool, int64_t slot_elems, const int32_t* from, const int32_t* to) {
   const double2* s = reinterpret_cast<const double2*>(pool + (int64_t)from[blockIdx.y] * slot_elems);

@@ -37,10 +37,18 @@ constexpr int KIND_INV = 11;
 constexpr int KIND_SEND = 12;
 constexpr int KIND_RECV = 13;
 constexpr int MAX_RANKS = 8;
+// Streamed host I/O pseudo-tasks (TINV_STREAM_IO plans): ARRIVE writes an
+// input tile (the copy engine does; completed by the inbox poller when its
+// arrival flag is set); DEPART reads a final result tile (SYMMETRIZE: writes
+// its transposed / mirrored copy into a staging slot, one item per 128-block)
+// and, when complete, counts it in its copy group, which the copy engines
+// wait on before moving the tile to the host.
+constexpr int KIND_ARRIVE = 14;
+constexpr int KIND_DEPART = 15;
 
 enum TaskFlags : int32_t {
   TF_RENAMED = 1,   // output written to the alternate slot, slots swapped at completion
-  TF_EXTERNAL = 2,  // never queued: completed by the inbox poller (RECV)
+  TF_EXTERNAL = 2,  // never queued: completed by the inbox poller (RECV, ARRIVE)
   TF_DIAG_FROM_AUX = 4,  // TRTRI / INV: diagonal-block inverses copied from the POTRF aux tile (in1)
 };
 
@@ -58,8 +66,8 @@ struct TaskDev {
   int32_t ref_id;  // reference task id (errors / trace)
   int32_t succ_begin;
   int32_t succ_end;
-  int32_t aux0;    // SEND: destination rank
-  int32_t aux1;    // SEND / RECV: receive sequence number (inbox index, slot recv_base + seq)
+  int32_t aux0;    // SEND: destination rank; DEPART: matrix tile id (staging slot / copy group)
+  int32_t aux1;    // SEND / RECV / ARRIVE: inbox index (RECV: slot recv_base + seq); DEPART: i << 16 | j
 };
 
 struct ExecParams {
@@ -97,6 +105,13 @@ struct ExecParams {
   const int32_t* recv_task;        // inbox index -> exec task id (-1: not received here)
   int32_t nrecv;                   // inbox length
   int32_t recv_base;               // slot of receive sequence number 0 (same on every rank)
+  // streamed host output (DEPART; the copy engines do the device -> host moves)
+  int32_t depart_mode;             // TINV_DENSE_LOWER_TILES / TINV_DENSE_SYMMETRIZE
+  int32_t stage_base;              // slot of the staging tile of matrix tile 0 (SYMMETRIZE)
+  const int32_t* depart_group;     // matrix tile -> copy group
+  int32_t* depart_count;           // per copy group: departed tiles (the copy streams wait on it)
+  int32_t* depart_seq;             // observed departure order (matrix tile ids)
+  int32_t* depart_seq_ctr;
 };
 constexpr int NPHASE = 28;  // item-wait, mainloop, epilogue, job-end, item-end, completion, items, jobs,
                             // special: load, factor, inverse, store; potrf/trtri sub-steps;
@@ -118,7 +133,7 @@ inline int64_t tri_index(int64_t i, int64_t j) { return i * (i + 1) / 2 + j; }
 //    s >= 1: X[r][r-s] for r = s..R-1 (R-s items, two block GEMMs each).
 //  everything else: one phase.
 TINV_HD int phases_of(int kind, int R) {
-  if (kind == KIND_SEND || kind == KIND_RECV) return 1;
+  if (kind == KIND_SEND || kind == KIND_RECV || kind == KIND_ARRIVE) return 1;
   if (kind == TINV_POTRF) return 3 * R - 2;
   if (kind == TINV_TRTRI || kind == KIND_INV) return R;
   return 1;
@@ -140,6 +155,7 @@ TINV_HD int phase_items(int kind, int R, int p) {
       return R;
     case KIND_SEND:
     case KIND_RECV:
+    case KIND_ARRIVE:
       return 1;
     default:
       return R * R;

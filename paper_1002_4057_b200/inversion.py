@@ -84,3 +84,118 @@ def invert_batched(a: np.ndarray, nb: int | None = None, config: VariantConfig =
         return out
     finally:
         ctx.close()
+
+
+# ---------------------------------------------------------------- host-buffer fast path
+# (n, nb, batch, device, placement, loops, pipelined) -> (Context, Plan, TaskStream)
+_HOST_PLANS: dict = {}
+
+
+def clear_plan_cache() -> None:
+    """Release the device stores and plans kept by invert_host / invert_batched_host."""
+    for ctx, plan, _ in _HOST_PLANS.values():
+        plan.close()
+        ctx.close()
+    _HOST_PLANS.clear()
+
+
+def _host_buffer(x, name):
+    try:
+        import torch
+
+        if isinstance(x, torch.Tensor):
+            if x.device.type != "cpu":
+                raise ValueError(f"{name} must be a host array")
+            x = x.numpy()
+    except ImportError:  # pragma: no cover
+        pass
+    return x
+
+
+def _run_host(a: np.ndarray, out, nb: int, batch: int, config: VariantConfig, device: int) -> np.ndarray:
+    from . import _native
+    from .scheduler import ExecutionError, _cause
+    from .tile_matrix import InvalidSizeError
+
+    a = _host_buffer(a, "a")
+    if a.dtype != np.float64 or not a.flags.c_contiguous:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+    n = a.shape[-1]
+    if a.shape[-2] != n or n < 1 or nb < 1 or n % nb:
+        raise InvalidSizeError(f"matrix order {n} not divisible by tile order {nb}" if a.shape[-2] == n
+                               else f"expected square matrices, got shape {a.shape}")
+    out = np.empty_like(a) if out is None else _host_buffer(out, "out")
+    if out.shape != a.shape or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError("out must be a C-contiguous float64 array shaped like a")
+    t = n // nb
+    pipelined = True if batch > 1 else config.pipelined
+    key = (n, nb, batch, device, config.placement, config.loops, pipelined)
+    hit = _HOST_PLANS.get(key)
+    if hit is None:
+        s = gen_inversion(t, VariantConfig(config.placement, config.loops, pipelined, config.workers))
+        ctx = _native.Context(n, nb, device, batch=batch)
+        plan = _native.Plan(ctx, s.table(), t, np.array(sorted(s.barriers), dtype=np.int64), _native.STREAM_IO)
+        if plan.rc != _native.OK:
+            msg = plan.msg
+            plan.close()
+            ctx.close()
+            raise _native.NativeError(plan.rc, msg)
+        hit = _HOST_PLANS[key] = (ctx, plan, s)
+    ctx, plan, s = hit
+    rx = a.reshape(-1, n)
+    xo = out.reshape(-1, n)
+    rc, err, _ = plan.run_host(rx.ctypes.data, n, xo.ctypes.data, n, _native.DENSE_SYMMETRIZE)
+    if rc == _native.ERR_BAD_ARG and "page-locked" in plan.msg:
+        # output not page-locked: the staged path (put -> execute -> get) on the same store
+        ctx.put_dense(rx)
+        p2 = _native.Plan(ctx, s.table(), t, np.array(sorted(s.barriers), dtype=np.int64))
+        rc, err, _ = p2.run()
+        plan.msg = p2.msg
+        p2.close()
+        if rc == _native.OK:
+            ctx.get_dense(xo, _native.DENSE_SYMMETRIZE)
+    if rc != _native.OK:
+        msg = plan.msg
+        if err.task_id < 0:
+            raise _native.NativeError(rc, msg)
+        m, tid = divmod(err.task_id, len(s))
+        cause = _cause(err, msg)
+        exc = ExecutionError(s.tasks[tid], cause)
+        if batch > 1:
+            exc.matrix = m
+        raise exc from cause
+    return out
+
+
+def invert_host(a, nb: int, config: VariantConfig = VariantConfig(), out=None, device: int = 0) -> np.ndarray:
+    """A^-1 of an SPD matrix held in host memory, end to end on the B200 with
+    the transfers overlapped with the computation: symmetrize_lower(to_dense(
+    execute(gen_inversion(...), from_dense(a, nb)))) as one call.
+
+    A's lower tiles stream host -> device (copy engines, column order) while
+    the executor already factors the first panels, and each result tile is
+    written into `out` (mirrored) as soon as it is final. Pass page-locked
+    buffers (e.g. ``torch.empty(..., pin_memory=True).numpy()``) for the
+    overlap; other buffers take the staged path. The compiled plan and the
+    device store are cached per (n, nb, config, device) -- see
+    clear_plan_cache(). `a` is not pre-scanned for non-finite values (the
+    reference's from_dense check); such values surface as
+    NotPositiveDefiniteError from the factorization."""
+    a = _host_buffer(a, "a")
+    if np.ndim(a) != 2:
+        from .tile_matrix import InvalidSizeError
+
+        raise InvalidSizeError(f"expected a square matrix, got shape {np.shape(a)}")
+    return _run_host(a, out, nb, 1, config, device)
+
+
+def invert_batched_host(a, nb: int | None = None, config: VariantConfig = VariantConfig(), out=None,
+                        device: int = 0) -> np.ndarray:
+    """invert_batched with invert_host's streamed transfers (BASELINE config 4
+    end to end): a is (batch, n, n) in host memory, out likewise."""
+    a = _host_buffer(a, "a")
+    if np.ndim(a) != 3 or a.shape[1] != a.shape[2]:
+        from .tile_matrix import InvalidSizeError
+
+        raise InvalidSizeError(f"expected a (batch, n, n) array, got shape {np.shape(a)}")
+    return _run_host(a, out, a.shape[1] if nb is None else nb, a.shape[0], config, device)

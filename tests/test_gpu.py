@@ -346,3 +346,77 @@ def test_distributed_device_transport_bitwise(grid):
     tm = P.from_dense(a, b)
     execute_distributed(s, tm, grid, transport="device")
     assert np.array_equal(P.to_dense(tm), P.to_dense(ref))
+
+
+# ---------------------------------------------------------------- streamed host I/O (tinv_plan_exec_host)
+def _pinned(shape):
+    import torch
+
+    return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+
+
+@pytest.mark.parametrize("n,b,placement,pipelined", [(1536, 128, "out", True), (1000, 200, "in", True),
+                                                      (1152, 384, "out", False), (256, 256, "in", True)])
+def test_streamed_host_io_bitwise(n, b, placement, pipelined):
+    a = O.spd_matrix(n, 7, 0.5)
+    cfg = P.VariantConfig(P.Placement(placement), "UDU", pipelined)
+    ref = P.invert(a, b, cfg)
+    ha, hx = _pinned(a.shape), _pinned(a.shape)
+    ha[...] = a
+    for _ in range(2):  # second call: cached plan and store
+        hx.fill(np.nan)
+        P.invert_host(ha, b, cfg, out=hx)
+        assert np.array_equal(hx, ref)
+    # pageable output: staged fallback, same bits
+    assert np.array_equal(P.invert_host(a, b, cfg), ref)
+    P.clear_plan_cache()
+
+
+def test_streamed_lower_mode_and_batched():
+    n, b = 640, 128
+    a = O.spd_matrix(n, 8, 0.5)
+    t = n // b
+    s = P.gen_inversion(t, P.VariantConfig(P.Placement.OUT_OF_PLACE))
+    ctx = _native.Context(n, b)
+    ctx.put_dense(a)
+    plan = _native.Plan(ctx, s.table(), t, np.array(sorted(s.barriers), np.int64))
+    assert plan.run()[0] == 0
+    lower = np.full((n, n), np.nan)
+    ctx.get_dense(lower, _native.DENSE_LOWER)
+    plan.close()
+    sp = _native.Plan(ctx, s.table(), t, np.array(sorted(s.barriers), np.int64), _native.STREAM_IO)
+    ha, hx = _pinned((n, n)), _pinned((n, n))
+    ha[...] = a
+    hx.fill(np.nan)
+    rc, err, ms = sp.run_host(ha.ctypes.data, n, hx.ctypes.data, n, _native.DENSE_LOWER)
+    assert rc == 0, sp.msg
+    assert np.array_equal(np.isnan(hx), np.isnan(lower))  # upper tiles untouched
+    assert np.array_equal(np.nan_to_num(hx), np.nan_to_num(lower))
+    assert sp.run()[0] == _native.ERR_BAD_ARG  # a STREAM_IO plan needs host buffers
+    sp.close()
+    ctx.close()
+    rng = np.random.default_rng(4)
+    g = rng.standard_normal((40, 256, 256))
+    ab = g @ g.transpose(0, 2, 1) / 256 + np.eye(256)
+    ab = np.tril(ab) + np.transpose(np.tril(ab, -1), (0, 2, 1))
+    for nb in (256, 128):
+        ref = P.invert_batched(ab, nb)
+        hb, hy = _pinned(ab.shape), _pinned(ab.shape)
+        hb[...] = ab
+        P.invert_batched_host(hb, nb, out=hy)
+        assert np.array_equal(hy, ref)
+    P.clear_plan_cache()
+
+
+def test_streamed_failure_reports_task():
+    a = O.spd_matrix(512, 9, 0.5)
+    a[300, 300] = -50.0  # not SPD: POTRF of diagonal tile 2 (b=128) fails
+    ha, hx = _pinned(a.shape), _pinned(a.shape)
+    ha[...] = a
+    with pytest.raises(P.ExecutionError) as ei:
+        P.invert_host(ha, 128, out=hx)
+    with pytest.raises(P.ExecutionError) as ej:
+        P.invert(a, 128)
+    assert str(ei.value.task) == str(ej.value.task)
+    assert ei.value.cause.index == ej.value.cause.index
+    P.clear_plan_cache()
