@@ -720,12 +720,110 @@ __device__ __forceinline__ void warp_inv16(const double (&r)[16], double (&x)[16
   }
 }
 
+// Warp 0: factor the 16x16 diagonal block at (p0, p0) of S in place (lane
+// i & 15 holds row i; right-looking, shuffles), 1 / L[k][k] -> dinv[0..15],
+// failing pivots (kernels.py:68-71) folded into ctl.scan_min.
+__device__ __noinline__ void factor16(double* S, int p0, double* dinv, SmemCtl& ctl) {
+  const int lane = threadIdx.x & 31, i = lane & 15;
+  double r[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) r[j] = j <= i ? S[(p0 + i) * SLD + p0 + j] : 0.0;
+  unsigned badmask = 0;
+  double my_il = 1.0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const double piv = __shfl_sync(FULL, r[k], k);
+    const bool bad = !(piv > 0.0) || !isfinite(piv);
+    badmask |= bad ? (1u << k) : 0u;
+    const double il = bad ? 1.0 : rsqrt(piv);  // every lane, no broadcast needed
+    const double l = bad ? 1.0 : piv * il;
+    my_il = (i == k) ? il : my_il;
+    r[k] = (i == k) ? l : (i > k ? r[k] * il : r[k]);
+#pragma unroll
+    for (int j = 1; j < 16; ++j) {  // constant trip count: r[] stays in registers
+      if (j > k) {
+        const double v = __shfl_sync(FULL, r[k], j);
+        r[j] = (i >= j) ? fma(-r[k], v, r[j]) : r[j];
+      }
+    }
+  }
+  if (lane == 0 && badmask) atomicMin(&ctl.scan_min, p0 + __ffs(badmask) - 1);
+  if (lane < 16) {
+    dinv[i] = my_il;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) S[(p0 + i) * SLD + p0 + j] = j <= i ? r[j] : 0.0;
+  }
+}
+
+// Panel rows below the diagonal block at p0: v L_PP^T = a by forward
+// substitution, one row per thread of [t0, t0 + nt).
+__device__ __forceinline__ void panel_subst(double* S, int p0, const double* dinv, int t0, int nt) {
+  for (int row = p0 + 16 + t0; row < BLK; row += nt) {
+    double v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = S[row * SLD + p0 + k];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      double w0 = v[j], w1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 15; ++k) {  // constant trip count: v[] stays in registers
+        if (k < j) {
+          if (k & 1)
+            w1 -= v[k] * S[(p0 + j) * SLD + p0 + k];
+          else
+            w0 -= v[k] * S[(p0 + j) * SLD + p0 + k];
+        }
+      }
+      v[j] = (w0 + w1) * dinv[j];
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) S[row * SLD + p0 + k] = v[k];
+  }
+}
+
+// Trailing update by panel P of the 16x16 blocks (I, J), ja <= J <= jb,
+// J <= I <= 7: A[I][J] -= L[I][P] L[J][P]^T, 4x4 micro-tiles (strided
+// columns: conflict-free loads) over threads [t0, t0 + nt).
+__device__ __noinline__ void trailing16(double* S, int P, int ja, int jb, int t0, int nt) {
+  const int p0 = 16 * P;
+  int nblk = 0;
+  for (int J = ja; J <= jb; ++J) nblk += 8 - J;
+  for (int tt = t0; tt < 16 * nblk; tt += nt) {
+    int blk = tt >> 4, J = ja;
+    while (blk >= 8 - J) {
+      blk -= 8 - J;
+      ++J;
+    }
+    const int I = J + blk, mt = tt & 15;
+    const int r0 = 16 * I + 4 * (mt >> 2), c0 = 16 * J + (mt & 3);
+    double acc[4][4] = {};
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = S[(r0 + q) * SLD + p0 + k];
+        b[q] = S[(c0 + 4 * q) * SLD + p0 + k];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) acc[q][w] += a[q] * b[w];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) S[(r0 + q) * SLD + c0 + 4 * w] -= acc[q][w];
+  }
+}
+
 // In-place Cholesky of the lower 128x128 block in S (right-looking, 16-wide
-// panels): warp 0 factors the diagonal sub-block with shuffles, one thread per
-// row solves the panel by forward substitution, 4x4 micro-tiles update the
-// trailing lower part. Returns the first failing pivot (kernels.py:68-71) or -1.
+// panels, look-ahead): after panel P's substitution and the update of
+// column block P + 1, warp 0 factors panel P + 1 while warps 1-7 apply panel
+// P to the rest of the trailing matrix. Returns the first failing pivot
+// (kernels.py:68-71) or -1.
 __device__ int block_potrf(double* S, SmemCtl& ctl) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5;
   double* dinv = S + BLK * SLD;  // 1 / L[k][k] of the current panel
   if (tid == 0) ctl.scan_min = 1 << 30;
   cons_bar();
@@ -735,91 +833,20 @@ __device__ int block_potrf(double* S, SmemCtl& ctl) {
     if (tid == 0) ctl.dbg2[k] += now - tq;
     tq = now;
   };
+  if (warp == 0) factor16(S, 0, dinv, ctl);
+  cons_bar();
+  probe(0);
   for (int P = 0; P < 8; ++P) {
-    const int p0 = 16 * P;
-    if (warp == 0) {
-      const int i = lane & 15;
-      double r[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) r[j] = j <= i ? S[(p0 + i) * SLD + p0 + j] : 0.0;
-      unsigned badmask = 0;
-      double my_il = 1.0;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const double piv = __shfl_sync(FULL, r[k], k);
-        const bool bad = !(piv > 0.0) || !isfinite(piv);
-        badmask |= bad ? (1u << k) : 0u;
-        const double il = bad ? 1.0 : rsqrt(piv);  // every lane, no broadcast needed
-        const double l = bad ? 1.0 : piv * il;
-        my_il = (i == k) ? il : my_il;
-        r[k] = (i == k) ? l : (i > k ? r[k] * il : r[k]);
-#pragma unroll
-        for (int j = 1; j < 16; ++j) {  // constant trip count: r[] stays in registers
-          if (j > k) {
-            const double v = __shfl_sync(FULL, r[k], j);
-            r[j] = (i >= j) ? fma(-r[k], v, r[j]) : r[j];
-          }
-        }
-      }
-      if (lane == 0 && badmask) atomicMin(&ctl.scan_min, p0 + __ffs(badmask) - 1);
-      if (lane < 16) {
-        dinv[i] = my_il;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) S[(p0 + i) * SLD + p0 + j] = j <= i ? r[j] : 0.0;
-      }
-    }
-    cons_bar();
-    probe(0);
-    // panel rows: v L_PP^T = a by forward substitution
-    for (int row = p0 + 16 + tid; row < BLK; row += 256) {
-      double v[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = S[row * SLD + p0 + k];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        double w0 = v[j], w1 = 0.0;
-#pragma unroll
-        for (int k = 0; k < 15; ++k) {  // constant trip count: v[] stays in registers
-          if (k < j) {
-            if (k & 1)
-              w1 -= v[k] * S[(p0 + j) * SLD + p0 + k];
-            else
-              w0 -= v[k] * S[(p0 + j) * SLD + p0 + k];
-          }
-        }
-        v[j] = (w0 + w1) * dinv[j];
-      }
-#pragma unroll
-      for (int k = 0; k < 16; ++k) S[row * SLD + p0 + k] = v[k];
-    }
+    panel_subst(S, 16 * P, dinv, tid, 256);
     cons_bar();
     probe(1);
-    // trailing: A[I][J] -= A[I][P] A[J][P]^T, P < J <= I, 4x4 micro-tiles
-    const int m = 7 - P;
-    for (int tt = tid; tt < 16 * m * (m + 1) / 2; tt += 256) {
-      int ii, jj;
-      lower_pair(tt >> 4, ii, jj);
-      const int mt = tt & 15;  // rows r0..r0+3, columns c0 + 4w (strided: conflict-free loads)
-      const int r0 = 16 * (P + 1 + ii) + 4 * (mt >> 2), c0 = 16 * (P + 1 + jj) + (mt & 3);
-      double acc[4][4] = {};
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        double a[4], b[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          a[q] = S[(r0 + q) * SLD + p0 + k];
-          b[q] = S[(c0 + 4 * q) * SLD + p0 + k];
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int w = 0; w < 4; ++w) acc[q][w] += a[q] * b[w];
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int w = 0; w < 4; ++w) S[(r0 + q) * SLD + c0 + 4 * w] -= acc[q][w];
-    }
+    if (P == 7) break;
+    trailing16(S, P, P + 1, P + 1, tid, 256);  // column block P + 1: the next panel
+    cons_bar();
+    if (warp == 0)
+      factor16(S, 16 * (P + 1), dinv, ctl);
+    else if (P + 2 <= 7)
+      trailing16(S, P, P + 2, 7, tid - 32, 224);
     cons_bar();
     probe(2);
   }
