@@ -298,11 +298,23 @@ def main():
     mg = None
     scaling = "weak"
     if world > 1 and batch == 1:
+        from paper_1002_4057_b200.distributed import MultiGPU, _agree, owned_mask
         try:
-            from paper_1002_4057_b200.distributed import MultiGPU, owned_mask
             if pipelined is False:
                 raise RuntimeError("the distributed run is pipelined only")
-            mg = MultiGPU(s, ctx)
+            why = None
+            try:
+                mg = MultiGPU(s, ctx)
+            except Exception as exc:  # noqa: BLE001
+                why = exc
+            if not _agree(why is None):  # every rank learns about a failure on any rank
+                raise why or RuntimeError("distributed setup failed on a peer rank")
+            # trial run: any failure on any rank (incl. the executor's 30 s
+            # no-progress watchdog) sends every rank to the replica fallback
+            ctx.put_dense_device(a.data_ptr(), n)
+            rc_t, _, _ = mg.run()
+            if not _agree(rc_t == 0):
+                raise RuntimeError(f"distributed trial run failed (rc {rc_t} on rank {rank})")
             scaling = "strong"
             st = mg.dist.stats(nb)
             config["parallelism"] = f"2d-block-cyclic {mg.grid[0]}x{mg.grid[1]} (tile versions over NVLink peer memory)"
@@ -310,7 +322,10 @@ def main():
             config["transfers"] = st["transfers"]
         except Exception as exc:  # noqa: BLE001 -- report and fall back
             mg = None
-            config["parallelism"] = f"replicas x{world} (distributed setup failed: {type(exc).__name__}: {exc})"[:300]
+            config["parallelism"] = f"replicas x{world} (distributed run failed: {type(exc).__name__}: {exc})"[:300]
+            ctx.close()  # the exported store cannot be reused: a fresh one for the replicas
+            ctx = _native.Context(n, nb, local, batch=batch)
+            ctx.set_stream(stream.cuda_stream)
     plan = mg.plan if mg is not None else _native.Plan(ctx, table, t, bars)
     if plan.rc != 0:
         raise RuntimeError(plan.msg)
