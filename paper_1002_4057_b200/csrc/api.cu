@@ -629,6 +629,7 @@ struct tinv_plan {
   std::vector<uint8_t> rename_parity;  // per matrix tile: odd number of renaming writers (final slot = alt)
   int32_t *d_depart_group = nullptr, *d_depart_count = nullptr;
   int32_t *d_depart_seq = nullptr;  // observed completion order of the departures ([T] = counter)
+  int32_t *d_recv_gate = nullptr, *d_gate_flag = nullptr;  // streamed arrivals: entry -> copy run, run flags
   int32_t *d_recv_task = nullptr, *d_inbox = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<unsigned long long> h_ts, h_te;
@@ -794,7 +795,7 @@ int tinv_plan_destroy(tinv_plan* p) {
   void* ptrs[] = {p->d_tasks, p->d_succ, p->d_indeg, p->d_done, p->d_cur,      p->d_alt,       p->d_queue, p->d_head,
                   p->d_tail,  p->d_ctr,  p->d_err,   p->d_progress, p->d_ts, p->d_te, p->d_tsm, p->d_snap_from,
                   p->d_snap_to, p->d_phase, p->d_recv_task, p->d_inbox, p->d_depart_group, p->d_depart_count,
-                  p->d_depart_seq};
+                  p->d_depart_seq, p->d_recv_gate, p->d_gate_flag};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->ev0) cudaEventDestroy(p->ev0);
@@ -1156,7 +1157,8 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
     }
   }
   if (sio && (ckm((void**)&p->d_depart_group, T * 4) || ckm((void**)&p->d_depart_count, T * 4) ||
-              ckm((void**)&p->d_depart_seq, (T + 1) * 4))) {
+              ckm((void**)&p->d_depart_seq, (T + 1) * 4) || ckm((void**)&p->d_recv_gate, nrecv * 4) ||
+              ckm((void**)&p->d_gate_flag, nrecv * 4))) {
     tinv_plan_destroy(p);
     return fail(c, TINV_ERR_CUDA, "departure counters allocation failed");
   }
@@ -1257,14 +1259,47 @@ struct HostIO {
   int64_t ldx;
   int mode;
 };
-constexpr int kDepartStreams = 8;
+// device -> host copy streams of a streamed run. Few: CUDA multiplexes streams
+// onto a limited set of hardware connections (CUDA_DEVICE_MAX_CONNECTIONS,
+// default 8), and a stream blocked in cuStreamWaitValue32 must not share one
+// with the arrival copies or the executor (TINV_DEPART_STREAMS overrides, <= 8)
+constexpr int kMaxDepartStreams = 8;
+static int depart_streams() {
+  const char* e = getenv("TINV_DEPART_STREAMS");
+  const int v = e ? atoi(e) : 4;
+  return v < 1 ? 1 : (v > kMaxDepartStreams ? kMaxDepartStreams : v);
+}
 
 typedef CUresult (*PFN_batchMemOp)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
 
 // Copy engines: A's lower tiles into their slots in inbox order, each followed
 // by its arrival flag (a stream write-value, ordered after the copy). Runs of
 // tiles contiguous on both sides (batched t = 1 stores) move as one copy.
-static int enqueue_arrivals(tinv_ctx* c, tinv_plan* p, const HostIO& io, int32_t* inbox, cudaStream_t st) {
+// Arrival copy runs (inbox order): runs of tiles contiguous on both sides
+// (batched t = 1 stores) move as one copy. Each run is gated by ONE flag
+// (gate_flag[run]): a flag write per tile costs the copy engine about half of
+// its H2D rate (measured, tools/copy_probe.py).
+static void arrival_runs(tinv_ctx* c, tinv_plan* p, const HostIO& io, std::vector<int32_t>& run_first,
+                         std::vector<int32_t>& gate) {
+  const int64_t na = (int64_t)p->arrive_tile.size(), n = c->n, T1 = c->T1;
+  run_first.clear();
+  gate.assign(std::max<int64_t>(na, 1), 0);
+  for (int64_t s0 = 0; s0 < na;) {
+    const int32_t o = p->arrive_tile[s0];
+    int64_t run = 1;
+    if (T1 == 1 && c->b == c->bp && io.lda == n)
+      while (s0 + run < na && run < 64 && p->arrive_tile[s0 + run] == o + run &&
+             c->a_slot[o + run] == c->a_slot[o] + run)
+        ++run;
+    for (int64_t r = 0; r < run; ++r) gate[s0 + r] = (int32_t)run_first.size();
+    run_first.push_back((int32_t)s0);
+    s0 += run;
+  }
+  run_first.push_back((int32_t)na);
+}
+
+static int enqueue_arrivals(tinv_ctx* c, tinv_plan* p, const HostIO& io, const std::vector<int32_t>& run_first,
+                            int32_t* gate_flag, cudaStream_t st) {
   static PFN_batchMemOp batch_mem_op = nullptr;
   if (!batch_mem_op) {
     void* fn = nullptr;
@@ -1273,10 +1308,10 @@ static int enqueue_arrivals(tinv_ctx* c, tinv_plan* p, const HostIO& io, int32_t
     if (!fn || q != cudaDriverEntryPointSuccess) return fail(c, TINV_ERR_CUDA, "cuStreamBatchMemOp unavailable");
     batch_mem_op = (PFN_batchMemOp)fn;
   }
-  const int64_t na = (int64_t)p->arrive_tile.size(), b = c->b, bp = c->bp, n = c->n, T1 = c->T1;
+  const int64_t b = c->b, bp = c->bp, n = c->n, T1 = c->T1;
   const size_t tile_bytes = (size_t)c->slot_elems * 8;
-  std::vector<CUstreamBatchMemOpParams> ops;
-  for (int64_t s0 = 0; s0 < na;) {
+  for (size_t g = 0; g + 1 < run_first.size(); ++g) {
+    const int64_t s0 = run_first[g], run = run_first[g + 1] - s0;
     const int32_t o = p->arrive_tile[s0];
     const int64_t m = o / T1, k = o % T1;
     int64_t i = (int64_t)((std::sqrt(8.0 * (double)k + 1.0) - 1.0) * 0.5);
@@ -1285,25 +1320,17 @@ static int enqueue_arrivals(tinv_ctx* c, tinv_plan* p, const HostIO& io, int32_t
     const int64_t j = k - i * (i + 1) / 2;
     double* dst = c->pool + (int64_t)c->a_slot[o] * c->slot_elems;
     const double* src = io.a + m * n * io.lda + i * b * io.lda + j * b;
-    int64_t run = 1;
-    if (T1 == 1 && b == bp && io.lda == n)
-      while (s0 + run < na && run < 64 && p->arrive_tile[s0 + run] == o + run &&
-             c->a_slot[o + run] == c->a_slot[o] + run)
-        ++run;
     if (run > 1)
       CK(c, cudaMemcpyAsync(dst, src, tile_bytes * run, cudaMemcpyHostToDevice, st));
     else
       CK(c, cudaMemcpy2DAsync(dst, bp * 8, src, io.lda * 8, b * 8, b, cudaMemcpyHostToDevice, st));
-    ops.assign(run, CUstreamBatchMemOpParams{});
-    for (int64_t r = 0; r < run; ++r) {
-      ops[r].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
-      ops[r].writeValue.address = (CUdeviceptr)(inbox + s0 + r);
-      ops[r].writeValue.value = 1;
-      ops[r].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
-    }
-    const CUresult r = batch_mem_op((CUstream)st, (unsigned)run, ops.data(), 0);
+    CUstreamBatchMemOpParams op{};
+    op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+    op.writeValue.address = (CUdeviceptr)(gate_flag + g);
+    op.writeValue.value = 1;
+    op.writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+    const CUresult r = batch_mem_op((CUstream)st, 1u, &op, 0);
     if (r != CUDA_SUCCESS) return fail(c, TINV_ERR_CUDA, "arrival flag write failed (CUresult " + std::to_string(r) + ")");
-    s0 += run;
   }
   return TINV_OK;
 }
@@ -1311,7 +1338,7 @@ static int enqueue_arrivals(tinv_ctx* c, tinv_plan* p, const HostIO& io, int32_t
 typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 
 // Copy engines, device -> host: for each copy group (departure order, spread
-// over kDepartStreams streams) wait until all its tiles departed, then move
+// over depart_streams() streams) wait until all its tiles departed, then move
 // them: LOWER: the tile's final slot (renaming parity decides cur or alt) to
 // block (i, j); SYMMETRIZE: off-diagonal tiles also their staged transpose to
 // block (j, i), diagonal tiles their staged mirrored form.
@@ -1325,7 +1352,8 @@ static int enqueue_departures(tinv_ctx* c, tinv_plan* p, const HostIO& io, const
     if (!fn || q != cudaDriverEntryPointSuccess) return fail(c, TINV_ERR_CUDA, "cuStreamWaitValue32 unavailable");
     wait_value = (PFN_waitValue32)fn;
   }
-  for (int k = 0; k < kDepartStreams; ++k) {
+  const int nds = depart_streams();
+  for (int k = 0; k < nds; ++k) {
     if (!c->dst[k]) CK(c, cudaStreamCreateWithFlags(&c->dst[k], cudaStreamNonBlocking));
     CK(c, cudaStreamWaitEvent(c->dst[k], after, 0));
   }
@@ -1333,7 +1361,7 @@ static int enqueue_departures(tinv_ctx* c, tinv_plan* p, const HostIO& io, const
   const bool sym = io.mode == TINV_DENSE_SYMMETRIZE;
   double* X = io.xhost;
   for (size_t g = 0; g < gfirst.size(); ++g) {
-    cudaStream_t s = c->dst[g % kDepartStreams];
+    cudaStream_t s = c->dst[g % nds];
     if (wait_value((CUstream)s, (CUdeviceptr)(p->d_depart_count + g), (cuuint32_t)gsize[g], CU_STREAM_WAIT_VALUE_GEQ) !=
         CUDA_SUCCESS)
       return fail(c, TINV_ERR_CUDA, "departure wait failed");
@@ -1472,7 +1500,13 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
     P.peer_inbox[r] = c->peer_inbox[r] ? c->peer_inbox[r] : P.inbox;
   }
   std::vector<int32_t> grp_first, grp_size;  // copy groups of departing tiles (in departure order)
+  std::vector<int32_t> run_first, gate;       // arrival copy runs and entry -> run
   if (io) {
+    arrival_runs(c, p, *io, run_first, gate);
+    CK(c, cudaMemcpyAsync(p->d_recv_gate, gate.data(), gate.size() * 4, cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemsetAsync(p->d_gate_flag, 0, gate.size() * 4, st));
+    P.recv_gate = p->d_recv_gate;
+    P.gate_flag = p->d_gate_flag;
     P.depart_mode = io->mode;
     P.stage_base = (int32_t)backup_base;  // staging tiles (SYMMETRIZE) use the snapshot region
     // groups: runs of consecutive staged diagonal tiles that are contiguous in
@@ -1519,7 +1553,7 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
     CK(c, cudaMemsetAsync(p->d_depart_count, 0x7f, T * 4, st));
   if (io) {  // copy engines, after the state reset above (ev0), concurrent with the executor
     CK(c, cudaStreamWaitEvent(c->st2, p->ev0, 0));
-    int rc2 = enqueue_arrivals(c, p, *io, P.inbox, c->st2);
+    int rc2 = enqueue_arrivals(c, p, *io, run_first, p->d_gate_flag, c->st2);
     if (!rc2) rc2 = enqueue_departures(c, p, *io, grp_first, grp_size, backup_base, p->ev0);
     if (rc2) {
       cudaStreamSynchronize(st);
@@ -1530,7 +1564,8 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
   CK(c, cudaStreamSynchronize(st));
   if (io) {
     CK(c, cudaStreamSynchronize(c->st2));
-    for (int k = 0; k < kDepartStreams; ++k) CK(c, cudaStreamSynchronize(c->dst[k]));
+    for (int k = 0; k < kMaxDepartStreams; ++k)
+      if (c->dst[k]) CK(c, cudaStreamSynchronize(c->dst[k]));
   }
   if (ms) {
     float f = 0.f;
@@ -1551,17 +1586,20 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
   }
   if (p->d_ts && io && getenv("TINV_DEPART_PROFILE")) {  // when do result tiles become final?
     unsigned long long t0 = ~0ull, t1 = 0;
-    std::vector<unsigned long long> de;
+    std::vector<unsigned long long> de, ar;
     for (int64_t u = 0; u < nx; ++u) {
       if (p->h_ts[u] != ~0ull) t0 = std::min(t0, p->h_ts[u]);
       t1 = std::max(t1, p->h_te[u]);
       if (p->tasks[u].kind == KIND_DEPART) de.push_back(p->h_te[u]);
+      if (p->tasks[u].kind == KIND_ARRIVE) ar.push_back(p->h_te[u]);
     }
-    std::sort(de.begin(), de.end());
-    fprintf(stderr, "[tinv depart] run %.1f ms; tiles final at (ms): ", (t1 - t0) * 1e-6);
-    for (double q : {0.1, 0.25, 0.5, 0.75, 0.9, 0.99, 1.0})
-      fprintf(stderr, "q%.2f %.1f ", q, (de[std::min(de.size() - 1, (size_t)(q * de.size()))] - t0) * 1e-6);
-    fprintf(stderr, "\n");
+    for (auto* v : {&ar, &de}) {
+      std::sort(v->begin(), v->end());
+      fprintf(stderr, "[tinv %s] run %.1f ms; tiles at (ms): ", v == &ar ? "arrive" : "depart", (t1 - t0) * 1e-6);
+      for (double q : {0.1, 0.25, 0.5, 0.75, 0.9, 0.99, 1.0})
+        fprintf(stderr, "q%.2f %.1f ", q, ((*v)[std::min(v->size() - 1, (size_t)(q * v->size()))] - t0) * 1e-6);
+      fprintf(stderr, "\n");
+    }
   }
   if (p->d_phase) {
     std::vector<unsigned long long> ph((size_t)c->nsm * NPHASE);

@@ -1471,25 +1471,31 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       return;
     }
     if (warp == NCONS_WARPS + 2) {
-      // ============================ inbox poller (one per launch): completes RECV tasks
-      if (blockIdx.x != 0 || P.nrecv == 0) return;
-      // Entries below `lo` are all consumed. Flags mostly arrive in inbox
+      // ============================ inbox pollers (warp 10 of every CTA): complete
+      // external tasks (RECV, ARRIVE). CTA b owns inbox entries b, b + G, ...:
+      // completions (successor pushes) proceed on all SMs in parallel.
+      const int G = gridDim.x, bid = blockIdx.x;
+      const int nloc = bid < P.nrecv ? (P.nrecv - bid + G - 1) / G : 0;
+      if (nloc == 0) return;
+      // Local entries below `lo` are all consumed. Flags mostly arrive in inbox
       // order (ARRIVE: copy order; RECV: send order), so each round scans a
-      // window of PWIN entries from `lo` with all loads in flight at once, and
-      // every 64th idle round scans everything beyond it.
+      // window of PWIN local entries from `lo` with all loads in flight at
+      // once, and every 64th idle round scans everything beyond it.
       constexpr int PW = 8, PWIN = PW * 32;
       int lo = 0;
       for (unsigned round = 0;; ++round) {
         if (ld_relaxed_s32(P.abort_flag) || ld_relaxed_s32(P.remaining) <= 0) break;
         bool any = false;
         const bool full = (round & 63) == 63;
-        for (int base = lo; base < (full ? P.nrecv : min(P.nrecv, lo + PWIN)); base += PWIN) {
+        for (int base = lo; base < (full ? nloc : min(nloc, lo + PWIN)); base += PWIN) {
           int fl[PW], tk[PW];
 #pragma unroll
           for (int k = 0; k < PW; ++k) {
-            const int i = base + k * 32 + lane;
-            tk[k] = i < P.nrecv ? __ldg(P.recv_task + i) : -1;
+            const int j = base + k * 32 + lane, i = bid + G * j;
+            tk[k] = j < nloc ? __ldg(P.recv_task + i) : -1;
             fl[k] = (tk[k] >= 0) ? ld_relaxed_sys_s32(P.inbox + i) : 2;
+            if (P.recv_gate && fl[k] == 0)  // gated entry: arrived when its copy run's flag is set
+              fl[k] = ld_relaxed_sys_s32(P.gate_flag + __ldg(P.recv_gate + i));
           }
           bool lead = base == lo;  // consumed prefix of the window -> advance lo
 #pragma unroll
@@ -1497,7 +1503,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             unsigned m = __ballot_sync(FULL, fl[k] == 1);
             if (m) fence_acq_rel_sys();
             while (m) {
-              const int idx = base + k * 32 + __ffs(m) - 1;
+              const int idx = bid + G * (base + k * 32 + __ffs(m) - 1);
               m &= m - 1;
               if (lane == 0) P.inbox[idx] = 2;
               __syncwarp();

@@ -105,6 +105,8 @@ struct ExecParams {
   const int32_t* recv_task;        // inbox index -> exec task id (-1: not received here)
   int32_t nrecv;                   // inbox length
   int32_t recv_base;               // slot of receive sequence number 0 (same on every rank)
+  const int32_t* recv_gate;        // streamed arrivals: entry -> copy run (null: the entry's own inbox flag)
+  const int32_t* gate_flag;        // per copy run: 1 = arrived (stream write-value)
   // streamed host output (DEPART; the copy engines do the device -> host moves)
   int32_t depart_mode;             // TINV_DENSE_LOWER_TILES / TINV_DENSE_SYMMETRIZE
   int32_t stage_base;              // slot of the staging tile of matrix tile 0 (SYMMETRIZE)
