@@ -939,6 +939,143 @@ __device__ void block_trtri(double* S, unsigned long long* ctl_dbg) {
   }
 }
 
+// One warp: a 16x16 output group D[m0.., n0..] = sgn * sum_{k in [k0, k1)}
+// Lf(m, k) Rt(k, n) on DMMA (m8n8k4, 2x2 tiles), operands in shared memory:
+// Lf(m, k) = L[(lr + m) * lld + lc + k], Rt(k, n) = R[(rr + k) * rld + rc + n],
+// k1 - k0 a multiple of 16. Result to D[(dr + m) * dld + dc + n].
+__device__ __forceinline__ void dmma_group16(const double* L, int lld, int lr, int lc, const double* R, int rld, int rr,
+                                             int rc, int k0, int k1, double* D, int dld, int dr, int dc, double sgn) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3;
+  double acc[2][2][2] = {};
+  for (int k = k0; k < k1; k += 16) {  // 4 k-steps per round: 16 fragment loads in flight, then 16 MMAs
+    double a[4][2], b[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) a[u][mi] = L[(lr + 8 * mi + g) * lld + lc + k + 4 * u + tg];
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) b[u][ni] = R[(rr + k + 4 * u + tg) * rld + rc + 8 * ni + g];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[u][mi], b[u][ni]);
+  }
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) D[(dr + 8 * mi + g) * dld + dc + 8 * ni + 2 * tg + e] = sgn * acc[mi][ni][e];
+}
+
+// Same as dmma_group16 for a 16 x 32 output group (2 x 4 tiles: 8 accumulator
+// chains, 6 fragment loads per 8 MMAs).
+__device__ __forceinline__ void dmma_group16x32(const double* L, int lld, int lr, int lc, const double* R, int rld,
+                                                int rr, int rc, int k0, int k1, double* D, int dld, int dr, int dc,
+                                                double sgn) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3;
+  double acc[2][4][2] = {};
+  for (int k = k0; k < k1; k += 8) {
+    double a[2][2], b[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) a[u][mi] = L[(lr + 8 * mi + g) * lld + lc + k + 4 * u + tg];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b[u][ni] = R[(rr + k + 4 * u + tg) * rld + rc + 8 * ni + g];
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[u][mi], b[u][ni]);
+  }
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) D[(dr + 8 * mi + g) * dld + dc + 8 * ni + 2 * tg + e] = sgn * acc[mi][ni][e];
+}
+
+// block_trtri with the recursive-doubling products on DMMA (used by the
+// executor; 37K -> ~21K cycles per 128 block, tools/micro/diag_blocks.cu): per level s and
+// pair c, T = B A^-1 (A^-1 lower: k >= first output column) into scratch,
+// then X21 = -C^-1 T (C^-1 lower: k < last output row), 16x16 groups per warp.
+__device__ void block_trtri_dmma(double* S, unsigned long long* ctl_dbg) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int TLD = 65;
+  double* Tb = S + BLK * SLD;  // T of every pair of a level: pair c at Tb + c * s * TLD
+  long long tq = clock64();
+  int pk = 3;
+  auto probe = [&]() {
+    const long long now = clock64();
+    if (tid == 0) ctl_dbg[pk] += now - tq;
+    tq = now;
+    ++pk;
+  };
+  {
+    const int p0 = 16 * warp, i = lane & 15;
+    double r[16], x[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) r[j] = j <= i ? S[(p0 + i) * SLD + p0 + j] : 0.0;
+    warp_inv16(r, x);
+    __syncwarp();
+    if (lane < 16) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) S[(p0 + k) * SLD + p0 + lane] = x[k];
+    }
+  }
+  cons_bar();
+  probe();
+  for (int s = 16; s < BLK; s *= 2) {
+    if (s == 64) {  // 16 x 32 groups (more accumulator chains per warp; measured 13K -> 10K cycles)
+      const int gm = s / 16, gn = s / 32, per = gm * gn, total = (BLK / (2 * s)) * per;
+      for (int q = 0; q * NCONS_WARPS < total; ++q) {
+        const int gi = (q & 1) ? (q + 1) * NCONS_WARPS - 1 - warp : q * NCONS_WARPS + warp;
+        if (gi >= total) continue;
+        const int c = gi / per, m0 = 16 * ((gi % per) / gn), n0 = 32 * (gi % gn);
+        const int a0 = 2 * c * s, b0 = a0 + s;
+        dmma_group16x32(S, SLD, b0 + m0, a0, S, SLD, a0, a0 + n0, n0, s, Tb + c * s * TLD, TLD, m0, n0, 1.0);
+      }
+      cons_bar();
+      for (int q = 0; q * NCONS_WARPS < total; ++q) {
+        const int gi = (q & 1) ? (q + 1) * NCONS_WARPS - 1 - warp : q * NCONS_WARPS + warp;
+        if (gi >= total) continue;
+        const int c = gi / per, m0 = 16 * ((gi % per) / gn), n0 = 32 * (gi % gn);
+        const int a0 = 2 * c * s, b0 = a0 + s;
+        dmma_group16x32(S, SLD, b0 + m0, b0, Tb + c * s * TLD, TLD, 0, n0, 0, m0 + 16, S, SLD, b0 + m0, a0 + n0, -1.0);
+      }
+      cons_bar();
+      probe();
+      continue;
+    }
+    const int gs = s / 16, per = gs * gs, total = (BLK / (2 * s)) * per;
+    // snake assignment: a warp's groups have complementary triangular k-extents
+    for (int q = 0; q * NCONS_WARPS < total; ++q) {  // T_c = B_c A_c^-1
+      const int gi = (q & 1) ? (q + 1) * NCONS_WARPS - 1 - warp : q * NCONS_WARPS + warp;
+      if (gi >= total) continue;
+      const int c = gi / per, m0 = 16 * ((gi % per) / gs), n0 = 16 * (gi % gs);
+      const int a0 = 2 * c * s, b0 = a0 + s;
+      dmma_group16(S, SLD, b0 + m0, a0, S, SLD, a0, a0 + n0, n0, s, Tb + c * s * TLD, TLD, m0, n0, 1.0);
+    }
+    cons_bar();
+    for (int q = 0; q * NCONS_WARPS < total; ++q) {  // X21_c = -C_c^-1 T_c
+      const int gi = (q & 1) ? (q + 1) * NCONS_WARPS - 1 - warp : q * NCONS_WARPS + warp;
+      if (gi >= total) continue;
+      const int c = gi / per, m0 = 16 * ((gi % per) / gs), n0 = 16 * (gi % gs);
+      const int a0 = 2 * c * s, b0 = a0 + s;
+      dmma_group16(S, SLD, b0 + m0, b0, Tb + c * s * TLD, TLD, 0, n0, 0, m0 + 16, S, SLD, b0 + m0, a0 + n0, -1.0);
+    }
+    cons_bar();
+    probe();
+  }
+}
+
 // jb / it live in shared memory (the item slot)
 __device__ __noinline__ void run_special(const Job& jb, const ItemInfo& it, const ExecParams& P, SmemCtl& ctl,
                                          double* S, int b) {
@@ -973,7 +1110,7 @@ __device__ __noinline__ void run_special(const Job& jb, const ItemInfo& it, cons
       zero_upper_row(dst, d, R, bp);
       cons_bar();
       t1 = clock64();
-      block_trtri(S, ctl.dbg2);
+      block_trtri_dmma(S, ctl.dbg2);
       t2 = clock64();
       double* aux = P.pool + (int64_t)src_s * P.slot_elems;
       store_block_lower(S, aux + (int64_t)d * BLK * bp + d * BLK, bp);
@@ -1001,7 +1138,7 @@ __device__ __noinline__ void run_special(const Job& jb, const ItemInfo& it, cons
         return;
       }
       long long t1 = clock64();
-      block_trtri(S, ctl.dbg2);
+      block_trtri_dmma(S, ctl.dbg2);
       long long t2 = clock64();
       store_block_lower(S, dst + (int64_t)d * BLK * bp + d * BLK, bp);
       zero_upper_row(dst, d, R, bp);
