@@ -579,6 +579,8 @@ int expected_reads(int kind) {
 
 double weight_of(int kind) {  // flops in units of b^3 (SURVEY.md §7 hard part 2)
   switch (kind) {
+    case KIND_POTRF_INV:
+      return 2.0 / 3.0;  // factor + the factor's inverse
     case TINV_POTRF:
     case TINV_TRTRI:
     case TINV_LAUUM:
@@ -934,14 +936,23 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
     // the factor's diagonal-block inverses computed by POTRF (its aux tile)
     auto potrf_aux = [&](int32_t tile) -> int32_t {
       const int32_t w = last_writer_exec[tile];
-      return (w >= 0 && xs[w].kind == TINV_POTRF) ? xs[w].in0 : -1;
+      return (w >= 0 && (xs[w].kind == TINV_POTRF || xs[w].kind == KIND_POTRF_INV)) ? xs[w].in0 : -1;
     };
-    if (kind == TINV_TRTRI) {  // TRTRI of an unchanged factor: reuse INV's inverse, or POTRF's diagonal blocks
-      const int64_t key = ((int64_t)o << 32) | (int64_t)(last_writer_exec[o] + 1);
-      auto it = inv_cache.find(key);
-      if (it != inv_cache.end()) {
+    auto full_inv_aux = [&](int32_t tile) -> int32_t {  // aux of a POTRF_INV (full inverse) or -1
+      const int32_t w = last_writer_exec[tile];
+      return (w >= 0 && xs[w].kind == KIND_POTRF_INV) ? xs[w].in0 : -1;
+    };
+    if (kind == TINV_TRTRI) {  // TRTRI of an unchanged factor: copy POTRF_INV's inverse, or reuse INV's,
+                               // or start from POTRF's diagonal-block inverses
+      int32_t src_inv = full_inv_aux(o);
+      if (src_inv < 0) {
+        const int64_t key = ((int64_t)o << 32) | (int64_t)(last_writer_exec[o] + 1);
+        auto it = inv_cache.find(key);
+        if (it != inv_cache.end()) src_inv = it->second;
+      }
+      if (src_inv >= 0) {
         last_writer_exec[o] = (int32_t)xs.size();
-        xs.push_back({TINV_COPY, TINV_STEP_COPY, o, it->second, -1, 1, (int)v, -1, -1, 0});
+        xs.push_back({TINV_COPY, TINV_STEP_COPY, o, src_inv, -1, 1, (int)v, -1, -1, 0});
         continue;
       }
       const int32_t pa = potrf_aux(o);
@@ -950,7 +961,11 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
         xflags = TF_DIAG_FROM_AUX;
       }
     }
-    if (kind == TINV_TRSM) {
+    if (kind == TINV_TRSM && potrf_aux(in0) >= 0) {
+      // multiply by the factor's inverse, kept whole by the POTRF (no INV task on the critical path)
+      xs[last_writer_exec[in0]].kind = KIND_POTRF_INV;
+      in0 = potrf_aux(in0);
+    } else if (kind == TINV_TRSM) {
       const int64_t key = ((int64_t)in0 << 32) | (int64_t)(last_writer_exec[in0] + 1);
       auto it = inv_cache.find(key);
       int32_t inv_t;
@@ -997,7 +1012,9 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
   {
     std::vector<std::vector<Acc>> acc(nx);
     for (int64_t v = 0; v < nx; ++v) {
-      if (xs[v].in0 >= 0 && xs[v].kind != TINV_POTRF) acc[v].push_back({xs[v].in0, 0});
+      const bool potrf = xs[v].kind == TINV_POTRF || xs[v].kind == KIND_POTRF_INV;
+      if (xs[v].in0 >= 0 && !potrf) acc[v].push_back({xs[v].in0, 0});
+      if (xs[v].in0 >= 0 && potrf) acc[v].push_back({xs[v].in0, 2});  // writes its aux
       if (xs[v].in1 >= 0) acc[v].push_back({xs[v].in1, 0});
       if (xs[v].out >= 0) acc[v].push_back({xs[v].out, xs[v].mode});
     }

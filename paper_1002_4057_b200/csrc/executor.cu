@@ -181,12 +181,12 @@ __device__ __forceinline__ void lower_pair(int i, int& r, int& c) {
 
 // jobs of one item of phase p: two for the off-diagonal items of TRTRI / INV
 // phases >= 1, one otherwise
-__device__ __forceinline__ int phase_jobs(int kind, int p) {
-  return ((kind == TINV_TRTRI || kind == KIND_INV) && p > 0) ? 2 : 1;
+__device__ __forceinline__ int phase_jobs(int kind, int p, int R) {
+  return (((kind == TINV_TRTRI || kind == KIND_INV) && p > 0) || (kind == KIND_POTRF_INV && p >= 3 * R - 2)) ? 2 : 1;
 }
-__device__ __forceinline__ int job_count(const ItemInfo& it) {
+__device__ __forceinline__ int job_count(const ItemInfo& it, int R) {
   int n = 0;
-  for (int p = it.ph0; p < it.ph0 + it.nph; ++p) n += phase_jobs(it.kind, p);
+  for (int p = it.ph0; p < it.ph0 + it.nph; ++p) n += phase_jobs(it.kind, p, R);
   return n;
 }
 
@@ -229,7 +229,19 @@ __device__ __forceinline__ void special_job(Job& j, int8_t sp, int d, int src, i
 __device__ __forceinline__ void get_job_phase(const ItemInfo& it, int n, int R, Job& j) {
   const int o = it.out_s, a = it.alt_s, x = it.in0_s, y = it.in1_s;
   const int kind = it.kind;
-  if (kind == TINV_POTRF) {  // in place on o; inverses of the diagonal blocks kept in aux tile x
+  if (kind == KIND_POTRF_INV && it.phase >= 3 * R - 2) {  // X = L^-1 into aux x: X[r][r-s] (TRTRI phase s)
+    const int s = it.phase - (3 * R - 2) + 1, r = s + it.item, d = r - s;
+    if (n == 0) {  // X[r][d] <- sum_{k=d+1..r} X[r][k] L[k][d]
+      gemm_job(j, V_NN, x, r, d + 1, o, d, d + 1, d + 1, r + 1, x, r, d, -1, 1);
+      j.a_mask = r;
+    } else {  // X[r][d] <- -X[r][d] X[d][d]
+      gemm_job(j, V_NN, x, r, d, x, d, d, d, d + 1, x, r, d, -1, -1);
+      j.b_mask = d;
+      j.dep = 1;
+    }
+    return;
+  }
+  if (kind == TINV_POTRF || kind == KIND_POTRF_INV) {  // in place on o; inverse diagonal blocks -> aux x
     const int d = it.phase / 3;
     switch (it.phase % 3) {
       case 0:
@@ -349,7 +361,7 @@ __device__ __forceinline__ void get_job(const ItemInfo& it, int n, int R, Job& j
   }
   ItemInfo sub = it;
   for (int p = it.ph0; p < it.ph0 + it.nph; ++p) {
-    const int nj = phase_jobs(it.kind, p);
+    const int nj = phase_jobs(it.kind, p, R);
     if (n < nj) {
       sub.phase = p;
       sub.item = 0;
@@ -1114,6 +1126,7 @@ __device__ __noinline__ void run_special(const Job& jb, const ItemInfo& it, cons
       t2 = clock64();
       double* aux = P.pool + (int64_t)src_s * P.slot_elems;
       store_block_lower(S, aux + (int64_t)d * BLK * bp + d * BLK, bp);
+      if (it.kind == KIND_POTRF_INV) zero_upper_row(aux, d, R, bp);  // aux becomes the full lower L^-1
       cons_bar();
       if (threadIdx.x == 0) {
         ctl.dbg[3] += t1 - t0 + clock64() - t2;
@@ -1445,7 +1458,7 @@ __device__ __forceinline__ unsigned long long produce_item(unsigned long long e,
     it.scr_s = P.scratch_base + blockIdx.x;
     it.aux0 = t.aux0;
     it.aux1 = t.aux1;
-    it.njobs = job_count(it);
+    it.njobs = job_count(it, R);
     for (int jn = 0; jn < it.njobs && jn < MAXJ; ++jn) get_job(it, jn, R, ctl.jobs[slot][jn]);
     fence_proxy_async();  // tiles written by other SMs (generic proxy) -> TMA reads
     mbar_arrive(&ctl.item_full[slot]);

@@ -45,6 +45,9 @@ constexpr int MAX_RANKS = 8;
 // wait on before moving the tile to the host.
 constexpr int KIND_ARRIVE = 14;
 constexpr int KIND_DEPART = 15;
+// POTRF whose aux tile receives the factor's full inverse (planner upgrade of
+// a POTRF whose factor a TRSM reads: TRSM multiplies by the aux directly).
+constexpr int KIND_POTRF_INV = 16;
 
 enum TaskFlags : int32_t {
   TF_RENAMED = 1,   // output written to the alternate slot, slots swapped at completion
@@ -129,20 +132,28 @@ inline int64_t tri_index(int64_t i, int64_t j) { return i * (i + 1) / 2 + j; }
 
 // Phases of a task over tiles of R x R blocks (128 x 128).
 //  POTRF (3R-2 phases): d = p/3; p%3 == 0: factor + invert diagonal block d
-//    (1 item); 1: block TRSMs A[r][d] <- A[r][d] inv(L_dd)^T, r > d (R-1-d);
-//    2: trailing block updates A[r][c] -= A[r][d] A[c][d]^T, r >= c > d.
+//    (1 item; the inverse block goes to the aux tile); 1: block TRSMs A[r][d]
+//    <- A[r][d] inv(L_dd)^T, r > d (R-1-d); 2: trailing block updates
+//    A[r][c] -= A[r][d] A[c][d]^T, r >= c > d.
+//  POTRF_INV (4R-3 phases): POTRF's, then s = p-(3R-2)+1 = 1..R-1: the
+//    off-diagonal blocks X[r][r-s] of X = L^-1 in the aux tile (R-s items,
+//    two block GEMMs each), so the aux holds the factor's full inverse (TRSM
+//    multiplies by it, TRTRI of the factor copies it).
 //  TRTRI / INV (R phases): 0: invert every diagonal block (R items);
 //    s >= 1: X[r][r-s] for r = s..R-1 (R-s items, two block GEMMs each).
 //  everything else: one phase.
 TINV_HD int phases_of(int kind, int R) {
   if (kind == KIND_SEND || kind == KIND_RECV || kind == KIND_ARRIVE) return 1;
   if (kind == TINV_POTRF) return 3 * R - 2;
+  if (kind == KIND_POTRF_INV) return 4 * R - 3;
   if (kind == TINV_TRTRI || kind == KIND_INV) return R;
   return 1;
 }
 TINV_HD int phase_items(int kind, int R, int p) {
   switch (kind) {
-    case TINV_POTRF: {
+    case TINV_POTRF:
+    case KIND_POTRF_INV: {
+      if (p >= 3 * R - 2) return R - (p - (3 * R - 2) + 1);  // inverse phases (POTRF_INV)
       const int d = p / 3, m = R - 1 - d;
       return p % 3 == 0 ? 1 : (p % 3 == 1 ? m : m * (m + 1) / 2);
     }
