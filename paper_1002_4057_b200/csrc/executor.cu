@@ -2,14 +2,17 @@
 // (B200 / sm_100a). Replaces the reference's threaded dynamic scheduler
 // (scheduler.py:261-351) and its numpy tile kernels (kernels.py:59-151).
 //
-// One CTA per SM, 288 threads:
+// One CTA per SM, 384 threads:
 //   warps 0-7  "consumers": FP64 DMMA (mma.sync m8n8k4 -> SASS DMMA.8x8x4)
-//              on 128x128 output blocks, epilogues, diagonal-block phases,
-//              and task completion (successor release) for the scheduler;
-//   warp 8     "producer": pops ready work items from the device queues,
-//              expands each into jobs and streams their operand chunks into a
-//              4-stage shared-memory ring with TMA (cp.async.bulk.tensor,
-//              128B swizzle) on mbarriers, running ahead across items.
+//              on 128x128 output blocks, epilogues staged for the storer,
+//              diagonal-block phases (128x128 factor / inverse in smem);
+//   warp 8     "producer": claims ready work items from the device queues,
+//              builds their jobs in the item's smem slot and streams operand
+//              chunks into a 4-stage shared-memory ring with TMA
+//              (cp.async.bulk.tensor, 128B swizzle) on mbarriers;
+//   warp 9     "storer": TMA stores / FP64 TMA reduce-adds of the staged
+//              epilogues, job completion, item completion (successor release);
+//   warp 10    inbox poller: completes external tasks (RECV, ARRIVE).
 // A task of kind K over tiles of order bp = R*128 is split into work items
 // (128x128 output blocks) which run on any CTA; the last item to finish
 // releases the task's successors in the hazard DAG (RAW/WAR/WAW edges built
@@ -866,91 +869,6 @@ __device__ int block_potrf(double* S, SmemCtl& ctl) {
   return f < (1 << 30) ? f : -1;
 }
 
-// In-place inverse of the lower-triangular 128x128 block in S by recursive
-// doubling: the eight 16x16 diagonal blocks (one warp each), then for
-// s = 16, 32, 64 every pair [[A,0],[B,C]] -> [[A^-1,0],[-C^-1 B A^-1, C^-1]]
-// (two micro-tiled products per level, all pairs of a level at once).
-// Strict upper part of S must be zero on entry.
-__device__ void block_trtri(double* S, unsigned long long* ctl_dbg) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  double* T = S + BLK * SLD;  // B A^-1 of every pair, 64 x 65 doubles per level
-  long long tq = clock64();
-  int pk = 3;
-  auto probe = [&]() {
-    const long long now = clock64();
-    if (tid == 0) ctl_dbg[pk] += now - tq;
-    tq = now;
-    ++pk;
-  };
-  {
-    const int p0 = 16 * warp, i = lane & 15;
-    double r[16], x[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) r[j] = j <= i ? S[(p0 + i) * SLD + p0 + j] : 0.0;
-    warp_inv16(r, x);
-    __syncwarp();
-    if (lane < 16) {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) S[(p0 + k) * SLD + p0 + lane] = x[k];
-    }
-  }
-  cons_bar();
-  probe();
-  for (int s = 16; s < BLK; s *= 2) {
-    const int per = (s / 4) * (s / 4), total = (BLK / (2 * s)) * per;
-    const int cs = s / 4;  // micro-tile columns c0 + cs*w (strided: conflict-free loads)
-    for (int tt = tid; tt < total; tt += 256) {  // T_c = B_c A_c^-1
-      const int c = tt / per, mt = tt % per;
-      const int tr = 4 * (mt / cs), c0 = mt % cs;
-      const int a0 = 2 * c * s, b0 = a0 + s;
-      double acc[4][4] = {};
-#pragma unroll 4
-      for (int k = c0; k < s; ++k) {  // A^-1 lower: rows k >= c0 only
-        double a[4], b[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          a[q] = S[(b0 + tr + q) * SLD + a0 + k];
-          b[q] = S[(a0 + k) * SLD + a0 + c0 + cs * q];
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int w = 0; w < 4; ++w) acc[q][w] += a[q] * b[w];
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int w = 0; w < 4; ++w) T[c * s * 65 + (tr + q) * 65 + c0 + cs * w] = acc[q][w];
-    }
-    cons_bar();
-    for (int tt = tid; tt < total; tt += 256) {  // X21_c = -C_c^-1 T_c
-      const int c = tt / per, mt = tt % per;
-      const int tr = 4 * (mt / cs), c0 = mt % cs;
-      const int a0 = 2 * c * s, b0 = a0 + s;
-      double acc[4][4] = {};
-#pragma unroll 4
-      for (int k = 0; k < tr + 4; ++k) {  // C^-1 lower: columns k <= row only
-        double a[4], b[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          a[q] = S[(b0 + tr + q) * SLD + b0 + k];
-          b[q] = T[c * s * 65 + k * 65 + c0 + cs * q];
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int w = 0; w < 4; ++w) acc[q][w] += a[q] * b[w];
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int w = 0; w < 4; ++w) S[(b0 + tr + q) * SLD + a0 + c0 + cs * w] = -acc[q][w];
-    }
-    cons_bar();
-    probe();
-  }
-}
-
 // One warp: a 16x16 output group D[m0.., n0..] = sgn * sum_{k in [k0, k1)}
 // Lf(m, k) Rt(k, n) on DMMA (m8n8k4, 2x2 tiles), operands in shared memory:
 // Lf(m, k) = L[(lr + m) * lld + lc + k], Rt(k, n) = R[(rr + k) * rld + rc + n],
@@ -1014,8 +932,12 @@ __device__ __forceinline__ void dmma_group16x32(const double* L, int lld, int lr
       for (int e = 0; e < 2; ++e) D[(dr + 8 * mi + g) * dld + dc + 8 * ni + 2 * tg + e] = sgn * acc[mi][ni][e];
 }
 
-// block_trtri with the recursive-doubling products on DMMA (used by the
-// executor; 37K -> ~21K cycles per 128 block, tools/micro/diag_blocks.cu): per level s and
+// In-place inverse of the lower-triangular 128x128 block in S by recursive
+// doubling: the eight 16x16 diagonal blocks (one warp each, warp shuffles),
+// then for s = 16, 32, 64 every pair [[A,0],[B,C]] -> [[A^-1,0],[-C^-1 B
+// A^-1, C^-1]] with the products on DMMA (~21K cycles per block vs 37K for
+// 4x4 FMA micro-tiles, tools/micro/diag_blocks.cu). Strict upper part of S
+// must be zero on entry. Per level s and
 // pair c, T = B A^-1 (A^-1 lower: k >= first output column) into scratch,
 // then X21 = -C^-1 T (C^-1 lower: k < last output row), 16x16 groups per warp.
 __device__ void block_trtri_dmma(double* S, unsigned long long* ctl_dbg) {

@@ -23,8 +23,6 @@ __global__ void __launch_bounds__(256, 1) bench(const double* A, double* out, lo
     const long long t0 = clock64();
     if (which == 0) {
       block_potrf(S, ctl);
-    } else if (which == 1) {
-      block_trtri(S, ctl.dbg2);
     } else {
       block_trtri_dmma(S, ctl.dbg2);
     }
@@ -84,7 +82,7 @@ int main() {
   cudaMemcpy(dL, L, n * n * 8, cudaMemcpyHostToDevice);
   const int smem = 128 * 129 * 8 + 64 * 65 * 8 * 2;
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int which = 0; which < 3; ++which) {
+  for (int which = 0; which < 2; ++which) {
     const double* in = which ? dL : dA;
     const double* ref = which ? X : L;
     bench<<<1, 256, smem>>>(in, out, cyc, dbg, 20, which);
@@ -98,7 +96,7 @@ int main() {
       mx = std::fmax(mx, std::fabs(ref[k]));
     }
     printf("%s: %lld cycles per 128x128 call (%s), max rel err %.2e; probes:",
-           which == 2 ? "block_trtri_dmma" : (which ? "block_trtri" : "block_potrf"),
+           which ? "block_trtri_dmma" : "block_potrf",
            *cyc, cudaGetErrorString(e), err / mx);
     for (int k = 0; k < 8; ++k) printf(" %llu", dbg[k]);
     printf("\n");
