@@ -127,6 +127,8 @@ def _run_host(a: np.ndarray, out, nb: int, batch: int, config: VariantConfig, de
     out = np.empty_like(a) if out is None else _host_buffer(out, "out")
     if out.shape != a.shape or out.dtype != np.float64 or not out.flags.c_contiguous:
         raise ValueError("out must be a C-contiguous float64 array shaped like a")
+    if np.shares_memory(a, out):  # result tiles stream out while input tiles still stream in
+        raise ValueError("out must not overlap a")
     t = n // nb
     pipelined = True if batch > 1 else config.pipelined
     key = (n, nb, batch, device, config.placement, config.loops, pipelined)

@@ -180,3 +180,15 @@ def test_batched_validation():
         P.invert_batched(np.zeros((2, 6, 6)), 4)
     with pytest.raises(ValueError):
         P.invert_batched(np.full((1, 2, 2), np.inf), 2)
+
+
+def test_invert_host_validation():
+    a = np.eye(8) * 2.0
+    with pytest.raises(ValueError):
+        P.invert_host(a, 4, out=a)  # in-place would race the streamed copies
+    with pytest.raises(ValueError):
+        P.invert_host(a, 4, out=np.empty((8, 8), dtype=np.float32))
+    with pytest.raises(P.InvalidSizeError):
+        P.invert_host(np.eye(6), 4)
+    with pytest.raises(P.InvalidSizeError):
+        P.invert_batched_host(np.eye(4), 2)
