@@ -203,6 +203,29 @@ int tinv_plan_trace(const tinv_plan* plan, int64_t* start_ns, int64_t* end_ns, i
 int tinv_run(tinv_ctx* ctx, const int32_t* table, int64_t ntasks, int32_t stream_t,
              const int64_t* barriers, int64_t nbar, uint32_t flags, tinv_err* err);
 
+/* ---- batched small inversions (BASELINE config 4), no context ----------
+ * For nb = n the reference runs gen_inversion(1) -- POTRF, TRTRI, LAUUM of
+ * one tile (taskgen.py:178-223; kernels.py:59-76, 120-130, 148-151) -- and
+ * then symmetrize_lower(to_dense(tm)) (tile_matrix.py:102-119), once per
+ * matrix. These entry points run that per-matrix sequence fused into one
+ * thread block per matrix (csrc/batched.cu), 1 <= n <= 256.
+ *
+ * tinv_batch_small_launch: device pointers; matrix k at dA + k * stride
+ * (row-major, ld = n; only its lower triangle is read), its full symmetric
+ * inverse to dX + k * stride (dX may equal dA). Asynchronous on cuda_stream
+ * (null = legacy default stream). *dfail is a device u64 the caller sets to
+ * all ones; it receives min over failing matrices of (k << 32 | column), the
+ * column being POTRF's NotPositiveDefiniteError index (kernels.py:68-71). */
+int tinv_batch_small_launch(const double* dA, double* dX, int64_t batch, int64_t n, int64_t stride,
+                            void* cuda_stream, unsigned long long* dfail);
+/* tinv_batch_small_host: host buffers (page-locked for overlap), blocking.
+ * The batch streams through the device in chunks: host -> device copy,
+ * kernel, device -> host copy on three streams, overlapped. On a failure
+ * returns TINV_ERR_NOT_SPD with *fail_matrix / *fail_index set (else -1);
+ * *ms (optional) = wall time of the device work. */
+int tinv_batch_small_host(const double* hA, double* hX, int64_t batch, int64_t n, int device,
+                          int64_t* fail_matrix, int64_t* fail_index, double* ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,9 @@ EXPORTS = (
     "tinv_put_tile", "tinv_get_tile", "tinv_gen_stream", "tinv_dag_edges", "tinv_dist_stream", "tinv_plan_create",
     "tinv_plan_create_xfer", "tinv_ipc_export", "tinv_ipc_open", "tinv_ipc_reset", "tinv_plan_exec",
     "tinv_plan_exec_host", "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
+    "tinv_batch_small_launch", "tinv_batch_small_host",
 )
+BATCH_SMALL_MAX_N = 256  # tinv_batch_small_*: 1 <= n <= 256
 
 
 class TinvErr(ctypes.Structure):
@@ -95,6 +97,9 @@ def lib():
         "tinv_plan_stats": ([_P, _I64P, _I64P, _I64P], ctypes.c_int),
         "tinv_plan_trace": ([_P, _I64P, _I64P, _I32P, _I64], ctypes.c_int),
         "tinv_run": ([_P, _I32P, _I64, _I32, _I64P, _I64, _U32, ctypes.POINTER(TinvErr)], ctypes.c_int),
+        "tinv_batch_small_launch": ([_P, _P, _I64, _I64, _I64, _P, _P], ctypes.c_int),
+        "tinv_batch_small_host": ([_P, _P, _I64, _I64, ctypes.c_int, _I64P, _I64P, ctypes.POINTER(ctypes.c_double)],
+                                  ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -130,6 +135,21 @@ def check(rc, ctx=None):
 
 def device_count():
     return lib().tinv_device_count()
+
+
+def batch_small_launch(a_ptr, x_ptr, batch, n, stride, stream_ptr, fail_ptr):
+    """Asynchronous fused batched inversion on device buffers (tinv_batch_small_launch)."""
+    check(lib().tinv_batch_small_launch(a_ptr, x_ptr, batch, n, stride, stream_ptr, fail_ptr))
+
+
+def batch_small_host(a_ptr, x_ptr, batch, n, device=0):
+    """Blocking fused batched inversion of host buffers; returns (rc, fail_matrix, fail_index, ms)."""
+    fm, fi, ms = ctypes.c_int64(-1), ctypes.c_int64(-1), ctypes.c_double(0.0)
+    rc = lib().tinv_batch_small_host(a_ptr, x_ptr, batch, n, device, ctypes.byref(fm), ctypes.byref(fi),
+                                     ctypes.byref(ms))
+    if rc not in (OK, ERR_NOT_SPD):
+        check(rc)
+    return rc, fm.value, fi.value, ms.value
 
 
 def gen_stream(t, steps_mask, loops, out_of_place, pipelined):

@@ -79,6 +79,13 @@ struct tinv_ctx {
     }                                                                                               \
   } while (0)
 
+namespace tinv {
+int set_error(int code, const std::string& msg) {  // error text for context-free entry points (batched.cu)
+  g_err = msg;
+  return code;
+}
+}  // namespace tinv
+
 static int fail(tinv_ctx* ctx, int code, const std::string& msg) {
   if (ctx) ctx->err = msg;
   g_err = msg;

@@ -1,0 +1,693 @@
+// Batched small SPD inversions (BASELINE config 4: 8192 independent n = 256
+// matrices), one thread block per matrix.
+//
+// With nb = n the reference's stream is gen_inversion(1) = POTRF -> TRTRI ->
+// LAUUM on a single tile (taskgen.py:178-223 at t = 1; kernels.py:59-76,
+// 120-130, 148-151). Running that through the DAG executor spends most of the
+// time in queue round trips and in 128x128 diagonal chains that hold a whole
+// SM. Here the three steps of one matrix are fused into one CTA that walks a
+// fixed program of 64x64 block operations:
+//
+//   step 1 (POTRF, right-looking over 64-wide panels p):
+//     DIAG p      L_pp = chol(A_pp), Linv_pp = L_pp^-1     (smem, warp chains)
+//     TRSM i>p    L_ip = A_ip Linv_pp^T                    (DMMA, triangular K)
+//     UPD  i>=j>p A_ij -= L_ip L_jp^T                      (DMMA)
+//   step 2 (TRTRI, column j, row i > j):
+//     T = sum_{k=j}^{i-1} L_ik X_kj ;  X_ij = -X_ii T      (X_jj = Linv_jj from DIAG)
+//   step 3 (LAUUM, row i, column j <= i):
+//     W_ij = sum_{k>=i} X_ki^T X_kj, written with its mirror (full symmetric
+//     output = symmetrize_lower(to_dense(...)), tile_matrix.py:102-119)
+//
+// The matrix itself is the working store (X's lower blocks, L2-resident while
+// the CTA works on it). Operand blocks are staged in three 32 KB shared-memory
+// buffers managed as a tiny write-through block cache: the operands of the
+// next operation are prefetched with cp.async while the current one runs,
+// results a later operation reads are inserted as they are stored. Two CTAs
+// share an SM (~106 KB smem each), so one matrix's latency-bound diagonal
+// chain overlaps the other's DMMA work.
+//
+// Products run on the FP64 tensor pipe (mma.sync m8n8k4 -> DMMA.8x8x4; there
+// is no f64 tcgen05 kind on sm_100a). Smem blocks are 64x64 row-major with an
+// XOR swizzle (column ^ 4 * (row & 3)) that makes every m8n8k4 fragment load
+// -- row- or column-oriented -- hit 16 distinct 8-byte bank pairs per half warp.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <chrono>
+#include <string>
+
+#include "tinv_internal.h"
+
+namespace tinv {
+int set_error(int code, const std::string& msg);
+
+namespace bsm {
+
+constexpr int BB = 64;            // block order
+constexpr int NT = 256;           // 8 warps
+constexpr int NBMAX = 4;          // n <= 256
+constexpr int MAXOPS = 64;        // program length for nbk = 4 is 56
+constexpr int BUFD = BB * BB;     // doubles per smem block buffer
+constexpr int NBUF = 3;
+constexpr int TLD = 36;           // row stride of the 32x32 TRTRI scratch
+constexpr int SMEM_DYN = NBUF * BUFD * 8 + 32 * TLD * 8;
+constexpr unsigned FULL = 0xffffffffu;
+
+enum : int8_t { OP_DIAG = 1, OP_MMA = 2 };
+// per-warp K range of a triangular operand (the warp's output tile is rows
+// [32 wm, 32 wm + 32) x columns [16 wn, 16 wn + 16) of the 64x64 block)
+enum : int8_t { KR_FULL, KR_LT_COL, KR_LT_ROW, KR_GE_COL, KR_GE_ROW, KR_GE_BOTH };
+enum : int8_t { ST_NONE = 0, ST_FULL = 1, ST_LOWER = 2, ST_SYM = 3 };
+enum : int8_t { F_ZERO = 1, F_NEGC = 2, F_CACHE = 4, F_SKIPU = 8, F_TA = 16, F_TB = 32 };
+
+// One block operation; arrays: 0 = A (input), 1 = X (working store / output).
+struct BOp {
+  int8_t type, flags, kr, st;
+  int8_t aa, ai, aj, ba;
+  int8_t bi, bj, ca, ci;
+  int8_t cj, oi, oj, sg;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ int sw(int r, int c) { return r * BB + (c ^ ((r & 3) << 2)); }
+__device__ __forceinline__ void cp16(double* dst, const double* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------- program
+__device__ int gen_program(BOp* ops, int nb) {
+  int k = 0;
+  auto mma = [&](int aa, int ai, int aj, int ba, int bi, int bj, int flags, int kr, int st, int oi, int oj, int sg,
+                 int ca = 0, int ci = 0, int cj = 0) {
+    BOp o;
+    o.type = OP_MMA;
+    o.flags = (int8_t)flags;
+    o.kr = (int8_t)kr;
+    o.st = (int8_t)st;
+    o.aa = (int8_t)aa, o.ai = (int8_t)ai, o.aj = (int8_t)aj;
+    o.ba = (int8_t)ba, o.bi = (int8_t)bi, o.bj = (int8_t)bj;
+    o.ca = (int8_t)ca, o.ci = (int8_t)ci, o.cj = (int8_t)cj;
+    o.oi = (int8_t)oi, o.oj = (int8_t)oj, o.sg = (int8_t)sg;
+    ops[k++] = o;
+  };
+  // step 1: Cholesky (POTRF), right-looking over 64-wide panels
+  for (int p = 0; p < nb; ++p) {
+    const int src = p ? 1 : 0;
+    BOp d = {};
+    d.type = OP_DIAG;
+    d.aa = (int8_t)src, d.ai = (int8_t)p, d.aj = (int8_t)p, d.oi = (int8_t)p, d.oj = (int8_t)p;
+    ops[k++] = d;
+    for (int i = p + 1; i < nb; ++i)  // L_ip = A_ip Linv_pp^T
+      mma(src, i, p, 1, p, p, F_ZERO | F_CACHE | F_TB, KR_LT_COL, ST_FULL, i, p, 1);
+    for (int i = p + 1; i < nb; ++i)  // A_ij -= L_ip L_jp^T
+      for (int j = p + 1; j <= i; ++j)
+        mma(1, i, p, 1, j, p, F_NEGC | F_TB | (i == j ? F_SKIPU : 0), KR_FULL, i == j ? ST_LOWER : ST_FULL, i, j,
+            -1, src, i, j);
+  }
+  // step 2: X = L^-1 (TRTRI); X_jj = Linv_jj already in place
+  for (int j = 0; j + 1 < nb; ++j)
+    for (int i = j + 1; i < nb; ++i) {
+      for (int q = j; q < i; ++q)  // T = sum_q L_iq X_qj (X_jj lower: K >= column)
+        mma(1, i, q, 1, q, j, q == j ? F_ZERO : 0, q == j ? KR_GE_COL : KR_FULL, q == i - 1 ? ST_FULL : ST_NONE,
+            i, j, 1);
+      ops[k - 1].flags |= F_CACHE;
+      mma(1, i, i, 1, i, j, F_ZERO | F_CACHE, KR_LT_ROW, ST_FULL, i, j, -1);  // X_ij = -X_ii T
+    }
+  // step 3: A^-1 = X^T X (LAUUM), lower blocks with their mirrors
+  for (int i = 0; i < nb; ++i)
+    for (int j = 0; j <= i; ++j)
+      for (int q = i; q < nb; ++q)
+        mma(1, q, i, 1, q, j, F_TA | (q == i ? F_ZERO : 0) | (i == j ? F_SKIPU : 0),
+            q == i ? (j == i ? KR_GE_BOTH : KR_GE_ROW) : KR_FULL, q == nb - 1 ? ST_SYM : ST_NONE, i, j, 1);
+  return k;
+}
+
+// ---------------------------------------------------------------- block I/O
+// global block (bi, bj) of an n x n row-major matrix -> swizzled smem buffer;
+// zero outside the matrix. One cp.async group per call.
+__device__ __forceinline__ void load_blk(double* S, const double* G, int n, int bi, int bj) {
+  const int r0 = bi * BB, c0 = bj * BB;
+  if ((n & 1) == 0) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = threadIdx.x + NT * u, r = idx >> 5, c = (idx & 31) * 2;
+      const bool ok = r0 + r < n && c0 + c < n;
+      cp16(S + sw(r, c), ok ? G + (int64_t)(r0 + r) * n + c0 + c : G, ok ? 16 : 0);
+    }
+  } else {
+    for (int e = threadIdx.x; e < BUFD; e += NT) {
+      const int r = e >> 6, c = e & 63;
+      S[sw(r, c)] = (r0 + r < n && c0 + c < n) ? G[(int64_t)(r0 + r) * n + c0 + c] : 0.0;
+    }
+  }
+  cp_commit();
+}
+
+// ---------------------------------------------------------------- DMMA block product
+// acc (warp tile rows 32 wm.., cols 16 wn..) += sum_{k0 <= k < k1} A(r, k) B(k, c);
+// A(r, k) = SA[r][k] (or SA[k][r] if TA), B(k, c) = SB[k][c] (or SB[c][k] if TB).
+// k0, k1 multiples of 16.
+template <bool TA, bool TB>
+__device__ __forceinline__ void mma_blk(const double* SA, const double* SB, int k0, int k1, double (&acc)[4][2][2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3, warp = threadIdx.x >> 5;
+  const int m0 = 32 * (warp & 1), n0 = 16 * (warp >> 1);
+  for (int k = k0; k < k1; k += 16) {
+    double a[4][4], b[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int kk = k + 4 * u + tg;
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[u][mi] = TA ? SA[sw(kk, m0 + 8 * mi + g)] : SA[sw(m0 + 8 * mi + g, kk)];
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) b[u][ni] = TB ? SB[sw(n0 + 8 * ni + g, kk)] : SB[sw(kk, n0 + 8 * ni + g)];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[u][mi], b[u][ni]);
+  }
+}
+
+// ---------------------------------------------------------------- diagonal block
+// Warp 0: factor the 16x16 diagonal sub-block at (p0, p0) in place (lane i & 15
+// holds row i; right-looking, shuffles); 1 / L[k][k] -> dinv[p0 + k]; the first
+// failing pivot (kernels.py:68-71: not d > 0, or d non-finite) -> *fail.
+__device__ __noinline__ void factor16(double* S, int p0, double* dinv, int* fail) {
+  const int lane = threadIdx.x & 31, i = lane & 15;
+  double r[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) r[j] = j <= i ? S[sw(p0 + i, p0 + j)] : 0.0;
+  unsigned bad = 0;
+  double myil = 1.0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const double piv = __shfl_sync(FULL, r[k], k);
+    const bool b = !(piv > 0.0) || !isfinite(piv);
+    bad |= b ? (1u << k) : 0u;
+    const double il = b ? 1.0 : rsqrt(piv);
+    myil = i == k ? il : myil;
+    r[k] = i == k ? (b ? 1.0 : piv * il) : (i > k ? r[k] * il : r[k]);
+#pragma unroll
+    for (int j = k + 1; j < 16; ++j) {
+      const double v = __shfl_sync(FULL, r[k], j);  // L[j][k]
+      r[j] = i >= j ? fma(-r[k], v, r[j]) : r[j];
+    }
+  }
+  if (lane == 0 && bad) atomicMin(fail, p0 + __ffs(bad) - 1);
+  if (lane < 16) {
+    dinv[p0 + i] = myil;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) S[sw(p0 + i, p0 + j)] = j <= i ? r[j] : 0.0;
+  }
+}
+
+// In-place Cholesky of the lower 64x64 block in S (16-wide panels): warp 0
+// factors the panel's diagonal sub-block, every thread row-solves the panel
+// below it, the trailing lower 8x8 tiles are updated on DMMA. The strict upper
+// part of S must be zero on entry; it is zero on exit.
+__device__ void factor64(double* S, double* dinv, int* fail) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
+  for (int P = 0; P < 4; ++P) {
+    const int p0 = 16 * P;
+    if (warp == 0) factor16(S, p0, dinv, fail);
+    __syncthreads();
+    if (P == 3) break;
+    // panel rows q >= p0 + 16: v L_PP^T = a, right-looking substitution
+    for (int q = p0 + 16 + tid; q < BB; q += NT) {
+      double v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = S[sw(q, p0 + k)];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        v[j] *= dinv[p0 + j];
+#pragma unroll
+        for (int jj = j + 1; jj < 16; ++jj) v[jj] = fma(-v[j], S[sw(p0 + jj, p0 + j)], v[jj]);
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) S[sw(q, p0 + k)] = v[k];
+    }
+    __syncthreads();
+    // trailing lower 8x8 tiles of rows / columns [p0 + 16, 64): -= L_P L_P^T
+    const int t0 = p0 + 16, nt8 = (BB - t0) / 8, ntiles = nt8 * (nt8 + 1) / 2;
+    for (int tt = warp; tt < ntiles; tt += NT / 32) {
+      int ti = 0, rem = tt;
+      while (rem > ti) {
+        rem -= ti + 1;
+        ++ti;
+      }
+      const int r0 = t0 + 8 * ti, c0 = t0 + 8 * rem;
+      double acc[2] = {S[sw(r0 + g, c0 + 2 * tg)], S[sw(r0 + g, c0 + 2 * tg + 1)]};
+#pragma unroll
+      for (int k = 0; k < 16; k += 4) dmma(acc, -S[sw(r0 + g, p0 + k + tg)], S[sw(c0 + g, p0 + k + tg)]);
+      S[sw(r0 + g, c0 + 2 * tg)] = acc[0];
+      S[sw(r0 + g, c0 + 2 * tg + 1)] = acc[1];
+    }
+    __syncthreads();
+  }
+}
+
+// One warp: 8x8 tile D[dr..][dc..] = sgn * sum_{k < K} A(ar + i, ac + k) B(br + k, bc + j).
+template <class FA, class FB, class FD>
+__device__ __forceinline__ void tile8(FA A, FB B, FD D, int K, double sgn) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3;
+  double acc[2] = {0.0, 0.0};
+  for (int k = 0; k < K; k += 4) dmma(acc, A(g, k + tg), B(k + tg, g));
+  D(g, 2 * tg, sgn * acc[0]);
+  D(g, 2 * tg + 1, sgn * acc[1]);
+}
+
+// X = L^-1 for the lower 64x64 L (strict upper zero, 1 / L[k][k] in dinv), by
+// recursive doubling: 16x16 diagonal inverses (warps 0-3, lane = column), then
+// for s = 16, 32: [[A, 0], [B, C]]^-1 = [[A^-1, 0], [-C^-1 B A^-1, C^-1]].
+__device__ void trtri64(const double* L, double* X, double* T, const double* dinv) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < BUFD; e += NT) X[e] = 0.0;
+  __syncthreads();
+  if (warp < 4) {
+    const int q0 = 16 * warp, jc = lane & 15;
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = i == jc ? 1.0 : 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      x[i] *= dinv[q0 + i];
+#pragma unroll
+      for (int ii = i + 1; ii < 16; ++ii) x[ii] = fma(-L[sw(q0 + ii, q0 + i)], x[i], x[ii]);
+    }
+    if (lane < 16) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) X[sw(q0 + i, q0 + jc)] = x[i];
+    }
+  }
+  __syncthreads();
+  // s = 16: pairs c = 0, 1 (a0 = 32 c, b0 = a0 + 16); 4 tiles each, one per warp
+  {
+    const int c = warp >> 2, ti = (warp >> 1) & 1, tj = warp & 1, a0 = 32 * c, b0 = a0 + 16;
+    const int r0 = 8 * ti, c0 = 8 * tj;
+    tile8([&](int i, int k) { return L[sw(b0 + r0 + i, a0 + k)]; },
+          [&](int k, int j) { return X[sw(a0 + k, a0 + c0 + j)]; },
+          [&](int i, int j, double v) { T[(16 * c + r0 + i) * TLD + c0 + j] = v; }, 16, 1.0);
+    __syncthreads();
+    tile8([&](int i, int k) { return X[sw(b0 + r0 + i, b0 + k)]; },
+          [&](int k, int j) { return T[(16 * c + k) * TLD + c0 + j]; },
+          [&](int i, int j, double v) { X[sw(b0 + r0 + i, a0 + c0 + j)] = v; }, 16, -1.0);
+    __syncthreads();
+  }
+  // s = 32: one pair (a0 = 0, b0 = 32); 16 tiles, two per warp
+  for (int tt = warp; tt < 16; tt += 8) {
+    const int r0 = 8 * (tt >> 2), c0 = 8 * (tt & 3);
+    tile8([&](int i, int k) { return L[sw(32 + r0 + i, k)]; }, [&](int k, int j) { return X[sw(k, c0 + j)]; },
+          [&](int i, int j, double v) { T[(r0 + i) * TLD + c0 + j] = v; }, 32, 1.0);
+  }
+  __syncthreads();
+  for (int tt = warp; tt < 16; tt += 8) {
+    const int r0 = 8 * (tt >> 2), c0 = 8 * (tt & 3);
+    tile8([&](int i, int k) { return X[sw(32 + r0 + i, 32 + k)]; }, [&](int k, int j) { return T[k * TLD + c0 + j]; },
+          [&](int i, int j, double v) { X[sw(32 + r0 + i, c0 + j)] = v; }, 32, -1.0);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- block cache (per-thread replicated state)
+struct Cache {
+  int tag[NBUF];
+  unsigned use[NBUF];
+  unsigned clk;
+  __device__ __forceinline__ int find(int t) const {
+    int f = -1;
+#pragma unroll
+    for (int b = 0; b < NBUF; ++b) f = (t && tag[b] == t) ? b : f;
+    return f;
+  }
+  // empty buffer first, else least recently used; -1 if all excluded
+  __device__ __forceinline__ int victim(unsigned excl) const {
+    int best = -1;
+    unsigned bu = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < NBUF; ++b) {
+      if (excl & (1u << b)) continue;
+      const unsigned u = tag[b] ? use[b] : 0u;
+      if (best < 0 || u < bu) best = b, bu = u;
+    }
+    return best;
+  }
+  __device__ __forceinline__ void set(int b, int t) {
+#pragma unroll
+    for (int q = 0; q < NBUF; ++q)
+      if (q == b) tag[q] = t, use[q] = ++clk;
+  }
+  __device__ __forceinline__ void touch(int b) {
+#pragma unroll
+    for (int q = 0; q < NBUF; ++q)
+      if (q == b) use[q] = ++clk;
+  }
+  __device__ __forceinline__ void drop_tag(int t) {
+#pragma unroll
+    for (int q = 0; q < NBUF; ++q)
+      if (tag[q] == t) tag[q] = 0;
+  }
+};
+__device__ __forceinline__ int tagof(int arr, int i, int j) { return 1 + ((arr << 8) | (i << 4) | j); }
+
+// ---------------------------------------------------------------- kernel
+__global__ void __launch_bounds__(NT, 2)
+    k_bsmall(const double* __restrict__ A, double* X, int n, int nb, int64_t mstride, unsigned long long* fail,
+             int64_t id0) {
+  extern __shared__ __align__(128) double dsm[];
+  __shared__ BOp ops[MAXOPS];
+  __shared__ double dinv[BB];
+  __shared__ int sfail, nops;
+  double* const scr = dsm + NBUF * BUFD;
+  const int64_t mat = blockIdx.x;
+  const double* const a = A + mat * mstride;
+  double* const x = X + mat * mstride;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1, m0 = 32 * wm, n0 = 16 * wn;
+  if (tid == 0) {
+    nops = gen_program(ops, nb);
+    sfail = 1 << 30;
+  }
+  __syncthreads();
+  const int nop = nops;
+  auto buf = [&](int b) { return dsm + b * BUFD; };
+  auto base = [&](int arr) -> const double* { return arr ? x : a; };
+  Cache cc;
+#pragma unroll
+  for (int b = 0; b < NBUF; ++b) cc.tag[b] = 0, cc.use[b] = 0;
+  cc.clk = 0;
+  double acc[4][2][2];
+
+  for (int o = 0; o < nop; ++o) {
+    const BOp op = ops[o];
+    // 1. operands not prefetched: load now (exposed). The barrier orders the
+    // previous operation's global stores and smem reads before the loads.
+    int ba = -1, bb = -1;
+    if (op.type == OP_DIAG) {
+      __syncthreads();
+      ba = cc.victim(0);
+      bb = cc.victim(1u << ba);
+      load_blk(buf(ba), base(op.aa), n, op.ai, op.aj);
+      cc.set(ba, 0);  // factored in place: not a copy of any global block
+    } else {
+      const int ta = tagof(op.aa, op.ai, op.aj), tb = tagof(op.ba, op.bi, op.bj);
+      ba = cc.find(ta);
+      bb = tb == ta ? ba : cc.find(tb);
+      if (ba < 0 || bb < 0) __syncthreads();
+      if (ba < 0) {
+        ba = cc.victim(bb >= 0 ? 1u << bb : 0u);
+        load_blk(buf(ba), base(op.aa), n, op.ai, op.aj);
+        cc.set(ba, ta);
+        if (tb == ta) bb = ba;
+      }
+      if (bb < 0) {
+        bb = cc.victim(1u << ba);
+        load_blk(buf(bb), base(op.ba), n, op.bi, op.bj);
+        cc.set(bb, tb);
+      }
+      cc.touch(ba);
+      cc.touch(bb);
+    }
+    cp_wait_all();
+    __syncthreads();
+    // 2. prefetch the next operation's operands into buffers this one does not use
+    unsigned next_mask = 0;
+    if (o + 1 < nop && ops[o + 1].type == OP_MMA) {
+      const BOp nx = ops[o + 1];
+      const int outt = (op.type == OP_DIAG || op.st != ST_NONE) ? tagof(1, op.oi, op.oj) : 0;
+      unsigned excl = (1u << ba) | (1u << bb);
+      const int t2[2] = {tagof(nx.aa, nx.ai, nx.aj), tagof(nx.ba, nx.bi, nx.bj)};
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int f = (t2[q] == outt) ? -1 : cc.find(t2[q]);
+        if (f >= 0) next_mask |= 1u << f;
+      }
+      excl |= next_mask;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (t2[q] == outt || (q == 1 && t2[1] == t2[0]) || cc.find(t2[q]) >= 0) continue;
+        const int v = cc.victim(excl);
+        if (v < 0) break;
+        load_blk(buf(v), base(q ? nx.ba : nx.aa), n, q ? nx.bi : nx.ai, q ? nx.bj : nx.aj);
+        cc.set(v, t2[q]);
+        excl |= 1u << v;
+        next_mask |= 1u << v;
+      }
+    }
+    // 3. the operation
+    if (op.type == OP_DIAG) {
+      double* S = buf(ba);
+      const int p = op.ai, gr = p * BB;
+      for (int e = tid; e < BUFD; e += NT) {  // lower part only; identity on the padded diagonal
+        const int r = e >> 6, c = e & 63;
+        if (c > r) S[sw(r, c)] = 0.0;
+        else if (c == r && gr + r >= n) S[sw(r, c)] = 1.0;
+      }
+      __syncthreads();
+      factor64(S, dinv, &sfail);
+      if (sfail < (1 << 30)) {
+        if (tid == 0) atomicMin(fail, ((unsigned long long)(id0 + mat) << 32) | (unsigned)(gr + sfail));
+        cp_wait_all();
+        return;
+      }
+      double* Xs = buf(bb);
+      trtri64(S, Xs, scr, dinv);
+      for (int e = tid; e < BUFD; e += NT) {  // X_pp = Linv_pp (lower, zero upper)
+        const int r = e >> 6, c = e & 63;
+        if (gr + r < n && gr + c < n) x[(int64_t)(gr + r) * n + gr + c] = Xs[sw(r, c)];
+      }
+      cc.drop_tag(tagof(1, p, p));
+      cc.set(bb, tagof(1, p, p));
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)  // (no accumulation chain crosses a DIAG: acc is dead in it)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      continue;
+    }
+    const double* SA = buf(ba);
+    const double* SB = buf(bb);
+    const bool skip = (op.flags & F_SKIPU) && n0 >= m0 + 32;  // warp tile entirely above the diagonal
+    if (op.flags & (F_ZERO | F_NEGC)) {
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    }
+    if (!skip) {
+      int k0 = 0, k1 = BB;
+      switch (op.kr) {
+        case KR_LT_COL: k1 = n0 + 16; break;
+        case KR_LT_ROW: k1 = m0 + 32; break;
+        case KR_GE_COL: k0 = n0; break;
+        case KR_GE_ROW: k0 = m0; break;
+        case KR_GE_BOTH: k0 = max(m0, n0); break;
+        default: break;
+      }
+      const int fl = op.flags & (F_TA | F_TB);
+      if (fl == F_TB)
+        mma_blk<false, true>(SA, SB, k0, k1, acc);
+      else if (fl == F_TA)
+        mma_blk<true, false>(SA, SB, k0, k1, acc);
+      else
+        mma_blk<false, false>(SA, SB, k0, k1, acc);
+      if (op.flags & F_NEGC) {  // acc = A B - C  (sign -1 below gives C - A B)
+        const double* C = base(op.ca);
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int r = op.ci * BB + m0 + 8 * mi + g, c = op.cj * BB + n0 + 8 * ni + 2 * tg + e;
+              if (r < n && c < n) acc[mi][ni][e] -= C[(int64_t)r * n + c];
+            }
+      }
+    }
+    if (op.st == ST_NONE) continue;
+    // 4. store (write-through), optionally inserting the result into the cache
+    const double sg = (double)op.sg;
+    const int to = tagof(1, op.oi, op.oj);
+    cc.drop_tag(to);
+    if (op.flags & F_CACHE) {
+      __syncthreads();  // every warp is done reading this operation's operands
+      const int v = cc.victim(next_mask);
+      double* D = buf(v);
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) D[sw(m0 + 8 * mi + g, n0 + 8 * ni + 2 * tg + e)] = sg * acc[mi][ni][e];
+      cc.set(v, to);
+    }
+    if (skip) continue;
+    const int gr = op.oi * BB, gc = op.oj * BB;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = m0 + 8 * mi + g, c = n0 + 8 * ni + 2 * tg + e;
+          if (gr + r >= n || gc + c >= n) continue;
+          const double v = sg * acc[mi][ni][e];
+          const bool diag = op.oi == op.oj;
+          if (op.st == ST_FULL) {
+            x[(int64_t)(gr + r) * n + gc + c] = v;
+          } else if (op.st == ST_LOWER) {
+            if (c <= r) x[(int64_t)(gr + r) * n + gc + c] = v;
+          } else {  // ST_SYM
+            if (diag && c > r) continue;
+            x[(int64_t)(gr + r) * n + gc + c] = v;
+            if (!(diag && c == r)) x[(int64_t)(gc + c) * n + gr + r] = v;
+          }
+        }
+  }
+}
+
+}  // namespace bsm
+
+cudaError_t launch_bsmall(const double* dA, double* dX, int64_t batch, int64_t n, int64_t stride, cudaStream_t st,
+                          unsigned long long* dfail, int64_t id0) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(bsm::k_bsmall, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm::SMEM_DYN);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int nb = (int)((n + bsm::BB - 1) / bsm::BB);
+  for (int64_t b0 = 0; b0 < batch; b0 += 0x7fffffff) {
+    const int64_t cnt = batch - b0 < 0x7fffffff ? batch - b0 : 0x7fffffff;
+    bsm::k_bsmall<<<(unsigned)cnt, bsm::NT, bsm::SMEM_DYN, st>>>(dA + b0 * stride, dX + b0 * stride, (int)n, nb,
+                                                                   stride, dfail, id0 + b0);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace tinv
+
+using namespace tinv;
+
+extern "C" {
+
+int tinv_batch_small_launch(const double* dA, double* dX, int64_t batch, int64_t n, int64_t stride,
+                            void* cuda_stream, unsigned long long* dfail) {
+  if (!dA || !dX || !dfail) return set_error(TINV_ERR_BAD_ARG, "null pointer");
+  if (batch < 0 || n < 1 || n > bsm::NBMAX * bsm::BB || stride < n * n)
+    return set_error(TINV_ERR_BAD_ARG, "batched small inversion needs 1 <= n <= 256 and stride >= n*n");
+  if (batch == 0) return TINV_OK;
+  const cudaError_t e = launch_bsmall(dA, dX, batch, n, stride, (cudaStream_t)cuda_stream, dfail, 0);
+  if (e != cudaSuccess) return set_error(TINV_ERR_CUDA, std::string("k_bsmall: ") + cudaGetErrorString(e));
+  return TINV_OK;
+}
+
+// Host-buffer pipeline state, kept between calls (one per process; not
+// thread-safe, like a context).
+namespace {
+struct BsHost {
+  int device = -1;
+  size_t slot_bytes = 0;
+  static constexpr int NS = 3;
+  double* slot[NS] = {};
+  unsigned long long* dfail = nullptr;
+  cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr;
+  cudaEvent_t h2d[NS] = {}, comp[NS] = {}, d2h[NS] = {};
+};
+BsHost g_bs;
+}  // namespace
+
+int tinv_batch_small_host(const double* hA, double* hX, int64_t batch, int64_t n, int device, int64_t* fail_matrix,
+                          int64_t* fail_index, double* ms) {
+  if (fail_matrix) *fail_matrix = -1;
+  if (fail_index) *fail_index = -1;
+  if (!hA || !hX) return set_error(TINV_ERR_BAD_ARG, "null pointer");
+  if (batch < 0 || n < 1 || n > bsm::NBMAX * bsm::BB)
+    return set_error(TINV_ERR_BAD_ARG, "batched small inversion needs 1 <= n <= 256");
+  if (batch == 0) return TINV_OK;
+  int nd = 0;
+  if (cudaGetDeviceCount(&nd) != cudaSuccess || device < 0 || device >= nd) {
+    cudaGetLastError();
+    return set_error(TINV_ERR_NO_DEVICE, "no CUDA device");
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10)
+    return set_error(TINV_ERR_NO_DEVICE, "device is not sm_100 (B200)");
+#define BCK(call)                                                                               \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess) return set_error(TINV_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+  BCK(cudaSetDevice(device));
+  BsHost& H = g_bs;
+  const int64_t mat_bytes = n * n * 8;
+  // chunks of >= 2 waves of CTAs (2 per SM) and ~128 MB: PCIe time per chunk
+  // dwarfs the kernel, three slots keep both copy directions busy
+  int64_t chunk = std::max<int64_t>(4 * prop.multiProcessorCount, (128ll << 20) / mat_bytes);
+  chunk = std::min<int64_t>(chunk, batch);
+  const size_t need = (size_t)(chunk * mat_bytes);
+  if (H.device != device) {
+    H = BsHost();
+    H.device = device;
+    BCK(cudaStreamCreateWithFlags(&H.sh, cudaStreamNonBlocking));
+    BCK(cudaStreamCreateWithFlags(&H.sc, cudaStreamNonBlocking));
+    BCK(cudaStreamCreateWithFlags(&H.sd, cudaStreamNonBlocking));
+    for (int s = 0; s < BsHost::NS; ++s) {
+      BCK(cudaEventCreateWithFlags(&H.h2d[s], cudaEventDisableTiming));
+      BCK(cudaEventCreateWithFlags(&H.comp[s], cudaEventDisableTiming));
+      BCK(cudaEventCreateWithFlags(&H.d2h[s], cudaEventDisableTiming));
+    }
+    BCK(cudaMalloc(&H.dfail, sizeof(unsigned long long)));
+  }
+  if (H.slot_bytes < need) {
+    for (int s = 0; s < BsHost::NS; ++s) {
+      if (H.slot[s]) cudaFree(H.slot[s]);
+      H.slot[s] = nullptr;
+    }
+    H.slot_bytes = 0;
+    for (int s = 0; s < BsHost::NS; ++s) BCK(cudaMalloc(&H.slot[s], need));
+    H.slot_bytes = need;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  BCK(cudaMemsetAsync(H.dfail, 0xff, sizeof(unsigned long long), H.sc));
+  const int64_t nchunks = (batch + chunk - 1) / chunk;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int s = (int)(c % BsHost::NS);
+    const int64_t m0 = c * chunk, cnt = std::min(chunk, batch - m0);
+    const size_t bytes = (size_t)(cnt * mat_bytes);
+    if (c >= BsHost::NS) BCK(cudaStreamWaitEvent(H.sh, H.d2h[s], 0));
+    BCK(cudaMemcpyAsync(H.slot[s], hA + m0 * n * n, bytes, cudaMemcpyHostToDevice, H.sh));
+    BCK(cudaEventRecord(H.h2d[s], H.sh));
+    BCK(cudaStreamWaitEvent(H.sc, H.h2d[s], 0));
+    BCK(launch_bsmall(H.slot[s], H.slot[s], cnt, n, n * n, H.sc, H.dfail, m0));  // failure ids absolute
+    BCK(cudaEventRecord(H.comp[s], H.sc));
+    BCK(cudaStreamWaitEvent(H.sd, H.comp[s], 0));
+    BCK(cudaMemcpyAsync(hX + m0 * n * n, H.slot[s], bytes, cudaMemcpyDeviceToHost, H.sd));
+    BCK(cudaEventRecord(H.d2h[s], H.sd));
+  }
+  BCK(cudaStreamSynchronize(H.sd));
+  BCK(cudaStreamSynchronize(H.sc));
+  unsigned long long f = ~0ull;
+  BCK(cudaMemcpy(&f, H.dfail, sizeof f, cudaMemcpyDeviceToHost));
+  if (ms) *ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+#undef BCK
+  if (f != ~0ull) {
+    if (fail_matrix) *fail_matrix = (int64_t)(f >> 32);
+    if (fail_index) *fail_index = (int64_t)(f & 0xffffffffu);
+    return set_error(TINV_ERR_NOT_SPD, "matrix is not positive definite");
+  }
+  return TINV_OK;
+}
+
+}  // extern "C"

@@ -38,15 +38,47 @@ def step_lauum(linv: np.ndarray, nb: int, direction: str = "U", placement: Place
     return to_dense(tm)
 
 
+def _fused_ok(n: int, nb: int, engine: str) -> bool:
+    from . import _native
+
+    if engine not in ("auto", "fused", "dag"):
+        raise ValueError(f"engine must be 'auto', 'fused' or 'dag', got {engine!r}")
+    ok = nb == n and n <= _native.BATCH_SMALL_MAX_N
+    if engine == "fused" and not ok:
+        raise ValueError(f"the fused batched engine needs nb == n <= {_native.BATCH_SMALL_MAX_N}")
+    return ok and engine != "dag"
+
+
+def _fused_host(a: np.ndarray, out: np.ndarray, config: VariantConfig, device: int) -> np.ndarray:
+    """tinv_batch_small_host on C-contiguous (batch, n, n) float64 buffers."""
+    from . import _native
+    from .kernels import NotPositiveDefiniteError
+    from .scheduler import ExecutionError
+
+    batch, n = a.shape[0], a.shape[-1]
+    rc, fm, fi, _ = _native.batch_small_host(a.ctypes.data, out.ctypes.data, batch, n, device)
+    if rc != _native.OK:
+        s = gen_inversion(1, VariantConfig(config.placement, config.loops, True, config.workers))
+        potrf = next(t for t in s.tasks if t.kind.name == "POTRF")
+        cause = NotPositiveDefiniteError(fi)
+        exc = ExecutionError(potrf, cause)
+        exc.matrix = fm
+        raise exc from cause
+    return out
+
+
 def invert_batched(a: np.ndarray, nb: int | None = None, config: VariantConfig = VariantConfig(),
-                   device: int = 0) -> np.ndarray:
+                   device: int = 0, engine: str = "auto") -> np.ndarray:
     """Inverses of a batch of SPD matrices a[k] (BASELINE config 4: 8192 x n=256).
 
-    One device store holds the whole batch; the per-matrix stream
-    (gen_inversion(n/nb, config), pipelined) is replicated into one merged DAG
-    of independent chains and run by the persistent executor. Failures raise
-    ExecutionError for the failing task of the lowest failing matrix; the
-    exception carries `.matrix`.
+    engine "fused" (the default when nb == n <= 256): the per-matrix stream
+    gen_inversion(1) = POTRF -> TRTRI -> LAUUM runs fused in one thread block
+    per matrix (csrc/batched.cu), the batch streamed through the device in
+    chunks. engine "dag": one device store holds the whole batch; the
+    per-matrix stream (gen_inversion(n/nb, config), pipelined) is replicated
+    into one merged DAG of independent chains and run by the persistent
+    executor. Failures raise ExecutionError for the failing task of the lowest
+    failing matrix; the exception carries `.matrix`.
     """
     from . import _native
     from .scheduler import ExecutionError, _cause
@@ -61,6 +93,8 @@ def invert_batched(a: np.ndarray, nb: int | None = None, config: VariantConfig =
         raise InvalidSizeError(f"matrix order {n} not divisible by tile order {nb}")
     if not np.isfinite(a).all():
         raise ValueError("matrix contains non-finite values")
+    if _fused_ok(n, nb, engine):
+        return _fused_host(a, np.empty_like(a), config, device)
     t = n // nb
     cfg = VariantConfig(config.placement, config.loops, True, config.workers)
     s = gen_inversion(t, cfg)
@@ -112,7 +146,8 @@ def _host_buffer(x, name):
     return x
 
 
-def _run_host(a: np.ndarray, out, nb: int, batch: int, config: VariantConfig, device: int) -> np.ndarray:
+def _run_host(a: np.ndarray, out, nb: int, batch: int, config: VariantConfig, device: int,
+              engine: str = "dag") -> np.ndarray:
     from . import _native
     from .scheduler import ExecutionError, _cause
     from .tile_matrix import InvalidSizeError
@@ -129,6 +164,8 @@ def _run_host(a: np.ndarray, out, nb: int, batch: int, config: VariantConfig, de
         raise ValueError("out must be a C-contiguous float64 array shaped like a")
     if np.shares_memory(a, out):  # result tiles stream out while input tiles still stream in
         raise ValueError("out must not overlap a")
+    if a.ndim == 3 and _fused_ok(n, nb, engine):
+        return _fused_host(a, out, config, device)
     t = n // nb
     pipelined = True if batch > 1 else config.pipelined
     key = (n, nb, batch, device, config.placement, config.loops, pipelined)
@@ -192,12 +229,15 @@ def invert_host(a, nb: int, config: VariantConfig = VariantConfig(), out=None, d
 
 
 def invert_batched_host(a, nb: int | None = None, config: VariantConfig = VariantConfig(), out=None,
-                        device: int = 0) -> np.ndarray:
-    """invert_batched with invert_host's streamed transfers (BASELINE config 4
-    end to end): a is (batch, n, n) in host memory, out likewise."""
+                        device: int = 0, engine: str = "auto") -> np.ndarray:
+    """invert_batched with streamed transfers (BASELINE config 4 end to end):
+    a is (batch, n, n) in host memory, out likewise. The fused engine moves
+    the batch in chunks (host -> device, kernel, device -> host overlapped on
+    three streams); the DAG engine uses invert_host's tile arrivals /
+    departures."""
     a = _host_buffer(a, "a")
     if np.ndim(a) != 3 or a.shape[1] != a.shape[2]:
         from .tile_matrix import InvalidSizeError
 
         raise InvalidSizeError(f"expected a (batch, n, n) array, got shape {np.shape(a)}")
-    return _run_host(a, out, a.shape[1] if nb is None else nb, a.shape[0], config, device)
+    return _run_host(a, out, a.shape[1] if nb is None else nb, a.shape[0], config, device, engine)

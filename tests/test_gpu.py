@@ -317,6 +317,74 @@ def test_batched_failure_reports_matrix():
     assert ei.value.task.kind is P.KernelKind.POTRF
 
 
+# ---------------------------------------------------------------- C4: fused per-matrix engine (csrc/batched.cu)
+def _spd_batch(batch, n, seed, shift=1.0):
+    g = np.random.default_rng(seed).standard_normal((batch, n, n))
+    a = g @ g.transpose(0, 2, 1) / n + shift * np.eye(n)
+    return np.tril(a) + np.transpose(np.tril(a, -1), (0, 2, 1))
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 33, 64, 65, 100, 128, 130, 191, 200, 255, 256])
+def test_fused_batched_vs_oracle(n):
+    """gen_inversion(1) per matrix fused in one CTA: parity with the oracle's
+    POTRF -> TRTRI -> LAUUM of the single tile (odd n: synchronous loads;
+    n % 64 != 0: identity-padded blocks)."""
+    a = _spd_batch(7, n, 40 + n, 0.5)
+    x = P.invert_batched(a, n, engine="fused")
+    assert np.array_equal(x, np.transpose(x, (0, 2, 1)))  # exactly symmetric
+    for k in range(a.shape[0]):
+        ref = O.invert(a[k], n)
+        assert rel(x[k], ref) <= 1e-10 * np.linalg.cond(a[k])
+        assert O.residual(a[k], x[k]) < 10
+    assert np.array_equal(P.invert_batched(a, n, engine="fused"), x)  # deterministic
+
+
+def test_fused_batched_matches_dag_engine_and_device_api():
+    import torch
+
+    a = _spd_batch(300, 256, 7)
+    xf = P.invert_batched(a, 256)  # auto -> fused
+    xd = P.invert_batched(a, 256, engine="dag")
+    assert rel(xf, xd) <= 1e-10 * max(np.linalg.cond(a[k]) for k in range(0, 300, 50))
+    # device-pointer entry point, out of place and in place: same bits
+    da = torch.from_numpy(a).cuda()
+    dx = torch.empty_like(da)
+    fail = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    _native.batch_small_launch(da.data_ptr(), dx.data_ptr(), 300, 256, 256 * 256, st, fail.data_ptr())
+    torch.cuda.synchronize()
+    assert int(fail.item()) == -1
+    assert np.array_equal(dx.cpu().numpy(), xf)
+    _native.batch_small_launch(da.data_ptr(), da.data_ptr(), 300, 256, 256 * 256, st, fail.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(da.cpu().numpy(), xf)
+    # pinned host buffers through the chunked pipeline (several chunks)
+    big = np.concatenate([a] * 4)
+    hb, hy = _pinned(big.shape), _pinned(big.shape)
+    hb[...] = big
+    P.invert_batched_host(hb, out=hy)
+    assert np.array_equal(hy, np.concatenate([xf] * 4))
+
+
+@pytest.mark.parametrize("n,col", [(256, 10), (256, 200), (100, 70), (33, 0)])
+def test_fused_batched_failure_reports_matrix_and_column(n, col):
+    a = _spd_batch(9, n, 3)
+    a[6, col, col] = -5.0
+    a[4, col, col] = -5.0  # the lowest failing matrix is reported
+    with pytest.raises(O.NotPositiveDefinite) as eo:
+        O.potrf(np.tril(a[4]))
+    with pytest.raises(P.ExecutionError) as ei:
+        P.invert_batched(a, n)
+    assert ei.value.matrix == 4
+    assert isinstance(ei.value.cause, P.NotPositiveDefiniteError)
+    assert ei.value.cause.index == eo.value.index
+    assert ei.value.task.kind is P.KernelKind.POTRF
+    a[4, col, col] = np.nan
+    with pytest.raises(P.ExecutionError) as ei:
+        P.invert_batched_host(a, out=np.empty_like(a))
+    assert ei.value.matrix == 4 and ei.value.cause.index == eo.value.index
+
+
 # ---------------------------------------------------------------- multi-GPU distribution (loopback)
 @pytest.mark.parametrize("grid", [(1, 2), (2, 2), (2, 4)])
 def test_distributed_loopback_bitwise(grid):
