@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--n", type=int, default=None)
     p.add_argument("--nb", type=int, default=None)
     p.add_argument("--batch", type=int, default=None)
+    p.add_argument("--engine", default="auto", choices=["auto", "fused", "dag"],
+                   help="batched workloads: fused per-matrix kernel (nb == n <= 256) or the DAG executor")
     p.add_argument("--placement", default="out", choices=["in", "out"])
     p.add_argument("--loops", default=None,
                    help="loop orders of the three steps; default DDU at c3 (result tiles become final "
@@ -304,8 +306,14 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda") if in_bytes <= 4e8 else None
 
     stream = torch.cuda.current_stream()
-    ctx = _native.Context(n, nb, local, batch=batch)
-    ctx.set_stream(stream.cuda_stream)
+    fused = batch > 1 and args.engine != "dag" and nb == n <= _native.BATCH_SMALL_MAX_N
+    if args.engine == "fused" and not fused:
+        raise SystemExit("--engine fused needs a batched workload with nb == n <= 256")
+    config["engine"] = ("fused: one CTA per matrix runs gen_inversion(1) = POTRF -> TRTRI -> LAUUM "
+                        "(tinv_batch_small_launch)" if fused else "DAG executor (tinv_plan_exec)")
+    ctx = None if fused else _native.Context(n, nb, local, batch=batch)
+    if ctx is not None:
+        ctx.set_stream(stream.cuda_stream)
     s = P.gen_inversion(t, P.VariantConfig(P.Placement(args.placement), args.loops, pipelined))
     table = s.table()
     bars = np.array(sorted(s.barriers), dtype=np.int64)
@@ -344,14 +352,28 @@ def main():
             ctx.close()  # the exported store cannot be reused: a fresh one for the replicas
             ctx = _native.Context(n, nb, local, batch=batch)
             ctx.set_stream(stream.cuda_stream)
-    plan = mg.plan if mg is not None else _native.Plan(ctx, table, t, bars)
-    if plan.rc != 0:
+    plan = None if fused else mg.plan if mg is not None else _native.Plan(ctx, table, t, bars)
+    if plan is not None and plan.rc != 0:
         raise RuntimeError(plan.msg)
-    stats = plan.stats()
+    stats = {"engine": "fused", "ctas": batch, "block_ops_per_matrix": 56 if n > 192 else None} if fused \
+        else plan.stats()
 
     kern_ms = []
+    fail = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    kev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+
+    def fused_step():
+        kev[0].record(stream)
+        _native.batch_small_launch(a.data_ptr(), x.data_ptr(), batch, n, n * n, stream.cuda_stream, fail.data_ptr())
+        kev[1].record(stream)
+        kev[1].synchronize()
+        kern_ms.append(kev[0].elapsed_time(kev[1]))
+        if int(fail.item()) != -1:
+            raise RuntimeError(f"fused batched inversion failed: {int(fail.item()):#x}")
 
     def step():
+        if fused:
+            return fused_step()
         ctx.put_dense_device(a.data_ptr(), n)
         rc, err, ms = mg.run() if mg is not None else plan.run()
         if rc != 0:
@@ -456,9 +478,10 @@ def main():
         ha.copy_(a)
         hx = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
         del a, x
-        ctx.set_stream(0)
-        plan.close()
-        ctx.close()
+        if ctx is not None:
+            ctx.set_stream(0)
+            plan.close()
+            ctx.close()
         torch.cuda.empty_cache()
         ha_np, hx_np = ha.numpy(), hx.numpy()
         cfg = P.VariantConfig(P.Placement(args.placement), args.loops, pipelined)
@@ -467,7 +490,7 @@ def main():
             if batch == 1:
                 P.invert_host(ha_np, nb, cfg, out=hx_np, device=local)
             else:
-                P.invert_batched_host(ha_np, nb, cfg, out=hx_np, device=local)
+                P.invert_batched_host(ha_np, nb, cfg, out=hx_np, device=local, engine="fused" if fused else "dag")
 
         e2e_step()
         barrier()
@@ -479,9 +502,11 @@ def main():
         e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / k)
         T = t * (t + 1) // 2
         e2e = {"value": world * flops / (e2e_ms * 1e-3) / 1e9, "unit": "Gflop/s",
-               "h2d_bytes_per_step": batch * T * nb * nb * 8, "d2h_bytes_per_step": in_bytes,
+               "h2d_bytes_per_step": in_bytes if fused else batch * T * nb * nb * 8, "d2h_bytes_per_step": in_bytes,
                "ms_per_step": e2e_ms, "steps": k,
-               "path": ("paper_1002_4057_b200.invert_host(pinned A, out=pinned X): lower tiles host->device by the "
+               "path": ("paper_1002_4057_b200.invert_batched_host(pinned A, out=pinned X), fused engine: chunks "
+                        "of matrices host->device, kernel, device->host on three streams, overlapped") if fused else
+                       ("paper_1002_4057_b200.invert_host(pinned A, out=pinned X): lower tiles host->device by the "
                         "copy engines overlapped with the executor, result tiles device->host (symmetrized) as they "
                         "become final; plan cached after the warm-up call")}
         P.clear_plan_cache()
@@ -515,14 +540,16 @@ def main():
                          "frac": achieved / DMMA_PEAK_TFLOPS, "traffic": traffic,
                          "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one exec_kernel "
                                            "launch, ncu application replay (profiles/exec_c3_traffic.json)",
-                         "kernel": "tinv::exec_kernel (persistent DAG executor, DMMA.8x8x4)",
+                         "kernel": "tinv::bsm::k_bsmall (one CTA per matrix: fused POTRF -> TRTRI -> LAUUM, "
+                                   "64x64 DMMA.8x8x4 block program)" if fused else
+                                   "tinv::exec_kernel (persistent DAG executor, DMMA.8x8x4)",
                          "algorithmic": f"n^3 = {flops:.3e} flop per launch",
                          "peak_source": "measured FP64 DMMA peak (tools/fp64_peak.cu); cuBLAS DGEMM "
                                         f"{DGEMM_TFLOPS} TF/s for context; MEASURED_PEAKS.json has no FP64 entry"},
             "pct_fp64_peak": 100.0 * value / world / 1e3 / DMMA_PEAK_TFLOPS,  # per GPU
             "kernel_ms": kern_avg, "plan": stats,
             "residual": res, "symmetry_err": sym_err,
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": (1 if fused else 3) * args.steps,
             "clocks": clk.summary(),
             "e2e": e2e, "cpu_baseline": cpu,
         }

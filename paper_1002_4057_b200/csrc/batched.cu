@@ -33,6 +33,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <algorithm>
 #include <chrono>
 #include <string>
@@ -218,12 +221,22 @@ __device__ __noinline__ void factor16(double* S, int p0, double* dinv, int* fail
 // factors the panel's diagonal sub-block, every thread row-solves the panel
 // below it, the trailing lower 8x8 tiles are updated on DMMA. The strict upper
 // part of S must be zero on entry; it is zero on exit.
-__device__ void factor64(double* S, double* dinv, int* fail) {
+template <bool PROF>
+__device__ void factor64(double* S, double* dinv, int* fail, long long* pacc) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
+  long long t0 = PROF ? clock64() : 0;
+  auto probe = [&](int c) {
+    if constexpr (PROF) {
+      const long long now = clock64();
+      pacc[c] += now - t0;
+      t0 = now;
+    }
+  };
   for (int P = 0; P < 4; ++P) {
     const int p0 = 16 * P;
     if (warp == 0) factor16(S, p0, dinv, fail);
     __syncthreads();
+    probe(8);
     if (P == 3) break;
     // panel rows q >= p0 + 16: v L_PP^T = a, right-looking substitution
     for (int q = p0 + 16 + tid; q < BB; q += NT) {
@@ -240,6 +253,7 @@ __device__ void factor64(double* S, double* dinv, int* fail) {
       for (int k = 0; k < 16; ++k) S[sw(q, p0 + k)] = v[k];
     }
     __syncthreads();
+    probe(9);
     // trailing lower 8x8 tiles of rows / columns [p0 + 16, 64): -= L_P L_P^T
     const int t0 = p0 + 16, nt8 = (BB - t0) / 8, ntiles = nt8 * (nt8 + 1) / 2;
     for (int tt = warp; tt < ntiles; tt += NT / 32) {
@@ -256,6 +270,7 @@ __device__ void factor64(double* S, double* dinv, int* fail) {
       S[sw(r0 + g, c0 + 2 * tg + 1)] = acc[1];
     }
     __syncthreads();
+    probe(10);
   }
 }
 
@@ -363,9 +378,13 @@ struct Cache {
 __device__ __forceinline__ int tagof(int arr, int i, int j) { return 1 + ((arr << 8) | (i << 4) | j); }
 
 // ---------------------------------------------------------------- kernel
+// PROF: thread 0 accumulates clock64 spans per phase into prof[NPROF] (one
+// atomicAdd per CTA at exit); TINV_BSMALL_PROF=1 selects this instantiation.
+constexpr int NPROF = 13;  // wait, prefetch, factor, trtri, diag-store, mma, store, ops, f16, subst, trail, pf-issue, pf-count
+template <bool PROF>
 __global__ void __launch_bounds__(NT, 2)
     k_bsmall(const double* __restrict__ A, double* X, int n, int nb, int64_t mstride, unsigned long long* fail,
-             int64_t id0) {
+             int64_t id0, unsigned long long* prof) {
   extern __shared__ __align__(128) double dsm[];
   __shared__ BOp ops[MAXOPS];
   __shared__ double dinv[BB];
@@ -389,9 +408,25 @@ __global__ void __launch_bounds__(NT, 2)
   for (int b = 0; b < NBUF; ++b) cc.tag[b] = 0, cc.use[b] = 0;
   cc.clk = 0;
   double acc[4][2][2];
+  long long pt = 0, pacc[NPROF] = {};
+  auto probe = [&](int c) {
+    if constexpr (PROF) {
+      const long long now = clock64();
+      if (c >= 0) pacc[c] += now - pt;
+      pt = now;
+    }
+  };
+  auto flush = [&]() {
+    if constexpr (PROF) {
+      if (tid == 0)
+        for (int c = 0; c < NPROF; ++c) atomicAdd(prof + c, (unsigned long long)pacc[c]);
+    }
+  };
+  probe(-1);
 
   for (int o = 0; o < nop; ++o) {
     const BOp op = ops[o];
+    if constexpr (PROF) pacc[7] += 1;
     // 1. operands not prefetched: load now (exposed). The barrier orders the
     // previous operation's global stores and smem reads before the loads.
     int ba = -1, bb = -1;
@@ -422,6 +457,7 @@ __global__ void __launch_bounds__(NT, 2)
     }
     cp_wait_all();
     __syncthreads();
+    probe(0);
     // 2. prefetch the next operation's operands into buffers this one does not use
     unsigned next_mask = 0;
     if (o + 1 < nop && ops[o + 1].type == OP_MMA) {
@@ -440,12 +476,16 @@ __global__ void __launch_bounds__(NT, 2)
         if (t2[q] == outt || (q == 1 && t2[1] == t2[0]) || cc.find(t2[q]) >= 0) continue;
         const int v = cc.victim(excl);
         if (v < 0) break;
+        probe(1);
         load_blk(buf(v), base(q ? nx.ba : nx.aa), n, q ? nx.bi : nx.ai, q ? nx.bj : nx.aj);
+        probe(11);
+        if constexpr (PROF) pacc[12] += 1;
         cc.set(v, t2[q]);
         excl |= 1u << v;
         next_mask |= 1u << v;
       }
     }
+    probe(1);
     // 3. the operation
     if (op.type == OP_DIAG) {
       double* S = buf(ba);
@@ -456,20 +496,24 @@ __global__ void __launch_bounds__(NT, 2)
         else if (c == r && gr + r >= n) S[sw(r, c)] = 1.0;
       }
       __syncthreads();
-      factor64(S, dinv, &sfail);
+      factor64<PROF>(S, dinv, &sfail, pacc);
+      probe(2);
       if (sfail < (1 << 30)) {
         if (tid == 0) atomicMin(fail, ((unsigned long long)(id0 + mat) << 32) | (unsigned)(gr + sfail));
         cp_wait_all();
+        flush();
         return;
       }
       double* Xs = buf(bb);
       trtri64(S, Xs, scr, dinv);
+      probe(3);
       for (int e = tid; e < BUFD; e += NT) {  // X_pp = Linv_pp (lower, zero upper)
         const int r = e >> 6, c = e & 63;
         if (gr + r < n && gr + c < n) x[(int64_t)(gr + r) * n + gr + c] = Xs[sw(r, c)];
       }
       cc.drop_tag(tagof(1, p, p));
       cc.set(bb, tagof(1, p, p));
+      probe(4);
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)  // (no accumulation chain crosses a DIAG: acc is dead in it)
 #pragma unroll
@@ -515,6 +559,7 @@ __global__ void __launch_bounds__(NT, 2)
             }
       }
     }
+    probe(5);
     if (op.st == ST_NONE) continue;
     // 4. store (write-through), optionally inserting the result into the cache
     const double sg = (double)op.sg;
@@ -532,7 +577,10 @@ __global__ void __launch_bounds__(NT, 2)
           for (int e = 0; e < 2; ++e) D[sw(m0 + 8 * mi + g, n0 + 8 * ni + 2 * tg + e)] = sg * acc[mi][ni][e];
       cc.set(v, to);
     }
-    if (skip) continue;
+    if (skip) {
+      probe(6);
+      continue;
+    }
     const int gr = op.oi * BB, gc = op.oj * BB;
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
@@ -554,24 +602,54 @@ __global__ void __launch_bounds__(NT, 2)
             if (!(diag && c == r)) x[(int64_t)(gc + c) * n + gr + r] = v;
           }
         }
+    probe(6);
   }
+  flush();
 }
 
 }  // namespace bsm
 
 cudaError_t launch_bsmall(const double* dA, double* dX, int64_t batch, int64_t n, int64_t stride, cudaStream_t st,
                           unsigned long long* dfail, int64_t id0) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(bsm::k_bsmall, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm::SMEM_DYN);
-    if (e != cudaSuccess) return e;
-    attr = true;
+  static int prof_mode = -1;
+  static unsigned long long* dprof = nullptr;
+  if (prof_mode < 0) {
+    const char* e = getenv("TINV_BSMALL_PROF");
+    prof_mode = e && atoi(e) ? 1 : 0;
+    cudaError_t r = cudaFuncSetAttribute(bsm::k_bsmall<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         bsm::SMEM_DYN);
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(bsm::k_bsmall<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm::SMEM_DYN);
+    if (r == cudaSuccess && prof_mode) r = cudaMalloc(&dprof, bsm::NPROF * sizeof(unsigned long long));
+    if (r != cudaSuccess) {
+      prof_mode = -1;
+      return r;
+    }
   }
   const int nb = (int)((n + bsm::BB - 1) / bsm::BB);
+  static const int extra = getenv("TINV_BSMALL_EXTRA_SMEM") ? atoi(getenv("TINV_BSMALL_EXTRA_SMEM")) : 0;
+  if (extra) {
+    cudaFuncSetAttribute(bsm::k_bsmall<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm::SMEM_DYN + extra);
+    cudaFuncSetAttribute(bsm::k_bsmall<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm::SMEM_DYN + extra);
+  }
+  if (prof_mode) cudaMemsetAsync(dprof, 0, bsm::NPROF * sizeof(unsigned long long), st);
   for (int64_t b0 = 0; b0 < batch; b0 += 0x7fffffff) {
     const int64_t cnt = batch - b0 < 0x7fffffff ? batch - b0 : 0x7fffffff;
-    bsm::k_bsmall<<<(unsigned)cnt, bsm::NT, bsm::SMEM_DYN, st>>>(dA + b0 * stride, dX + b0 * stride, (int)n, nb,
-                                                                   stride, dfail, id0 + b0);
+    if (prof_mode)
+      bsm::k_bsmall<true><<<(unsigned)cnt, bsm::NT, bsm::SMEM_DYN + extra, st>>>(dA + b0 * stride, dX + b0 * stride, (int)n,
+                                                                         nb, stride, dfail, id0 + b0, dprof);
+    else
+      bsm::k_bsmall<false><<<(unsigned)cnt, bsm::NT, bsm::SMEM_DYN + extra, st>>>(dA + b0 * stride, dX + b0 * stride, (int)n,
+                                                                          nb, stride, dfail, id0 + b0, nullptr);
+  }
+  if (prof_mode) {
+    unsigned long long h[bsm::NPROF];
+    cudaMemcpyAsync(h, dprof, sizeof h, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    static const char* names[bsm::NPROF] = {"wait", "prefetch", "factor", "trtri", "diag-store", "mma", "store", "ops", "f16", "subst", "trail", "pf-issue", "pf-count"};
+    fprintf(stderr, "[tinv bsmall] cycles per matrix:");
+    for (int c = 0; c < bsm::NPROF; ++c) fprintf(stderr, " %s %.0f", names[c], (double)h[c] / (double)batch);
+    fprintf(stderr, "\n");
   }
   return cudaGetLastError();
 }
