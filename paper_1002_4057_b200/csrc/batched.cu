@@ -55,11 +55,11 @@ constexpr int BUFD = BB * BB;     // doubles per smem block buffer
 constexpr int NBUF = 3;
 constexpr int TLD = 36;           // row stride of the 32x32 TRTRI scratch
 constexpr int SMEM_DYN = NBUF * BUFD * 8 + 32 * TLD * 8;
-constexpr unsigned FULL = 0xffffffffu;
 
 enum : int8_t { OP_DIAG = 1, OP_MMA = 2 };
-// per-warp K range of a triangular operand (the warp's output tile is rows
-// [32 wm, 32 wm + 32) x columns [16 wn, 16 wn + 16) of the 64x64 block)
+// K range of a triangular operand per 16x16 output quad (qr, qc):
+// LT_COL k < 16(qc+1), LT_ROW k < 16(qr+1), GE_COL k >= 16 qc, GE_ROW k >= 16 qr,
+// GE_BOTH k >= 16 max(qr, qc)
 enum : int8_t { KR_FULL, KR_LT_COL, KR_LT_ROW, KR_GE_COL, KR_GE_ROW, KR_GE_BOTH };
 enum : int8_t { ST_NONE = 0, ST_FULL = 1, ST_LOWER = 2, ST_SYM = 3 };
 enum : int8_t { F_ZERO = 1, F_NEGC = 2, F_CACHE = 4, F_SKIPU = 8, F_TA = 16, F_TB = 32 };
@@ -70,6 +70,20 @@ struct BOp {
   int8_t aa, ai, aj, ba;
   int8_t bi, bj, ca, ci;
   int8_t cj, oi, oj, sg;
+  int8_t map, pad0, pad1, pad2;
+};
+
+// Output quads (16x16) of a warp: two slots, (qr << 2 | qc) or -1. The maps
+// balance the DMMA work of triangular K ranges over the 8 warps; every
+// operation of an accumulation chain uses the chain's map.
+enum : int8_t { MAP_COL = 0, MAP_ROW = 1, MAP_LOWER = 2 };
+__constant__ int8_t c_map[3][8][2] = {
+    // MAP_COL: quad columns qc and 3 - qc in one quad row (K ranges by column: 16(qc+1) + 16(4-qc))
+    {{0, 3}, {4, 7}, {8, 11}, {12, 15}, {1, 2}, {5, 6}, {9, 10}, {13, 14}},
+    // MAP_ROW: quad rows qr and 3 - qr in one quad column
+    {{0, 12}, {1, 13}, {2, 14}, {3, 15}, {4, 8}, {5, 9}, {6, 10}, {7, 11}},
+    // MAP_LOWER: the 10 lower quads; K >= 16 qr work 4,3,3,3,3,2,1,1 (x16)
+    {{0, -1}, {4, -1}, {5, -1}, {8, 12}, {9, 13}, {10, -1}, {14, -1}, {15, -1}},
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -102,6 +116,8 @@ __device__ int gen_program(BOp* ops, int nb) {
     o.ba = (int8_t)ba, o.bi = (int8_t)bi, o.bj = (int8_t)bj;
     o.ca = (int8_t)ca, o.ci = (int8_t)ci, o.cj = (int8_t)cj;
     o.oi = (int8_t)oi, o.oj = (int8_t)oj, o.sg = (int8_t)sg;
+    o.map = (flags & F_SKIPU) ? MAP_LOWER : (kr == KR_LT_ROW || kr == KR_GE_ROW) ? MAP_ROW : MAP_COL;
+    o.pad0 = o.pad1 = o.pad2 = 0;
     ops[k++] = o;
   };
   // step 1: Cholesky (POTRF), right-looking over 64-wide panels
@@ -130,9 +146,11 @@ __device__ int gen_program(BOp* ops, int nb) {
   // step 3: A^-1 = X^T X (LAUUM), lower blocks with their mirrors
   for (int i = 0; i < nb; ++i)
     for (int j = 0; j <= i; ++j)
-      for (int q = i; q < nb; ++q)
+      for (int q = i; q < nb; ++q) {
         mma(1, q, i, 1, q, j, F_TA | (q == i ? F_ZERO : 0) | (i == j ? F_SKIPU : 0),
             q == i ? (j == i ? KR_GE_BOTH : KR_GE_ROW) : KR_FULL, q == nb - 1 ? ST_SYM : ST_NONE, i, j, 1);
+        if (i != j) ops[k - 1].map = MAP_ROW;  // the chain's map (its first operation is GE_ROW)
+      }
   return k;
 }
 
@@ -157,72 +175,83 @@ __device__ __forceinline__ void load_blk(double* S, const double* G, int n, int 
   cp_commit();
 }
 
-// ---------------------------------------------------------------- DMMA block product
-// acc (warp tile rows 32 wm.., cols 16 wn..) += sum_{k0 <= k < k1} A(r, k) B(k, c);
-// A(r, k) = SA[r][k] (or SA[k][r] if TA), B(k, c) = SB[k][c] (or SB[c][k] if TB).
-// k0, k1 multiples of 16.
+// ---------------------------------------------------------------- DMMA quad product
+// acc (16x16 quad at rows 16 qr.., cols 16 qc..; 2x2 m8n8 tiles) +=
+// sum_{k0 <= k < k1} A(r, k) B(k, c); A(r, k) = SA[r][k] (SA[k][r] if TA),
+// B(k, c) = SB[k][c] (SB[c][k] if TB). k0, k1 multiples of 16.
 template <bool TA, bool TB>
-__device__ __forceinline__ void mma_blk(const double* SA, const double* SB, int k0, int k1, double (&acc)[4][2][2]) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3, warp = threadIdx.x >> 5;
-  const int m0 = 32 * (warp & 1), n0 = 16 * (warp >> 1);
+__device__ __forceinline__ void mma_quad(const double* SA, const double* SB, int qr, int qc, int k0, int k1,
+                                         double (&acc)[2][2][2]) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3;
+  const int r0 = 16 * qr, c0 = 16 * qc;
   for (int k = k0; k < k1; k += 16) {
-    double a[4][4], b[4][2];
+    double a[4][2], b[4][2];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int kk = k + 4 * u + tg;
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[u][mi] = TA ? SA[sw(kk, m0 + 8 * mi + g)] : SA[sw(m0 + 8 * mi + g, kk)];
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni) b[u][ni] = TB ? SB[sw(n0 + 8 * ni + g, kk)] : SB[sw(kk, n0 + 8 * ni + g)];
+      for (int t = 0; t < 2; ++t) {
+        a[u][t] = TA ? SA[sw(kk, r0 + 8 * t + g)] : SA[sw(r0 + 8 * t + g, kk)];
+        b[u][t] = TB ? SB[sw(c0 + 8 * t + g, kk)] : SB[sw(kk, c0 + 8 * t + g)];
+      }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
+      for (int ti = 0; ti < 2; ++ti)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], a[u][mi], b[u][ni]);
+        for (int tj = 0; tj < 2; ++tj) dmma(acc[ti][tj], a[u][ti], b[u][tj]);
   }
 }
 
 // ---------------------------------------------------------------- diagonal block
-// Warp 0: factor the 16x16 diagonal sub-block at (p0, p0) in place (lane i & 15
-// holds row i; right-looking, shuffles); 1 / L[k][k] -> dinv[p0 + k]; the first
-// failing pivot (kernels.py:68-71: not d > 0, or d non-finite) -> *fail.
-__device__ __noinline__ void factor16(double* S, int p0, double* dinv, int* fail) {
-  const int lane = threadIdx.x & 31, i = lane & 15;
-  double r[16];
+// Cholesky of the lower 8x8 block at (p0, p0) of S in registers (right-looking;
+// kernels.py:68-71 failure test: not d > 0, or d non-finite) and the inverse of
+// the factor: x = L^-1 (lower; x[i][i] = 1 / L[i][i]). Returns the first
+// failing pivot or -1.
+__device__ __forceinline__ int chol8_inv(const double* S, int p0, double (&x)[8][8]) {
+  double l[8][8], il[8];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) r[j] = j <= i ? S[sw(p0 + i, p0 + j)] : 0.0;
-  unsigned bad = 0;
-  double myil = 1.0;
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const double piv = __shfl_sync(FULL, r[k], k);
-    const bool b = !(piv > 0.0) || !isfinite(piv);
-    bad |= b ? (1u << k) : 0u;
-    const double il = b ? 1.0 : rsqrt(piv);
-    myil = i == k ? il : myil;
-    r[k] = i == k ? (b ? 1.0 : piv * il) : (i > k ? r[k] * il : r[k]);
+    for (int j = 0; j <= i; ++j) l[i][j] = S[sw(p0 + i, p0 + j)];
+  int bad = -1;
 #pragma unroll
-    for (int j = k + 1; j < 16; ++j) {
-      const double v = __shfl_sync(FULL, r[k], j);  // L[j][k]
-      r[j] = i >= j ? fma(-r[k], v, r[j]) : r[j];
+  for (int k = 0; k < 8; ++k) {
+    const double d = l[k][k];
+    const bool b = !(d > 0.0) || !isfinite(d);
+    bad = (b && bad < 0) ? k : bad;
+    il[k] = b ? 1.0 : rsqrt(d);
+    l[k][k] = b ? 1.0 : d * il[k];
+#pragma unroll
+    for (int i = k + 1; i < 8; ++i) l[i][k] *= il[k];
+#pragma unroll
+    for (int j = k + 1; j < 8; ++j)
+#pragma unroll
+      for (int i = j; i < 8; ++i) l[i][j] = fma(-l[i][k], l[j][k], l[i][j]);
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    x[c][c] = il[c];
+#pragma unroll
+    for (int i = c + 1; i < 8; ++i) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = c; k < i; ++k) t = fma(l[i][k], x[k][c], t);
+      x[i][c] = -t * il[i];
     }
   }
-  if (lane == 0 && bad) atomicMin(fail, p0 + __ffs(bad) - 1);
-  if (lane < 16) {
-    dinv[p0 + i] = myil;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) S[sw(p0 + i, p0 + j)] = j <= i ? r[j] : 0.0;
-  }
+  return bad;
 }
 
-// In-place Cholesky of the lower 64x64 block in S (16-wide panels): warp 0
-// factors the panel's diagonal sub-block, every thread row-solves the panel
-// below it, the trailing lower 8x8 tiles are updated on DMMA. The strict upper
-// part of S must be zero on entry; it is zero on exit.
+// In-place Cholesky of the lower 64x64 block in S over 8-wide panels: warps
+// 0-1 factor the panel's 8x8 diagonal block redundantly in registers
+// (chol8_inv: no shuffles on the column chain) and each solves one panel row
+// below it by the block inverse; the trailing lower 8x8 tiles are updated on
+// DMMA. The inverses of the eight 8x8 diagonal blocks go to X (zeroed here)
+// for trtri64. The strict upper part of S must be zero on entry.
 template <bool PROF>
-__device__ void factor64(double* S, double* dinv, int* fail, long long* pacc) {
+__device__ void factor64(double* S, double* X, int* fail, long long* pacc) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
   long long t0 = PROF ? clock64() : 0;
   auto probe = [&](int c) {
@@ -232,40 +261,50 @@ __device__ void factor64(double* S, double* dinv, int* fail, long long* pacc) {
       t0 = now;
     }
   };
-  for (int P = 0; P < 4; ++P) {
-    const int p0 = 16 * P;
-    if (warp == 0) factor16(S, p0, dinv, fail);
-    __syncthreads();
-    probe(8);
-    if (P == 3) break;
-    // panel rows q >= p0 + 16: v L_PP^T = a, right-looking substitution
-    for (int q = p0 + 16 + tid; q < BB; q += NT) {
-      double v[16];
+  for (int e = tid; e < BUFD; e += NT) X[e] = 0.0;
+  for (int P = 0; P < 8; ++P) {
+    const int p0 = 8 * P;
+    if (warp < 2) {
+      double x[8][8];
+      const int bad = chol8_inv(S, p0, x);
+      if (tid == 0) {
+        if (bad >= 0) atomicMin(fail, p0 + bad);
 #pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = S[sw(q, p0 + k)];
+        for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        v[j] *= dinv[p0 + j];
-#pragma unroll
-        for (int jj = j + 1; jj < 16; ++jj) v[jj] = fma(-v[j], S[sw(p0 + jj, p0 + j)], v[jj]);
+          for (int j = 0; j <= i; ++j) X[sw(p0 + i, p0 + j)] = x[i][j];
       }
+      const int q = p0 + 8 + tid;  // panel row: v = a L^-T = a x^T
+      if (q < BB) {
+        double a[8], v[8];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) S[sw(q, p0 + k)] = v[k];
+        for (int k = 0; k < 8; ++k) a[k] = S[sw(q, p0 + k)];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          double t = 0.0;
+#pragma unroll
+          for (int k = 0; k <= c; ++k) t = fma(a[k], x[c][k], t);
+          v[c] = t;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) S[sw(q, p0 + k)] = v[k];
+      }
     }
     __syncthreads();
-    probe(9);
-    // trailing lower 8x8 tiles of rows / columns [p0 + 16, 64): -= L_P L_P^T
-    const int t0 = p0 + 16, nt8 = (BB - t0) / 8, ntiles = nt8 * (nt8 + 1) / 2;
+    probe(8);
+    if (P == 7) break;
+    // trailing lower 8x8 tiles of rows / columns [p0 + 8, 64): -= L_P L_P^T (K = 8)
+    const int t0r = p0 + 8, nt8 = 7 - P, ntiles = nt8 * (nt8 + 1) / 2;
     for (int tt = warp; tt < ntiles; tt += NT / 32) {
       int ti = 0, rem = tt;
       while (rem > ti) {
         rem -= ti + 1;
         ++ti;
       }
-      const int r0 = t0 + 8 * ti, c0 = t0 + 8 * rem;
+      const int r0 = t0r + 8 * ti, c0 = t0r + 8 * rem;
       double acc[2] = {S[sw(r0 + g, c0 + 2 * tg)], S[sw(r0 + g, c0 + 2 * tg + 1)]};
 #pragma unroll
-      for (int k = 0; k < 16; k += 4) dmma(acc, -S[sw(r0 + g, p0 + k + tg)], S[sw(c0 + g, p0 + k + tg)]);
+      for (int k = 0; k < 8; k += 4) dmma(acc, -S[sw(r0 + g, p0 + k + tg)], S[sw(c0 + g, p0 + k + tg)]);
       S[sw(r0 + g, c0 + 2 * tg)] = acc[0];
       S[sw(r0 + g, c0 + 2 * tg + 1)] = acc[1];
     }
@@ -274,7 +313,7 @@ __device__ void factor64(double* S, double* dinv, int* fail, long long* pacc) {
   }
 }
 
-// One warp: 8x8 tile D[dr..][dc..] = sgn * sum_{k < K} A(ar + i, ac + k) B(br + k, bc + j).
+// One warp: 8x8 tile D(i, j) = sgn * sum_{k < K} A(i, k) B(k, j).
 template <class FA, class FB, class FD>
 __device__ __forceinline__ void tile8(FA A, FB B, FD D, int K, double sgn) {
   const int lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3;
@@ -284,56 +323,32 @@ __device__ __forceinline__ void tile8(FA A, FB B, FD D, int K, double sgn) {
   D(g, 2 * tg + 1, sgn * acc[1]);
 }
 
-// X = L^-1 for the lower 64x64 L (strict upper zero, 1 / L[k][k] in dinv), by
-// recursive doubling: 16x16 diagonal inverses (warps 0-3, lane = column), then
-// for s = 16, 32: [[A, 0], [B, C]]^-1 = [[A^-1, 0], [-C^-1 B A^-1, C^-1]].
-__device__ void trtri64(const double* L, double* X, double* T, const double* dinv) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int e = tid; e < BUFD; e += NT) X[e] = 0.0;
-  __syncthreads();
-  if (warp < 4) {
-    const int q0 = 16 * warp, jc = lane & 15;
-    double x[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) x[i] = i == jc ? 1.0 : 0.0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      x[i] *= dinv[q0 + i];
-#pragma unroll
-      for (int ii = i + 1; ii < 16; ++ii) x[ii] = fma(-L[sw(q0 + ii, q0 + i)], x[i], x[ii]);
+// X = L^-1 for the lower 64x64 L (strict upper zero) given the inverses of its
+// 8x8 diagonal blocks in X (rest of X zero), by recursive doubling: for
+// s = 8, 16, 32, every pair [[A, 0], [B, C]]^-1 = [[A^-1, 0], [-C^-1 B A^-1, C^-1]]
+// (T_c = B A^-1 into scratch columns [c s, c s + s), then X21 = -C^-1 T_c),
+// 8x8 tiles over the warps.
+__device__ void trtri64(const double* L, double* X, double* T) {
+  const int warp = threadIdx.x >> 5;
+  for (int s = 8; s < BB; s *= 2) {
+    const int per = (s / 8) * (s / 8), total = (BB / (2 * s)) * per;  // 8x8 tiles of all pairs
+    for (int tt = warp; tt < total; tt += NT / 32) {
+      const int c = tt / per, ti = (tt % per) / (s / 8), tj = tt % (s / 8);
+      const int a0 = 2 * c * s, b0 = a0 + s, r0 = 8 * ti, c0 = 8 * tj;
+      tile8([&](int i, int k) { return L[sw(b0 + r0 + i, a0 + k)]; },
+            [&](int k, int j) { return X[sw(a0 + k, a0 + c0 + j)]; },
+            [&](int i, int j, double v) { T[(r0 + i) * TLD + c * s + c0 + j] = v; }, s, 1.0);
     }
-    if (lane < 16) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) X[sw(q0 + i, q0 + jc)] = x[i];
-    }
-  }
-  __syncthreads();
-  // s = 16: pairs c = 0, 1 (a0 = 32 c, b0 = a0 + 16); 4 tiles each, one per warp
-  {
-    const int c = warp >> 2, ti = (warp >> 1) & 1, tj = warp & 1, a0 = 32 * c, b0 = a0 + 16;
-    const int r0 = 8 * ti, c0 = 8 * tj;
-    tile8([&](int i, int k) { return L[sw(b0 + r0 + i, a0 + k)]; },
-          [&](int k, int j) { return X[sw(a0 + k, a0 + c0 + j)]; },
-          [&](int i, int j, double v) { T[(16 * c + r0 + i) * TLD + c0 + j] = v; }, 16, 1.0);
     __syncthreads();
-    tile8([&](int i, int k) { return X[sw(b0 + r0 + i, b0 + k)]; },
-          [&](int k, int j) { return T[(16 * c + k) * TLD + c0 + j]; },
-          [&](int i, int j, double v) { X[sw(b0 + r0 + i, a0 + c0 + j)] = v; }, 16, -1.0);
+    for (int tt = warp; tt < total; tt += NT / 32) {
+      const int c = tt / per, ti = (tt % per) / (s / 8), tj = tt % (s / 8);
+      const int a0 = 2 * c * s, b0 = a0 + s, r0 = 8 * ti, c0 = 8 * tj;
+      tile8([&](int i, int k) { return X[sw(b0 + r0 + i, b0 + k)]; },
+            [&](int k, int j) { return T[k * TLD + c * s + c0 + j]; },
+            [&](int i, int j, double v) { X[sw(b0 + r0 + i, a0 + c0 + j)] = v; }, s, -1.0);
+    }
     __syncthreads();
   }
-  // s = 32: one pair (a0 = 0, b0 = 32); 16 tiles, two per warp
-  for (int tt = warp; tt < 16; tt += 8) {
-    const int r0 = 8 * (tt >> 2), c0 = 8 * (tt & 3);
-    tile8([&](int i, int k) { return L[sw(32 + r0 + i, k)]; }, [&](int k, int j) { return X[sw(k, c0 + j)]; },
-          [&](int i, int j, double v) { T[(r0 + i) * TLD + c0 + j] = v; }, 32, 1.0);
-  }
-  __syncthreads();
-  for (int tt = warp; tt < 16; tt += 8) {
-    const int r0 = 8 * (tt >> 2), c0 = 8 * (tt & 3);
-    tile8([&](int i, int k) { return X[sw(32 + r0 + i, 32 + k)]; }, [&](int k, int j) { return T[k * TLD + c0 + j]; },
-          [&](int i, int j, double v) { X[sw(32 + r0 + i, c0 + j)] = v; }, 32, -1.0);
-  }
-  __syncthreads();
 }
 
 // ---------------------------------------------------------------- block cache (per-thread replicated state)
@@ -387,14 +402,12 @@ __global__ void __launch_bounds__(NT, 2)
              int64_t id0, unsigned long long* prof) {
   extern __shared__ __align__(128) double dsm[];
   __shared__ BOp ops[MAXOPS];
-  __shared__ double dinv[BB];
   __shared__ int sfail, nops;
   double* const scr = dsm + NBUF * BUFD;
   const int64_t mat = blockIdx.x;
   const double* const a = A + mat * mstride;
   double* const x = X + mat * mstride;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1, m0 = 32 * wm, n0 = 16 * wn;
   if (tid == 0) {
     nops = gen_program(ops, nb);
     sfail = 1 << 30;
@@ -407,7 +420,7 @@ __global__ void __launch_bounds__(NT, 2)
 #pragma unroll
   for (int b = 0; b < NBUF; ++b) cc.tag[b] = 0, cc.use[b] = 0;
   cc.clk = 0;
-  double acc[4][2][2];
+  double acc[2][2][2][2];  // [slot][tile row][tile col][2]
   long long pt = 0, pacc[NPROF] = {};
   auto probe = [&](int c) {
     if constexpr (PROF) {
@@ -496,7 +509,8 @@ __global__ void __launch_bounds__(NT, 2)
         else if (c == r && gr + r >= n) S[sw(r, c)] = 1.0;
       }
       __syncthreads();
-      factor64<PROF>(S, dinv, &sfail, pacc);
+      double* Xs = buf(bb);
+      factor64<PROF>(S, Xs, &sfail, pacc);
       probe(2);
       if (sfail < (1 << 30)) {
         if (tid == 0) atomicMin(fail, ((unsigned long long)(id0 + mat) << 32) | (unsigned)(gr + sfail));
@@ -504,8 +518,7 @@ __global__ void __launch_bounds__(NT, 2)
         flush();
         return;
       }
-      double* Xs = buf(bb);
-      trtri64(S, Xs, scr, dinv);
+      trtri64(S, Xs, scr);
       probe(3);
       for (int e = tid; e < BUFD; e += NT) {  // X_pp = Linv_pp (lower, zero upper)
         const int r = e >> 6, c = e & 63;
@@ -515,47 +528,49 @@ __global__ void __launch_bounds__(NT, 2)
       cc.set(bb, tagof(1, p, p));
       probe(4);
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)  // (no accumulation chain crosses a DIAG: acc is dead in it)
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      for (int q = 0; q < 16; ++q)  // (no accumulation chain crosses a DIAG: acc is dead in it)
+        (&acc[0][0][0][0])[2 * q] = (&acc[0][0][0][0])[2 * q + 1] = 0.0;
       continue;
     }
     const double* SA = buf(ba);
     const double* SB = buf(bb);
-    const bool skip = (op.flags & F_SKIPU) && n0 >= m0 + 32;  // warp tile entirely above the diagonal
+    int quad[2];
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl) quad[sl] = c_map[op.map][warp][sl];
     if (op.flags & (F_ZERO | F_NEGC)) {
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      for (int q = 0; q < 16; ++q) (&acc[0][0][0][0])[2 * q] = (&acc[0][0][0][0])[2 * q + 1] = 0.0;
     }
-    if (!skip) {
+    const int fl = op.flags & (F_TA | F_TB);
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl) {
+      if (quad[sl] < 0) continue;
+      const int qr = quad[sl] >> 2, qc = quad[sl] & 3;
       int k0 = 0, k1 = BB;
       switch (op.kr) {
-        case KR_LT_COL: k1 = n0 + 16; break;
-        case KR_LT_ROW: k1 = m0 + 32; break;
-        case KR_GE_COL: k0 = n0; break;
-        case KR_GE_ROW: k0 = m0; break;
-        case KR_GE_BOTH: k0 = max(m0, n0); break;
+        case KR_LT_COL: k1 = 16 * (qc + 1); break;
+        case KR_LT_ROW: k1 = 16 * (qr + 1); break;
+        case KR_GE_COL: k0 = 16 * qc; break;
+        case KR_GE_ROW: k0 = 16 * qr; break;
+        case KR_GE_BOTH: k0 = 16 * max(qr, qc); break;
         default: break;
       }
-      const int fl = op.flags & (F_TA | F_TB);
       if (fl == F_TB)
-        mma_blk<false, true>(SA, SB, k0, k1, acc);
+        mma_quad<false, true>(SA, SB, qr, qc, k0, k1, acc[sl]);
       else if (fl == F_TA)
-        mma_blk<true, false>(SA, SB, k0, k1, acc);
+        mma_quad<true, false>(SA, SB, qr, qc, k0, k1, acc[sl]);
       else
-        mma_blk<false, false>(SA, SB, k0, k1, acc);
+        mma_quad<false, false>(SA, SB, qr, qc, k0, k1, acc[sl]);
       if (op.flags & F_NEGC) {  // acc = A B - C  (sign -1 below gives C - A B)
         const double* C = base(op.ca);
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
+        for (int ti = 0; ti < 2; ++ti)
 #pragma unroll
-          for (int ni = 0; ni < 2; ++ni)
+          for (int tj = 0; tj < 2; ++tj)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int r = op.ci * BB + m0 + 8 * mi + g, c = op.cj * BB + n0 + 8 * ni + 2 * tg + e;
-              if (r < n && c < n) acc[mi][ni][e] -= C[(int64_t)r * n + c];
+              const int r = op.ci * BB + 16 * qr + 8 * ti + g, c = op.cj * BB + 16 * qc + 8 * tj + 2 * tg + e;
+              if (r < n && c < n) acc[sl][ti][tj][e] -= C[(int64_t)r * n + c];
             }
       }
     }
@@ -565,43 +580,47 @@ __global__ void __launch_bounds__(NT, 2)
     const double sg = (double)op.sg;
     const int to = tagof(1, op.oi, op.oj);
     cc.drop_tag(to);
-    if (op.flags & F_CACHE) {
+    if (op.flags & F_CACHE) {  // (cached results are full blocks: MAP_COL / MAP_ROW cover all 16 quads)
       __syncthreads();  // every warp is done reading this operation's operands
       const int v = cc.victim(next_mask);
       double* D = buf(v);
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
+      for (int sl = 0; sl < 2; ++sl)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni)
+        for (int ti = 0; ti < 2; ++ti)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) D[sw(m0 + 8 * mi + g, n0 + 8 * ni + 2 * tg + e)] = sg * acc[mi][ni][e];
+          for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              D[sw(16 * (quad[sl] >> 2) + 8 * ti + g, 16 * (quad[sl] & 3) + 8 * tj + 2 * tg + e)] =
+                  sg * acc[sl][ti][tj][e];
       cc.set(v, to);
     }
-    if (skip) {
-      probe(6);
-      continue;
-    }
     const int gr = op.oi * BB, gc = op.oj * BB;
+    const bool diag = op.oi == op.oj;
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+    for (int sl = 0; sl < 2; ++sl) {
+      if (quad[sl] < 0) continue;
 #pragma unroll
-      for (int ni = 0; ni < 2; ++ni)
+      for (int ti = 0; ti < 2; ++ti)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = m0 + 8 * mi + g, c = n0 + 8 * ni + 2 * tg + e;
-          if (gr + r >= n || gc + c >= n) continue;
-          const double v = sg * acc[mi][ni][e];
-          const bool diag = op.oi == op.oj;
-          if (op.st == ST_FULL) {
-            x[(int64_t)(gr + r) * n + gc + c] = v;
-          } else if (op.st == ST_LOWER) {
-            if (c <= r) x[(int64_t)(gr + r) * n + gc + c] = v;
-          } else {  // ST_SYM
-            if (diag && c > r) continue;
-            x[(int64_t)(gr + r) * n + gc + c] = v;
-            if (!(diag && c == r)) x[(int64_t)(gc + c) * n + gr + r] = v;
+        for (int tj = 0; tj < 2; ++tj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = 16 * (quad[sl] >> 2) + 8 * ti + g, c = 16 * (quad[sl] & 3) + 8 * tj + 2 * tg + e;
+            if (gr + r >= n || gc + c >= n) continue;
+            const double v = sg * acc[sl][ti][tj][e];
+            if (op.st == ST_FULL) {
+              x[(int64_t)(gr + r) * n + gc + c] = v;
+            } else if (op.st == ST_LOWER) {
+              if (c <= r) x[(int64_t)(gr + r) * n + gc + c] = v;
+            } else {  // ST_SYM
+              if (diag && c > r) continue;
+              x[(int64_t)(gr + r) * n + gc + c] = v;
+              if (!(diag && c == r)) x[(int64_t)(gc + c) * n + gr + r] = v;
+            }
           }
-        }
+    }
     probe(6);
   }
   flush();
