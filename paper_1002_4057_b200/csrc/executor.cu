@@ -735,136 +735,113 @@ __device__ __forceinline__ void warp_inv16(const double (&r)[16], double (&x)[16
   }
 }
 
-// Warp 0: factor the 16x16 diagonal block at (p0, p0) of S in place (lane
-// i & 15 holds row i; right-looking, shuffles), 1 / L[k][k] -> dinv[0..15],
-// failing pivots (kernels.py:68-71) folded into ctl.scan_min.
-__device__ __noinline__ void factor16(double* S, int p0, double* dinv, SmemCtl& ctl) {
-  const int lane = threadIdx.x & 31, i = lane & 15;
-  double r[16];
+// Cholesky of the lower 8x8 block at (p0, p0) of S in registers
+// (right-looking; kernels.py:68-71 failure test: not d > 0, or d non-finite):
+// l = the factor, x = l^-1 (x[i][i] = 1 / l[i][i]). Returns the first failing
+// pivot or -1.
+__device__ __forceinline__ int chol8_inv(const double* S, int p0, double (&l)[8][8], double (&x)[8][8]) {
+  double il[8];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) r[j] = j <= i ? S[(p0 + i) * SLD + p0 + j] : 0.0;
-  unsigned badmask = 0;
-  double my_il = 1.0;
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const double piv = __shfl_sync(FULL, r[k], k);
-    const bool bad = !(piv > 0.0) || !isfinite(piv);
-    badmask |= bad ? (1u << k) : 0u;
-    const double il = bad ? 1.0 : rsqrt(piv);  // every lane, no broadcast needed
-    const double l = bad ? 1.0 : piv * il;
-    my_il = (i == k) ? il : my_il;
-    r[k] = (i == k) ? l : (i > k ? r[k] * il : r[k]);
+    for (int j = 0; j <= i; ++j) l[i][j] = S[(p0 + i) * SLD + p0 + j];
+  int bad = -1;
 #pragma unroll
-    for (int j = 1; j < 16; ++j) {  // constant trip count: r[] stays in registers
-      if (j > k) {
-        const double v = __shfl_sync(FULL, r[k], j);
-        r[j] = (i >= j) ? fma(-r[k], v, r[j]) : r[j];
-      }
+  for (int k = 0; k < 8; ++k) {
+    const double d = l[k][k];
+    const bool b = !(d > 0.0) || !isfinite(d);
+    bad = (b && bad < 0) ? k : bad;
+    il[k] = b ? 1.0 : rsqrt(d);
+    l[k][k] = b ? 1.0 : d * il[k];
+#pragma unroll
+    for (int i = k + 1; i < 8; ++i) l[i][k] *= il[k];
+#pragma unroll
+    for (int j = k + 1; j < 8; ++j)
+#pragma unroll
+      for (int i = j; i < 8; ++i) l[i][j] = fma(-l[i][k], l[j][k], l[i][j]);
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    x[c][c] = il[c];
+#pragma unroll
+    for (int i = c + 1; i < 8; ++i) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = c; k < i; ++k) t = fma(l[i][k], x[k][c], t);
+      x[i][c] = -t * il[i];
     }
   }
-  if (lane == 0 && badmask) atomicMin(&ctl.scan_min, p0 + __ffs(badmask) - 1);
-  if (lane < 16) {
-    dinv[i] = my_il;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) S[(p0 + i) * SLD + p0 + j] = j <= i ? r[j] : 0.0;
-  }
+  return bad;
 }
 
-// Panel rows below the diagonal block at p0: v L_PP^T = a by forward
-// substitution, one row per thread of [t0, t0 + nt).
-__device__ __forceinline__ void panel_subst(double* S, int p0, const double* dinv, int t0, int nt) {
-  for (int row = p0 + 16 + t0; row < BLK; row += nt) {
-    double v[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = S[row * SLD + p0 + k];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      double w0 = v[j], w1 = 0.0;
-#pragma unroll
-      for (int k = 0; k < 15; ++k) {  // constant trip count: v[] stays in registers
-        if (k < j) {
-          if (k & 1)
-            w1 -= v[k] * S[(p0 + j) * SLD + p0 + k];
-          else
-            w0 -= v[k] * S[(p0 + j) * SLD + p0 + k];
-        }
-      }
-      v[j] = (w0 + w1) * dinv[j];
-    }
-#pragma unroll
-    for (int k = 0; k < 16; ++k) S[row * SLD + p0 + k] = v[k];
-  }
-}
-
-// Trailing update by panel P of the 16x16 blocks (I, J), ja <= J <= jb,
-// J <= I <= 7: A[I][J] -= L[I][P] L[J][P]^T, 4x4 micro-tiles (strided
-// columns: conflict-free loads) over threads [t0, t0 + nt).
-__device__ __noinline__ void trailing16(double* S, int P, int ja, int jb, int t0, int nt) {
-  const int p0 = 16 * P;
-  int nblk = 0;
-  for (int J = ja; J <= jb; ++J) nblk += 8 - J;
-  for (int tt = t0; tt < 16 * nblk; tt += nt) {
-    int blk = tt >> 4, J = ja;
-    while (blk >= 8 - J) {
-      blk -= 8 - J;
-      ++J;
-    }
-    const int I = J + blk, mt = tt & 15;
-    const int r0 = 16 * I + 4 * (mt >> 2), c0 = 16 * J + (mt & 3);
-    double acc[4][4] = {};
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      double a[4], b[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a[q] = S[(r0 + q) * SLD + p0 + k];
-        b[q] = S[(c0 + 4 * q) * SLD + p0 + k];
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int w = 0; w < 4; ++w) acc[q][w] += a[q] * b[w];
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int w = 0; w < 4; ++w) S[(r0 + q) * SLD + c0 + 4 * w] -= acc[q][w];
-  }
-}
-
-// In-place Cholesky of the lower 128x128 block in S (right-looking, 16-wide
-// panels, look-ahead): after panel P's substitution and the update of
-// column block P + 1, warp 0 factors panel P + 1 while warps 1-7 apply panel
-// P to the rest of the trailing matrix. Returns the first failing pivot
-// (kernels.py:68-71) or -1.
+// In-place Cholesky of the lower 128x128 block in S over 8-wide panels: warps
+// 0-3 factor the panel's 8x8 diagonal block redundantly in registers
+// (chol8_inv: the column chain has no shuffles or shared-memory round trips)
+// and each solves one panel row below it by the block inverse; the trailing
+// lower 8x8 tiles are updated on DMMA by all 8 warps. Returns the first
+// failing pivot (kernels.py:68-71) or -1.
 __device__ int block_potrf(double* S, SmemCtl& ctl) {
-  const int tid = threadIdx.x, warp = tid >> 5;
-  double* dinv = S + BLK * SLD;  // 1 / L[k][k] of the current panel
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
   if (tid == 0) ctl.scan_min = 1 << 30;
-  cons_bar();
   long long tq = clock64();
   auto probe = [&](int k) {
     const long long now = clock64();
     if (tid == 0) ctl.dbg2[k] += now - tq;
     tq = now;
   };
-  if (warp == 0) factor16(S, 0, dinv, ctl);
-  cons_bar();
-  probe(0);
-  for (int P = 0; P < 8; ++P) {
-    panel_subst(S, 16 * P, dinv, tid, 256);
+  double* stage = S + BLK * SLD;  // the factored 8x8 diagonal block until every reader is past the barrier
+  for (int P = 0; P < BLK / 8; ++P) {
+    const int p0 = 8 * P;
+    if (warp < 4) {
+      double l[8][8], x[8][8];
+      const int bad = chol8_inv(S, p0, l, x);
+      if (tid == 0) {
+        if (bad >= 0) atomicMin(&ctl.scan_min, p0 + bad);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) stage[8 * i + j] = j <= i ? l[i][j] : 0.0;
+      }
+      const int q = p0 + 8 + tid;  // panel row: v = a L^-T = a x^T
+      if (q < BLK) {
+        double av[8], v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) av[k] = S[q * SLD + p0 + k];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          double t = 0.0;
+#pragma unroll
+          for (int k = 0; k <= c; ++k) t = fma(av[k], x[c][k], t);
+          v[c] = t;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) S[q * SLD + p0 + k] = v[k];
+      }
+    }
+    cons_bar();
+    probe(0);
+    if (tid < 64) S[(p0 + (tid >> 3)) * SLD + p0 + (tid & 7)] = stage[tid];
+    if (P == BLK / 8 - 1) break;
+    // trailing lower 8x8 tiles of rows / columns [p0 + 8, 128): -= L_P L_P^T (K = 8)
+    const int t0 = p0 + 8, nt8 = BLK / 8 - 1 - P, ntiles = nt8 * (nt8 + 1) / 2;
+    for (int tt = warp; tt < ntiles; tt += NCONS_WARPS) {
+      int ti = 0, rem = tt;
+      while (rem > ti) {
+        rem -= ti + 1;
+        ++ti;
+      }
+      const int r0 = t0 + 8 * ti, c0 = t0 + 8 * rem;
+      double acc[2] = {S[(r0 + g) * SLD + c0 + 2 * tg], S[(r0 + g) * SLD + c0 + 2 * tg + 1]};
+#pragma unroll
+      for (int k = 0; k < 8; k += 4)
+        dmma(acc, -S[(r0 + g) * SLD + p0 + k + tg], S[(c0 + g) * SLD + p0 + k + tg]);
+      S[(r0 + g) * SLD + c0 + 2 * tg] = acc[0];
+      S[(r0 + g) * SLD + c0 + 2 * tg + 1] = acc[1];
+    }
     cons_bar();
     probe(1);
-    if (P == 7) break;
-    trailing16(S, P, P + 1, P + 1, tid, 256);  // column block P + 1: the next panel
-    cons_bar();
-    if (warp == 0)
-      factor16(S, 16 * (P + 1), dinv, ctl);
-    else if (P + 2 <= 7)
-      trailing16(S, P, P + 2, 7, tid - 32, 224);
-    cons_bar();
-    probe(2);
   }
+  cons_bar();
   const int f = ctl.scan_min;
   return f < (1 << 30) ? f : -1;
 }
