@@ -19,12 +19,13 @@
 //     output = symmetrize_lower(to_dense(...)), tile_matrix.py:102-119)
 //
 // The matrix itself is the working store (X's lower blocks, L2-resident while
-// the CTA works on it). Operand blocks are staged in three 32 KB shared-memory
-// buffers managed as a tiny write-through block cache: the operands of the
-// next operation are prefetched with cp.async while the current one runs,
-// results a later operation reads are inserted as they are stored. Two CTAs
-// share an SM (~106 KB smem each), so one matrix's latency-bound diagonal
-// chain overlaps the other's DMMA work.
+// the CTA works on it). Operand blocks are staged with cp.async in two 32 KB
+// shared-memory buffers that remember which block they hold (an operand the
+// previous operation already loaded is not reloaded). Each CTA has 4 warps and
+// ~66 KB of shared memory, so three matrices are resident per SM: one CTA's
+// exposed loads and latency-bound diagonal chains overlap the others' DMMA
+// work. Each warp owns four 16x16 output quads chosen (c_map) so that the
+// triangular K ranges of TRSM / TRMM / SYRK-type products balance over warps.
 //
 // Products run on the FP64 tensor pipe (mma.sync m8n8k4 -> DMMA.8x8x4; there
 // is no f64 tcgen05 kind on sm_100a). Smem blocks are 64x64 row-major with an
@@ -48,13 +49,11 @@ int set_error(int code, const std::string& msg);
 namespace bsm {
 
 constexpr int BB = 64;            // block order
-constexpr int NT = 256;           // 8 warps
+constexpr int NT = 128;           // 4 warps; 3 CTAs per SM
 constexpr int NBMAX = 4;          // n <= 256
-constexpr int MAXOPS = 64;        // program length for nbk = 4 is 56
+constexpr int MAXOPS = 56;        // program length for nbk = 4
 constexpr int BUFD = BB * BB;     // doubles per smem block buffer
-constexpr int NBUF = 3;
-constexpr int TLD = 36;           // row stride of the 32x32 TRTRI scratch
-constexpr int SMEM_DYN = NBUF * BUFD * 8 + 32 * TLD * 8;
+constexpr int SMEM_DYN = 2 * BUFD * 8;  // two block buffers
 
 enum : int8_t { OP_DIAG = 1, OP_MMA = 2 };
 // K range of a triangular operand per 16x16 output quad (qr, qc):
@@ -62,7 +61,7 @@ enum : int8_t { OP_DIAG = 1, OP_MMA = 2 };
 // GE_BOTH k >= 16 max(qr, qc)
 enum : int8_t { KR_FULL, KR_LT_COL, KR_LT_ROW, KR_GE_COL, KR_GE_ROW, KR_GE_BOTH };
 enum : int8_t { ST_NONE = 0, ST_FULL = 1, ST_LOWER = 2, ST_SYM = 3 };
-enum : int8_t { F_ZERO = 1, F_NEGC = 2, F_CACHE = 4, F_SKIPU = 8, F_TA = 16, F_TB = 32 };
+enum : int8_t { F_ZERO = 1, F_NEGC = 2, F_SKIPU = 8, F_TA = 16, F_TB = 32 };
 
 // One block operation; arrays: 0 = A (input), 1 = X (working store / output).
 struct BOp {
@@ -73,18 +72,9 @@ struct BOp {
   int8_t map, pad0, pad1, pad2;
 };
 
-// Output quads (16x16) of a warp: two slots, (qr << 2 | qc) or -1. The maps
-// balance the DMMA work of triangular K ranges over the 8 warps; every
-// operation of an accumulation chain uses the chain's map.
+// Output quads (16x16) of a warp; every operation of an accumulation chain
+// uses the chain's map (see c_map).
 enum : int8_t { MAP_COL = 0, MAP_ROW = 1, MAP_LOWER = 2 };
-__constant__ int8_t c_map[3][8][2] = {
-    // MAP_COL: quad columns qc and 3 - qc in one quad row (K ranges by column: 16(qc+1) + 16(4-qc))
-    {{0, 3}, {4, 7}, {8, 11}, {12, 15}, {1, 2}, {5, 6}, {9, 10}, {13, 14}},
-    // MAP_ROW: quad rows qr and 3 - qr in one quad column
-    {{0, 12}, {1, 13}, {2, 14}, {3, 15}, {4, 8}, {5, 9}, {6, 10}, {7, 11}},
-    // MAP_LOWER: the 10 lower quads; K >= 16 qr work 4,3,3,3,3,2,1,1 (x16)
-    {{0, -1}, {4, -1}, {5, -1}, {8, 12}, {9, 13}, {10, -1}, {14, -1}, {15, -1}},
-};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -128,7 +118,7 @@ __device__ int gen_program(BOp* ops, int nb) {
     d.aa = (int8_t)src, d.ai = (int8_t)p, d.aj = (int8_t)p, d.oi = (int8_t)p, d.oj = (int8_t)p;
     ops[k++] = d;
     for (int i = p + 1; i < nb; ++i)  // L_ip = A_ip Linv_pp^T
-      mma(src, i, p, 1, p, p, F_ZERO | F_CACHE | F_TB, KR_LT_COL, ST_FULL, i, p, 1);
+      mma(src, i, p, 1, p, p, F_ZERO | F_TB, KR_LT_COL, ST_FULL, i, p, 1);
     for (int i = p + 1; i < nb; ++i)  // A_ij -= L_ip L_jp^T
       for (int j = p + 1; j <= i; ++j)
         mma(1, i, p, 1, j, p, F_NEGC | F_TB | (i == j ? F_SKIPU : 0), KR_FULL, i == j ? ST_LOWER : ST_FULL, i, j,
@@ -140,8 +130,7 @@ __device__ int gen_program(BOp* ops, int nb) {
       for (int q = j; q < i; ++q)  // T = sum_q L_iq X_qj (X_jj lower: K >= column)
         mma(1, i, q, 1, q, j, q == j ? F_ZERO : 0, q == j ? KR_GE_COL : KR_FULL, q == i - 1 ? ST_FULL : ST_NONE,
             i, j, 1);
-      ops[k - 1].flags |= F_CACHE;
-      mma(1, i, i, 1, i, j, F_ZERO | F_CACHE, KR_LT_ROW, ST_FULL, i, j, -1);  // X_ij = -X_ii T
+      mma(1, i, i, 1, i, j, F_ZERO, KR_LT_ROW, ST_FULL, i, j, -1);  // X_ij = -X_ii T
     }
   // step 3: A^-1 = X^T X (LAUUM), lower blocks with their mirrors
   for (int i = 0; i < nb; ++i)
@@ -152,27 +141,6 @@ __device__ int gen_program(BOp* ops, int nb) {
         if (i != j) ops[k - 1].map = MAP_ROW;  // the chain's map (its first operation is GE_ROW)
       }
   return k;
-}
-
-// ---------------------------------------------------------------- block I/O
-// global block (bi, bj) of an n x n row-major matrix -> swizzled smem buffer;
-// zero outside the matrix. One cp.async group per call.
-__device__ __forceinline__ void load_blk(double* S, const double* G, int n, int bi, int bj) {
-  const int r0 = bi * BB, c0 = bj * BB;
-  if ((n & 1) == 0) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int idx = threadIdx.x + NT * u, r = idx >> 5, c = (idx & 31) * 2;
-      const bool ok = r0 + r < n && c0 + c < n;
-      cp16(S + sw(r, c), ok ? G + (int64_t)(r0 + r) * n + c0 + c : G, ok ? 16 : 0);
-    }
-  } else {
-    for (int e = threadIdx.x; e < BUFD; e += NT) {
-      const int r = e >> 6, c = e & 63;
-      S[sw(r, c)] = (r0 + r < n && c0 + c < n) ? G[(int64_t)(r0 + r) * n + c0 + c] : 0.0;
-    }
-  }
-  cp_commit();
 }
 
 // ---------------------------------------------------------------- DMMA quad product
@@ -244,23 +212,55 @@ __device__ __forceinline__ int chol8_inv(const double* S, int p0, double (&x)[8]
   return bad;
 }
 
-// In-place Cholesky of the lower 64x64 block in S over 8-wide panels: warps
-// 0-1 factor the panel's 8x8 diagonal block redundantly in registers
-// (chol8_inv: no shuffles on the column chain) and each solves one panel row
-// below it by the block inverse; the trailing lower 8x8 tiles are updated on
-// DMMA. The inverses of the eight 8x8 diagonal blocks go to X (zeroed here)
-// for trtri64. The strict upper part of S must be zero on entry.
-template <bool PROF>
-__device__ void factor64(double* S, double* X, int* fail, long long* pacc) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
-  long long t0 = PROF ? clock64() : 0;
-  auto probe = [&](int c) {
-    if constexpr (PROF) {
-      const long long now = clock64();
-      pacc[c] += now - t0;
-      t0 = now;
+// One warp: 8x8 tile D(i, j) = sgn * sum_{k < K} A(i, k) B(k, j).
+template <class FA, class FB, class FD>
+__device__ __forceinline__ void tile8(FA A, FB B, FD D, int K, double sgn) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3;
+  double acc[2] = {0.0, 0.0};
+  for (int k = 0; k < K; k += 4) dmma(acc, A(g, k + tg), B(k + tg, g));
+  D(g, 2 * tg, sgn * acc[0]);
+  D(g, 2 * tg + 1, sgn * acc[1]);
+}
+
+// ---------------------------------------------------------------- kernel pieces
+__device__ __forceinline__ int tagof(int arr, int i, int j) { return 1 + ((arr << 8) | (i << 4) | j); }
+
+// Three CTAs per SM, 4 warps each, two 32 KB block buffers (no scratch: the
+// TRTRI products stage through the zero upper triangle of the inverse). Each
+// warp owns four 16x16 output quads; with three matrices resident per SM one
+// CTA's exposed loads and diagonal chains overlap the others' DMMA work.
+// quads (qr << 2 | qc) of warp w: MAP_COL = quad row w, MAP_ROW = quad column
+// w, MAP_LOWER = the 10 lower quads (K >= 16 qr work per warp 6,6,6,2 x16)
+__constant__ int8_t c_map[3][4][4] = {
+    {{0, 1, 2, 3}, {4, 5, 6, 7}, {8, 9, 10, 11}, {12, 13, 14, 15}},
+    {{0, 4, 8, 12}, {1, 5, 9, 13}, {2, 6, 10, 14}, {3, 7, 11, 15}},
+    {{0, 12, 13, -1}, {4, 5, -1, -1}, {8, 9, 10, -1}, {14, 15, -1, -1}},
+};
+
+__device__ __forceinline__ void load_blk(double* S, const double* G, int n, int bi, int bj) {
+  const int r0 = bi * BB, c0 = bj * BB;
+  if ((n & 1) == 0) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int idx = threadIdx.x + NT * u, r = idx >> 5, c = (idx & 31) * 2;
+      const bool ok = r0 + r < n && c0 + c < n;
+      cp16(S + sw(r, c), ok ? G + (int64_t)(r0 + r) * n + c0 + c : G, ok ? 16 : 0);
     }
-  };
+  } else {
+    for (int e = threadIdx.x; e < BUFD; e += NT) {
+      const int r = e >> 6, c = e & 63;
+      S[sw(r, c)] = (r0 + r < n && c0 + c < n) ? G[(int64_t)(r0 + r) * n + c0 + c] : 0.0;
+    }
+  }
+  cp_commit();
+}
+
+// In-place Cholesky of the lower 64x64 block in S (8-wide panels, 4 warps):
+// warps 0-1 factor the 8x8 diagonal block in registers and solve the panel
+// rows below it; all warps update the trailing lower 8x8 tiles on DMMA. The
+// 8x8 diagonal inverses go to X (zeroed here). Strict upper of S zero on entry.
+__device__ void factor64(double* S, double* X, int* fail) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
   for (int e = tid; e < BUFD; e += NT) X[e] = 0.0;
   for (int P = 0; P < 8; ++P) {
     const int p0 = 8 * P;
@@ -274,7 +274,7 @@ __device__ void factor64(double* S, double* X, int* fail, long long* pacc) {
 #pragma unroll
           for (int j = 0; j <= i; ++j) X[sw(p0 + i, p0 + j)] = x[i][j];
       }
-      const int q = p0 + 8 + tid;  // panel row: v = a L^-T = a x^T
+      const int q = p0 + 8 + tid;
       if (q < BB) {
         double a[8], v[8];
 #pragma unroll
@@ -291,9 +291,7 @@ __device__ void factor64(double* S, double* X, int* fail, long long* pacc) {
       }
     }
     __syncthreads();
-    probe(8);
     if (P == 7) break;
-    // trailing lower 8x8 tiles of rows / columns [p0 + 8, 64): -= L_P L_P^T (K = 8)
     const int t0r = p0 + 8, nt8 = 7 - P, ntiles = nt8 * (nt8 + 1) / 2;
     for (int tt = warp; tt < ntiles; tt += NT / 32) {
       int ti = 0, rem = tt;
@@ -309,101 +307,48 @@ __device__ void factor64(double* S, double* X, int* fail, long long* pacc) {
       S[sw(r0 + g, c0 + 2 * tg + 1)] = acc[1];
     }
     __syncthreads();
-    probe(10);
   }
 }
 
-// One warp: 8x8 tile D(i, j) = sgn * sum_{k < K} A(i, k) B(k, j).
-template <class FA, class FB, class FD>
-__device__ __forceinline__ void tile8(FA A, FB B, FD D, int K, double sgn) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3;
-  double acc[2] = {0.0, 0.0};
-  for (int k = 0; k < K; k += 4) dmma(acc, A(g, k + tg), B(k + tg, g));
-  D(g, 2 * tg, sgn * acc[0]);
-  D(g, 2 * tg + 1, sgn * acc[1]);
-}
-
-// X = L^-1 for the lower 64x64 L (strict upper zero) given the inverses of its
-// 8x8 diagonal blocks in X (rest of X zero), by recursive doubling: for
-// s = 8, 16, 32, every pair [[A, 0], [B, C]]^-1 = [[A^-1, 0], [-C^-1 B A^-1, C^-1]]
-// (T_c = B A^-1 into scratch columns [c s, c s + s), then X21 = -C^-1 T_c),
-// 8x8 tiles over the warps.
-__device__ void trtri64(const double* L, double* X, double* T) {
-  const int warp = threadIdx.x >> 5;
+// X = L^-1 (64x64) by recursive doubling from the 8x8 diagonal inverses in X;
+// T_c = B A^-1 of pair c at level s is staged in X's strictly upper block
+// [a0, a0 + s) x [b0, b0 + s) of the pair and zeroed after use.
+__device__ void trtri64(const double* L, double* X) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int s = 8; s < BB; s *= 2) {
-    const int per = (s / 8) * (s / 8), total = (BB / (2 * s)) * per;  // 8x8 tiles of all pairs
+    const int per = (s / 8) * (s / 8), total = (BB / (2 * s)) * per;
     for (int tt = warp; tt < total; tt += NT / 32) {
       const int c = tt / per, ti = (tt % per) / (s / 8), tj = tt % (s / 8);
       const int a0 = 2 * c * s, b0 = a0 + s, r0 = 8 * ti, c0 = 8 * tj;
       tile8([&](int i, int k) { return L[sw(b0 + r0 + i, a0 + k)]; },
             [&](int k, int j) { return X[sw(a0 + k, a0 + c0 + j)]; },
-            [&](int i, int j, double v) { T[(r0 + i) * TLD + c * s + c0 + j] = v; }, s, 1.0);
+            [&](int i, int j, double v) { X[sw(a0 + r0 + i, b0 + c0 + j)] = v; }, s, 1.0);
     }
     __syncthreads();
     for (int tt = warp; tt < total; tt += NT / 32) {
       const int c = tt / per, ti = (tt % per) / (s / 8), tj = tt % (s / 8);
       const int a0 = 2 * c * s, b0 = a0 + s, r0 = 8 * ti, c0 = 8 * tj;
       tile8([&](int i, int k) { return X[sw(b0 + r0 + i, b0 + k)]; },
-            [&](int k, int j) { return T[k * TLD + c * s + c0 + j]; },
+            [&](int k, int j) { return X[sw(a0 + k, b0 + c0 + j)]; },
             [&](int i, int j, double v) { X[sw(b0 + r0 + i, a0 + c0 + j)] = v; }, s, -1.0);
     }
     __syncthreads();
+    for (int e = threadIdx.x; e < (BB / (2 * s)) * s * s; e += NT) {  // clear the staged T_c
+      const int c = e / (s * s), i = (e % (s * s)) / s, j = e % s;
+      X[sw(2 * c * s + i, 2 * c * s + s + j)] = 0.0;
+    }
+    __syncthreads();
   }
+  (void)lane;
 }
 
-// ---------------------------------------------------------------- block cache (per-thread replicated state)
-struct Cache {
-  int tag[NBUF];
-  unsigned use[NBUF];
-  unsigned clk;
-  __device__ __forceinline__ int find(int t) const {
-    int f = -1;
-#pragma unroll
-    for (int b = 0; b < NBUF; ++b) f = (t && tag[b] == t) ? b : f;
-    return f;
-  }
-  // empty buffer first, else least recently used; -1 if all excluded
-  __device__ __forceinline__ int victim(unsigned excl) const {
-    int best = -1;
-    unsigned bu = 0xffffffffu;
-#pragma unroll
-    for (int b = 0; b < NBUF; ++b) {
-      if (excl & (1u << b)) continue;
-      const unsigned u = tag[b] ? use[b] : 0u;
-      if (best < 0 || u < bu) best = b, bu = u;
-    }
-    return best;
-  }
-  __device__ __forceinline__ void set(int b, int t) {
-#pragma unroll
-    for (int q = 0; q < NBUF; ++q)
-      if (q == b) tag[q] = t, use[q] = ++clk;
-  }
-  __device__ __forceinline__ void touch(int b) {
-#pragma unroll
-    for (int q = 0; q < NBUF; ++q)
-      if (q == b) use[q] = ++clk;
-  }
-  __device__ __forceinline__ void drop_tag(int t) {
-#pragma unroll
-    for (int q = 0; q < NBUF; ++q)
-      if (tag[q] == t) tag[q] = 0;
-  }
-};
-__device__ __forceinline__ int tagof(int arr, int i, int j) { return 1 + ((arr << 8) | (i << 4) | j); }
-
-// ---------------------------------------------------------------- kernel
-// PROF: thread 0 accumulates clock64 spans per phase into prof[NPROF] (one
-// atomicAdd per CTA at exit); TINV_BSMALL_PROF=1 selects this instantiation.
-constexpr int NPROF = 13;  // wait, prefetch, factor, trtri, diag-store, mma, store, ops, f16, subst, trail, pf-issue, pf-count
 template <bool PROF>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, 3)
     k_bsmall(const double* __restrict__ A, double* X, int n, int nb, int64_t mstride, unsigned long long* fail,
-             int64_t id0, unsigned long long* prof) {
+              int64_t id0, unsigned long long* prof) {
   extern __shared__ __align__(128) double dsm[];
   __shared__ BOp ops[MAXOPS];
   __shared__ int sfail, nops;
-  double* const scr = dsm + NBUF * BUFD;
   const int64_t mat = blockIdx.x;
   const double* const a = A + mat * mstride;
   double* const x = X + mat * mstride;
@@ -416,12 +361,9 @@ __global__ void __launch_bounds__(NT, 2)
   const int nop = nops;
   auto buf = [&](int b) { return dsm + b * BUFD; };
   auto base = [&](int arr) -> const double* { return arr ? x : a; };
-  Cache cc;
-#pragma unroll
-  for (int b = 0; b < NBUF; ++b) cc.tag[b] = 0, cc.use[b] = 0;
-  cc.clk = 0;
-  double acc[2][2][2][2];  // [slot][tile row][tile col][2]
-  long long pt = 0, pacc[NPROF] = {};
+  int tag0 = 0, tag1 = 0;  // global block held by buffer 0 / 1 (0: none)
+  double acc[4][2][2][2];
+  long long pt = 0, pacc[8] = {};
   auto probe = [&](int c) {
     if constexpr (PROF) {
       const long long now = clock64();
@@ -429,121 +371,73 @@ __global__ void __launch_bounds__(NT, 2)
       pt = now;
     }
   };
-  auto flush = [&]() {
-    if constexpr (PROF) {
-      if (tid == 0)
-        for (int c = 0; c < NPROF; ++c) atomicAdd(prof + c, (unsigned long long)pacc[c]);
-    }
-  };
   probe(-1);
-
   for (int o = 0; o < nop; ++o) {
     const BOp op = ops[o];
-    if constexpr (PROF) pacc[7] += 1;
-    // 1. operands not prefetched: load now (exposed). The barrier orders the
-    // previous operation's global stores and smem reads before the loads.
-    int ba = -1, bb = -1;
     if (op.type == OP_DIAG) {
       __syncthreads();
-      ba = cc.victim(0);
-      bb = cc.victim(1u << ba);
-      load_blk(buf(ba), base(op.aa), n, op.ai, op.aj);
-      cc.set(ba, 0);  // factored in place: not a copy of any global block
-    } else {
-      const int ta = tagof(op.aa, op.ai, op.aj), tb = tagof(op.ba, op.bi, op.bj);
-      ba = cc.find(ta);
-      bb = tb == ta ? ba : cc.find(tb);
-      if (ba < 0 || bb < 0) __syncthreads();
-      if (ba < 0) {
-        ba = cc.victim(bb >= 0 ? 1u << bb : 0u);
-        load_blk(buf(ba), base(op.aa), n, op.ai, op.aj);
-        cc.set(ba, ta);
-        if (tb == ta) bb = ba;
-      }
-      if (bb < 0) {
-        bb = cc.victim(1u << ba);
-        load_blk(buf(bb), base(op.ba), n, op.bi, op.bj);
-        cc.set(bb, tb);
-      }
-      cc.touch(ba);
-      cc.touch(bb);
-    }
-    cp_wait_all();
-    __syncthreads();
-    probe(0);
-    // 2. prefetch the next operation's operands into buffers this one does not use
-    unsigned next_mask = 0;
-    if (o + 1 < nop && ops[o + 1].type == OP_MMA) {
-      const BOp nx = ops[o + 1];
-      const int outt = (op.type == OP_DIAG || op.st != ST_NONE) ? tagof(1, op.oi, op.oj) : 0;
-      unsigned excl = (1u << ba) | (1u << bb);
-      const int t2[2] = {tagof(nx.aa, nx.ai, nx.aj), tagof(nx.ba, nx.bi, nx.bj)};
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int f = (t2[q] == outt) ? -1 : cc.find(t2[q]);
-        if (f >= 0) next_mask |= 1u << f;
-      }
-      excl |= next_mask;
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        if (t2[q] == outt || (q == 1 && t2[1] == t2[0]) || cc.find(t2[q]) >= 0) continue;
-        const int v = cc.victim(excl);
-        if (v < 0) break;
-        probe(1);
-        load_blk(buf(v), base(q ? nx.ba : nx.aa), n, q ? nx.bi : nx.ai, q ? nx.bj : nx.aj);
-        probe(11);
-        if constexpr (PROF) pacc[12] += 1;
-        cc.set(v, t2[q]);
-        excl |= 1u << v;
-        next_mask |= 1u << v;
-      }
-    }
-    probe(1);
-    // 3. the operation
-    if (op.type == OP_DIAG) {
-      double* S = buf(ba);
+      double* S = buf(0);
+      double* Xs = buf(1);
       const int p = op.ai, gr = p * BB;
+      load_blk(S, base(op.aa), n, p, p);
+      cp_wait_all();
+      __syncthreads();
+      probe(0);
       for (int e = tid; e < BUFD; e += NT) {  // lower part only; identity on the padded diagonal
         const int r = e >> 6, c = e & 63;
         if (c > r) S[sw(r, c)] = 0.0;
         else if (c == r && gr + r >= n) S[sw(r, c)] = 1.0;
       }
       __syncthreads();
-      double* Xs = buf(bb);
-      factor64<PROF>(S, Xs, &sfail, pacc);
-      probe(2);
+      factor64(S, Xs, &sfail);
       if (sfail < (1 << 30)) {
         if (tid == 0) atomicMin(fail, ((unsigned long long)(id0 + mat) << 32) | (unsigned)(gr + sfail));
-        cp_wait_all();
-        flush();
         return;
       }
-      trtri64(S, Xs, scr);
-      probe(3);
-      for (int e = tid; e < BUFD; e += NT) {  // X_pp = Linv_pp (lower, zero upper)
+      trtri64(S, Xs);
+      for (int e = tid; e < BUFD; e += NT) {
         const int r = e >> 6, c = e & 63;
         if (gr + r < n && gr + c < n) x[(int64_t)(gr + r) * n + gr + c] = Xs[sw(r, c)];
       }
-      cc.drop_tag(tagof(1, p, p));
-      cc.set(bb, tagof(1, p, p));
-      probe(4);
+      tag0 = 0;
+      tag1 = tagof(1, p, p);
 #pragma unroll
-      for (int q = 0; q < 16; ++q)  // (no accumulation chain crosses a DIAG: acc is dead in it)
-        (&acc[0][0][0][0])[2 * q] = (&acc[0][0][0][0])[2 * q + 1] = 0.0;
+      for (int q = 0; q < 32; ++q) (&acc[0][0][0][0])[2 * q] = (&acc[0][0][0][0])[2 * q + 1] = 0.0;
+      probe(1);
       continue;
     }
+    const int ta = tagof(op.aa, op.ai, op.aj), tb = tagof(op.ba, op.bi, op.bj);
+    int ba = tag0 == ta ? 0 : tag1 == ta ? 1 : -1;
+    int bb = tb == ta ? ba : tag0 == tb ? 0 : tag1 == tb ? 1 : -1;
+    if (ba < 0 || bb < 0) {
+      __syncthreads();  // the previous operation's smem reads and global stores are done
+      if (ba < 0) {
+        ba = bb == 0 ? 1 : 0;
+        load_blk(buf(ba), base(op.aa), n, op.ai, op.aj);
+        if (ba) tag1 = ta; else tag0 = ta;
+        if (tb == ta) bb = ba;
+      }
+      if (bb < 0) {
+        bb = 1 - ba;
+        load_blk(buf(bb), base(op.ba), n, op.bi, op.bj);
+        if (bb) tag1 = tb; else tag0 = tb;
+      }
+      cp_wait_all();
+      __syncthreads();
+    }
+    probe(0);
     const double* SA = buf(ba);
     const double* SB = buf(bb);
-    int quad[2];
+    int quad[4];
 #pragma unroll
-    for (int sl = 0; sl < 2; ++sl) quad[sl] = c_map[op.map][warp][sl];
+    for (int sl = 0; sl < 4; ++sl) quad[sl] = c_map[op.map][warp][sl];
     if (op.flags & (F_ZERO | F_NEGC)) {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) (&acc[0][0][0][0])[2 * q] = (&acc[0][0][0][0])[2 * q + 1] = 0.0;
+      for (int q = 0; q < 32; ++q) (&acc[0][0][0][0])[2 * q] = (&acc[0][0][0][0])[2 * q + 1] = 0.0;
     }
     const int fl = op.flags & (F_TA | F_TB);
 #pragma unroll
-    for (int sl = 0; sl < 2; ++sl) {
+    for (int sl = 0; sl < 4; ++sl) {
       if (quad[sl] < 0) continue;
       const int qr = quad[sl] >> 2, qc = quad[sl] & 3;
       int k0 = 0, k1 = BB;
@@ -561,7 +455,7 @@ __global__ void __launch_bounds__(NT, 2)
         mma_quad<true, false>(SA, SB, qr, qc, k0, k1, acc[sl]);
       else
         mma_quad<false, false>(SA, SB, qr, qc, k0, k1, acc[sl]);
-      if (op.flags & F_NEGC) {  // acc = A B - C  (sign -1 below gives C - A B)
+      if (op.flags & F_NEGC) {
         const double* C = base(op.ca);
 #pragma unroll
         for (int ti = 0; ti < 2; ++ti)
@@ -574,32 +468,16 @@ __global__ void __launch_bounds__(NT, 2)
             }
       }
     }
-    probe(5);
+    probe(2);
     if (op.st == ST_NONE) continue;
-    // 4. store (write-through), optionally inserting the result into the cache
-    const double sg = (double)op.sg;
     const int to = tagof(1, op.oi, op.oj);
-    cc.drop_tag(to);
-    if (op.flags & F_CACHE) {  // (cached results are full blocks: MAP_COL / MAP_ROW cover all 16 quads)
-      __syncthreads();  // every warp is done reading this operation's operands
-      const int v = cc.victim(next_mask);
-      double* D = buf(v);
-#pragma unroll
-      for (int sl = 0; sl < 2; ++sl)
-#pragma unroll
-        for (int ti = 0; ti < 2; ++ti)
-#pragma unroll
-          for (int tj = 0; tj < 2; ++tj)
-#pragma unroll
-            for (int e = 0; e < 2; ++e)
-              D[sw(16 * (quad[sl] >> 2) + 8 * ti + g, 16 * (quad[sl] & 3) + 8 * tj + 2 * tg + e)] =
-                  sg * acc[sl][ti][tj][e];
-      cc.set(v, to);
-    }
+    if (tag0 == to) tag0 = 0;  // the cached copy is stale once the block is stored
+    if (tag1 == to) tag1 = 0;
+    const double sg = (double)op.sg;
     const int gr = op.oi * BB, gc = op.oj * BB;
     const bool diag = op.oi == op.oj;
 #pragma unroll
-    for (int sl = 0; sl < 2; ++sl) {
+    for (int sl = 0; sl < 4; ++sl) {
       if (quad[sl] < 0) continue;
 #pragma unroll
       for (int ti = 0; ti < 2; ++ti)
@@ -614,61 +492,55 @@ __global__ void __launch_bounds__(NT, 2)
               x[(int64_t)(gr + r) * n + gc + c] = v;
             } else if (op.st == ST_LOWER) {
               if (c <= r) x[(int64_t)(gr + r) * n + gc + c] = v;
-            } else {  // ST_SYM
+            } else {
               if (diag && c > r) continue;
               x[(int64_t)(gr + r) * n + gc + c] = v;
               if (!(diag && c == r)) x[(int64_t)(gc + c) * n + gr + r] = v;
             }
           }
     }
-    probe(6);
+    probe(3);
   }
-  flush();
+  if constexpr (PROF) {
+    if (tid == 0)
+      for (int c = 0; c < 4; ++c) atomicAdd(prof + c, (unsigned long long)pacc[c]);
+  }
 }
 
 }  // namespace bsm
 
 cudaError_t launch_bsmall(const double* dA, double* dX, int64_t batch, int64_t n, int64_t stride, cudaStream_t st,
                           unsigned long long* dfail, int64_t id0) {
+  // TINV_BSMALL_PROF=1: per-phase clock64 spans of thread 0, printed per launch
   static int prof_mode = -1;
   static unsigned long long* dprof = nullptr;
   if (prof_mode < 0) {
     const char* e = getenv("TINV_BSMALL_PROF");
-    prof_mode = e && atoi(e) ? 1 : 0;
     cudaError_t r = cudaFuncSetAttribute(bsm::k_bsmall<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          bsm::SMEM_DYN);
     if (r == cudaSuccess)
       r = cudaFuncSetAttribute(bsm::k_bsmall<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm::SMEM_DYN);
-    if (r == cudaSuccess && prof_mode) r = cudaMalloc(&dprof, bsm::NPROF * sizeof(unsigned long long));
-    if (r != cudaSuccess) {
-      prof_mode = -1;
-      return r;
-    }
+    if (r == cudaSuccess && e && atoi(e)) r = cudaMalloc(&dprof, 4 * sizeof(unsigned long long));
+    if (r != cudaSuccess) return r;
+    prof_mode = e && atoi(e) ? 1 : 0;
   }
   const int nb = (int)((n + bsm::BB - 1) / bsm::BB);
-  static const int extra = getenv("TINV_BSMALL_EXTRA_SMEM") ? atoi(getenv("TINV_BSMALL_EXTRA_SMEM")) : 0;
-  if (extra) {
-    cudaFuncSetAttribute(bsm::k_bsmall<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm::SMEM_DYN + extra);
-    cudaFuncSetAttribute(bsm::k_bsmall<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm::SMEM_DYN + extra);
-  }
-  if (prof_mode) cudaMemsetAsync(dprof, 0, bsm::NPROF * sizeof(unsigned long long), st);
+  if (prof_mode) cudaMemsetAsync(dprof, 0, 4 * sizeof(unsigned long long), st);
   for (int64_t b0 = 0; b0 < batch; b0 += 0x7fffffff) {
     const int64_t cnt = batch - b0 < 0x7fffffff ? batch - b0 : 0x7fffffff;
     if (prof_mode)
-      bsm::k_bsmall<true><<<(unsigned)cnt, bsm::NT, bsm::SMEM_DYN + extra, st>>>(dA + b0 * stride, dX + b0 * stride, (int)n,
+      bsm::k_bsmall<true><<<(unsigned)cnt, bsm::NT, bsm::SMEM_DYN, st>>>(dA + b0 * stride, dX + b0 * stride, (int)n,
                                                                          nb, stride, dfail, id0 + b0, dprof);
     else
-      bsm::k_bsmall<false><<<(unsigned)cnt, bsm::NT, bsm::SMEM_DYN + extra, st>>>(dA + b0 * stride, dX + b0 * stride, (int)n,
+      bsm::k_bsmall<false><<<(unsigned)cnt, bsm::NT, bsm::SMEM_DYN, st>>>(dA + b0 * stride, dX + b0 * stride, (int)n,
                                                                           nb, stride, dfail, id0 + b0, nullptr);
   }
   if (prof_mode) {
-    unsigned long long h[bsm::NPROF];
+    unsigned long long h[4];
     cudaMemcpyAsync(h, dprof, sizeof h, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    static const char* names[bsm::NPROF] = {"wait", "prefetch", "factor", "trtri", "diag-store", "mma", "store", "ops", "f16", "subst", "trail", "pf-issue", "pf-count"};
-    fprintf(stderr, "[tinv bsmall] cycles per matrix:");
-    for (int c = 0; c < bsm::NPROF; ++c) fprintf(stderr, " %s %.0f", names[c], (double)h[c] / (double)batch);
-    fprintf(stderr, "\n");
+    fprintf(stderr, "[tinv bsmall] cycles per matrix: wait %.0f diag %.0f mma %.0f store %.0f\n", (double)h[0] / batch,
+            (double)h[1] / batch, (double)h[2] / batch, (double)h[3] / batch);
   }
   return cudaGetLastError();
 }
