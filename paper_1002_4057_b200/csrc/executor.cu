@@ -774,14 +774,50 @@ __device__ __forceinline__ int chol8_inv(const double* S, int p0, double (&l)[8]
   return bad;
 }
 
-// In-place Cholesky of the lower 128x128 block in S over 8-wide panels: warps
-// 0-3 factor the panel's 8x8 diagonal block redundantly in registers
-// (chol8_inv: the column chain has no shuffles or shared-memory round trips)
-// and each solves one panel row below it by the block inverse; the trailing
-// lower 8x8 tiles are updated on DMMA by all 8 warps. Returns the first
-// failing pivot (kernels.py:68-71) or -1.
+// Trailing update by panel p0 (8 columns, K = 8) of the lower 8x8 tiles in
+// tile columns [c_lo, c_hi] (rows >= the column): S -= L_p L_p^T. Warp wl of
+// nw takes tile rows c_lo + wl, c_lo + wl + nw, ...: the row's panel fragments
+// are loaded once, its tiles go two at a time.
+__device__ __forceinline__ void upd8(double* S, int p0, int c_lo, int c_hi, int wl, int nw) {
+  constexpr int T8 = BLK / 8;
+  const int lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3;
+  for (int ti = c_lo + wl; ti < T8; ti += nw) {
+    const int r = 8 * ti + g;
+    const double a0 = -S[r * SLD + p0 + tg], a1 = -S[r * SLD + p0 + 4 + tg];
+    const int jmax = min(c_hi, ti);
+    for (int tj = c_lo; tj <= jmax; tj += 2) {
+      const bool two = tj + 1 <= jmax;
+      const int c0 = 8 * tj, c1 = two ? c0 + 8 : c0;
+      double x0[2] = {S[r * SLD + c0 + 2 * tg], S[r * SLD + c0 + 2 * tg + 1]};
+      double x1[2] = {S[r * SLD + c1 + 2 * tg], S[r * SLD + c1 + 2 * tg + 1]};
+      const double b00 = S[(c0 + g) * SLD + p0 + tg], b01 = S[(c0 + g) * SLD + p0 + 4 + tg];
+      const double b10 = S[(c1 + g) * SLD + p0 + tg], b11 = S[(c1 + g) * SLD + p0 + 4 + tg];
+      dmma(x0, a0, b00);
+      dmma(x1, a0, b10);
+      dmma(x0, a1, b01);
+      dmma(x1, a1, b11);
+      S[r * SLD + c0 + 2 * tg] = x0[0];
+      S[r * SLD + c0 + 2 * tg + 1] = x0[1];
+      if (two) {
+        S[r * SLD + c1 + 2 * tg] = x1[0];
+        S[r * SLD + c1 + 2 * tg + 1] = x1[1];
+      }
+    }
+  }
+}
+
+// In-place Cholesky of the lower 128x128 block in S over 8-wide panels with
+// look-ahead. Iteration P starts with column block P updated by panels < P
+// and columns > P by panels < P - 1:
+//   A: warps 0-3 factor the 8x8 diagonal block of panel P redundantly in
+//      registers (chol8_inv: no shuffles or smem round trips on the column
+//      chain) and each solves one panel row below it by the block inverse,
+//      while warps 4-7 apply panel P - 1 to the columns > P (DMMA);
+//   B: all warps apply panel P to column block P + 1.
+// Returns the first failing pivot (kernels.py:68-71) or -1.
 __device__ int block_potrf(double* S, SmemCtl& ctl) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
+  constexpr int T8 = BLK / 8;
+  const int tid = threadIdx.x, warp = tid >> 5;
   if (tid == 0) ctl.scan_min = 1 << 30;
   long long tq = clock64();
   auto probe = [&](int k) {
@@ -790,17 +826,20 @@ __device__ int block_potrf(double* S, SmemCtl& ctl) {
     tq = now;
   };
   double* stage = S + BLK * SLD;  // the factored 8x8 diagonal block until every reader is past the barrier
-  for (int P = 0; P < BLK / 8; ++P) {
+  for (int P = 0; P < T8; ++P) {
     const int p0 = 8 * P;
     if (warp < 4) {
       double l[8][8], x[8][8];
       const int bad = chol8_inv(S, p0, l, x);
-      if (tid == 0) {
-        if (bad >= 0) atomicMin(&ctl.scan_min, p0 + bad);
+      if (tid == 0 && bad >= 0) atomicMin(&ctl.scan_min, p0 + bad);
+      if (tid < 8) {  // thread i stages row i (register-array rows picked by a select chain)
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int j = 0; j < 8; ++j) {
+          double v = 0.0;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) stage[8 * i + j] = j <= i ? l[i][j] : 0.0;
+          for (int i = 0; i < 8; ++i) v = (tid == i && j <= i) ? l[i][j] : v;
+          stage[8 * tid + j] = v;
+        }
       }
       const int q = p0 + 8 + tid;  // panel row: v = a L^-T = a x^T
       if (q < BLK) {
@@ -817,31 +856,16 @@ __device__ int block_potrf(double* S, SmemCtl& ctl) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) S[q * SLD + p0 + k] = v[k];
       }
+    } else if (P >= 1 && P + 1 < T8) {
+      upd8(S, p0 - 8, P + 1, T8 - 1, warp - 4, 4);  // look-ahead: panel P - 1 on the columns > P
     }
     cons_bar();
     probe(0);
     if (tid < 64) S[(p0 + (tid >> 3)) * SLD + p0 + (tid & 7)] = stage[tid];
-    if (P == BLK / 8 - 1) break;
-    // trailing lower 8x8 tiles of rows / columns [p0 + 8, 128): -= L_P L_P^T (K = 8)
-    const int t0 = p0 + 8, nt8 = BLK / 8 - 1 - P, ntiles = nt8 * (nt8 + 1) / 2;
-    for (int tt = warp; tt < ntiles; tt += NCONS_WARPS) {
-      int ti = 0, rem = tt;
-      while (rem > ti) {
-        rem -= ti + 1;
-        ++ti;
-      }
-      const int r0 = t0 + 8 * ti, c0 = t0 + 8 * rem;
-      double acc[2] = {S[(r0 + g) * SLD + c0 + 2 * tg], S[(r0 + g) * SLD + c0 + 2 * tg + 1]};
-#pragma unroll
-      for (int k = 0; k < 8; k += 4)
-        dmma(acc, -S[(r0 + g) * SLD + p0 + k + tg], S[(c0 + g) * SLD + p0 + k + tg]);
-      S[(r0 + g) * SLD + c0 + 2 * tg] = acc[0];
-      S[(r0 + g) * SLD + c0 + 2 * tg + 1] = acc[1];
-    }
+    if (P + 1 < T8) upd8(S, p0, P + 1, P + 1, warp, NCONS_WARPS);  // panel P on column block P + 1
     cons_bar();
     probe(1);
   }
-  cons_bar();
   const int f = ctl.scan_min;
   return f < (1 << 30) ? f : -1;
 }
