@@ -527,7 +527,9 @@ def main():
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "exec_c3_traffic.json")
-    if os.path.exists(tpath) and (n, nb, args.placement) == (32768, 512, "out"):
+    if fused:
+        tpath = os.path.join(ROOT, "profiles", "bsmall_c4_traffic.json")
+    if os.path.exists(tpath) and ((n, nb, args.placement) == (32768, 512, "out") or (fused and (n, batch) == (256, 8192))):
         with open(tpath) as fh:
             traffic = json.load(fh)["traffic_bytes"]
 
@@ -538,7 +540,9 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / DMMA_PEAK_TFLOPS, "traffic": traffic,
-                         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of one exec_kernel "
+                         "traffic_source": ("dram__bytes_read.sum + dram__bytes_write.sum of one k_bsmall launch "
+                                            "(profiles/bsmall_c4_traffic.json)") if fused else
+                                           "dram__bytes_read.sum + dram__bytes_write.sum of one exec_kernel "
                                            "launch, ncu application replay (profiles/exec_c3_traffic.json)",
                          "kernel": "tinv::bsm::k_bsmall (one CTA per matrix: fused POTRF -> TRTRI -> LAUUM, "
                                    "64x64 DMMA.8x8x4 block program)" if fused else
