@@ -3,6 +3,7 @@ and exports every header symbol; native stream generation, the native hazard
 scoreboard and the analysis API reproduce the reference (golden fixtures from
 the live reference, tests/golden/streams.json) and the oracle."""
 
+import ctypes
 import hashlib
 import json
 import os
@@ -192,3 +193,28 @@ def test_invert_host_validation():
         P.invert_host(np.eye(6), 4)
     with pytest.raises(P.InvalidSizeError):
         P.invert_batched_host(np.eye(4), 2)
+
+
+def test_fused_batched_engine_selection_and_abi_validation():
+    """Routing of invert_batched's engines (host logic) and the fused C-ABI
+    entry points' argument checks (they fail before touching a device)."""
+    from paper_1002_4057_b200.inversion import _fused_ok
+
+    assert _fused_ok(256, 256, "auto") and _fused_ok(1, 1, "fused")
+    assert not _fused_ok(256, 128, "auto") and not _fused_ok(512, 512, "auto")
+    assert not _fused_ok(256, 256, "dag")
+    with pytest.raises(ValueError):
+        _fused_ok(256, 128, "fused")  # the fused engine needs nb == n <= 256
+    with pytest.raises(ValueError):
+        _fused_ok(256, 256, "gpu")
+    with pytest.raises(ValueError):
+        P.invert_batched(np.stack([np.eye(4)] * 2), 2, engine="fused")
+    L = _native.lib()
+    fake = ctypes.c_void_p(16)
+    assert L.tinv_batch_small_launch(None, None, 1, 4, 16, None, None) == _native.ERR_BAD_ARG
+    assert L.tinv_batch_small_launch(fake, fake, 1, 300, 300 * 300, None, fake) == _native.ERR_BAD_ARG
+    assert L.tinv_batch_small_launch(fake, fake, 1, 8, 10, None, fake) == _native.ERR_BAD_ARG  # stride < n*n
+    fm, fi = ctypes.c_int64(0), ctypes.c_int64(0)
+    assert L.tinv_batch_small_host(fake, fake, 1, 257, 0, ctypes.byref(fm), ctypes.byref(fi), None) == \
+        _native.ERR_BAD_ARG
+    assert (fm.value, fi.value) == (-1, -1)
