@@ -660,6 +660,11 @@ __device__ __forceinline__ void run_gemm(const Job& jb, const ExecParams& P, Sme
 // ---------------------------------------------------------------- consumers: diagonal phases
 // A 128x128 diagonal block in shared memory uses row stride 129 doubles.
 constexpr int SLD = BLK + 1;
+// after the 128x128 block (row stride SLD): [0, 64) block_potrf's staging of
+// the factored 8x8 block, [XD_OFF, XD_OFF + 1024) the 8x8 diagonal inverses,
+// then 8 x 64 doubles of level-8 products (all inside block_trtri_dmma's T area)
+constexpr int XD_OFF = 64;
+constexpr int XT_OFF = XD_OFF + 16 * 64;
 
 // global -> global copy of n2 double2 by the 256 consumer threads, 8 loads in
 // flight per thread (a dependent load->store loop is latency-bound)
@@ -710,37 +715,35 @@ __device__ void zero_upper_row(double* tile, int d, int R, int64_t bp) {
   }
 }
 
-// ---- 128x128 diagonal-block kernels on S (shared, row stride SLD), blocked
-// over 16x16 sub-blocks: warp-shuffle factor / inverse of a 16x16 lower
-// sub-block (lane i&15 holds row i), 4x4 register micro-tiles for products.
+// ---- 128x128 diagonal-block kernels on S (shared, row stride SLD): 8x8
+// register factor / inverse blocks, DMMA for every product.
 constexpr unsigned FULL = 0xffffffffu;
 
-// column-parallel inverse of the 16x16 lower matrix held row-wise in r[]
-// (lane i&15 = row i): lane j&15 returns column j of the inverse in x[].
-__device__ __forceinline__ void warp_inv16(const double (&r)[16], double (&x)[16]) {
-  const int jc = threadIdx.x & 15;
+// x = l^-1 for a lower 8x8 l in registers (x[i][i] = 1 / l[i][i], column-wise
+// forward substitution). The one routine behind every 8x8 diagonal inverse, so
+// an inverse formed inside POTRF and one formed later from the stored factor
+// (TRTRI / INV of a received or reused tile) are bitwise equal.
+__device__ __forceinline__ void inv8(const double (&l)[8][8], double (&x)[8][8]) {
+  double d[8];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const double lii = __shfl_sync(FULL, r[i], i);
-    double acc = 0.0;
+  for (int i = 0; i < 8; ++i) d[i] = 1.0 / l[i][i];
 #pragma unroll
-    for (int k = 0; k < 15; ++k) {  // constant trip count: r[] / x[] stay in registers
-      if (k < i) {
-        const double lik = __shfl_sync(FULL, r[k], i);
-        acc = (k >= jc) ? fma(lik, x[k], acc) : acc;
-      }
+  for (int c = 0; c < 8; ++c) {
+    x[c][c] = d[c];
+#pragma unroll
+    for (int i = c + 1; i < 8; ++i) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = c; k < i; ++k) t = fma(l[i][k], x[k][c], t);
+      x[i][c] = -t * d[i];
     }
-    const double inv = 1.0 / lii;
-    x[i] = i < jc ? 0.0 : (i == jc ? inv : -acc * inv);
   }
 }
 
 // Cholesky of the lower 8x8 block at (p0, p0) of S in registers
 // (right-looking; kernels.py:68-71 failure test: not d > 0, or d non-finite):
-// l = the factor, x = l^-1 (x[i][i] = 1 / l[i][i]). Returns the first failing
-// pivot or -1.
+// l = the factor, x = l^-1. Returns the first failing pivot or -1.
 __device__ __forceinline__ int chol8_inv(const double* S, int p0, double (&l)[8][8], double (&x)[8][8]) {
-  double il[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -751,26 +754,16 @@ __device__ __forceinline__ int chol8_inv(const double* S, int p0, double (&l)[8]
     const double d = l[k][k];
     const bool b = !(d > 0.0) || !isfinite(d);
     bad = (b && bad < 0) ? k : bad;
-    il[k] = b ? 1.0 : rsqrt(d);
-    l[k][k] = b ? 1.0 : d * il[k];
+    const double il = b ? 1.0 : rsqrt(d);
+    l[k][k] = b ? 1.0 : d * il;
 #pragma unroll
-    for (int i = k + 1; i < 8; ++i) l[i][k] *= il[k];
+    for (int i = k + 1; i < 8; ++i) l[i][k] *= il;
 #pragma unroll
     for (int j = k + 1; j < 8; ++j)
 #pragma unroll
       for (int i = j; i < 8; ++i) l[i][j] = fma(-l[i][k], l[j][k], l[i][j]);
   }
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    x[c][c] = il[c];
-#pragma unroll
-    for (int i = c + 1; i < 8; ++i) {
-      double t = 0.0;
-#pragma unroll
-      for (int k = c; k < i; ++k) t = fma(l[i][k], x[k][c], t);
-      x[i][c] = -t * il[i];
-    }
-  }
+  inv8(l, x);
   return bad;
 }
 
@@ -825,20 +818,26 @@ __device__ int block_potrf(double* S, SmemCtl& ctl) {
     if (tid == 0) ctl.dbg2[k] += now - tq;
     tq = now;
   };
-  double* stage = S + BLK * SLD;  // the factored 8x8 diagonal block until every reader is past the barrier
+  // the factored 8x8 diagonal block until every reader is past the barrier;
+  // stage + XD_OFF: the inverses of the 16 diagonal 8x8 blocks (block_trtri_dmma's base)
+  double* stage = S + BLK * SLD;
   for (int P = 0; P < T8; ++P) {
     const int p0 = 8 * P;
     if (warp < 4) {
       double l[8][8], x[8][8];
       const int bad = chol8_inv(S, p0, l, x);
       if (tid == 0 && bad >= 0) atomicMin(&ctl.scan_min, p0 + bad);
-      if (tid < 8) {  // thread i stages row i (register-array rows picked by a select chain)
+      if (tid < 8) {  // thread i stages row i of L_PP and of its inverse (rows picked by select chains)
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          double v = 0.0;
+          double v = 0.0, w = 0.0;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v = (tid == i && j <= i) ? l[i][j] : v;
+          for (int i = 0; i < 8; ++i) {
+            v = (tid == i && j <= i) ? l[i][j] : v;
+            w = (tid == i && j <= i) ? x[i][j] : w;
+          }
           stage[8 * tid + j] = v;
+          stage[XD_OFF + 64 * P + 8 * tid + j] = w;
         }
       }
       const int q = p0 + 8 + tid;  // panel row: v = a L^-T = a x^T
@@ -934,14 +933,13 @@ __device__ __forceinline__ void dmma_group16x32(const double* L, int lld, int lr
 }
 
 // In-place inverse of the lower-triangular 128x128 block in S by recursive
-// doubling: the eight 16x16 diagonal blocks (one warp each, warp shuffles),
-// then for s = 16, 32, 64 every pair [[A,0],[B,C]] -> [[A^-1,0],[-C^-1 B
-// A^-1, C^-1]] with the products on DMMA (~21K cycles per block vs 37K for
-// 4x4 FMA micro-tiles, tools/micro/diag_blocks.cu). Strict upper part of S
-// must be zero on entry. Per level s and
-// pair c, T = B A^-1 (A^-1 lower: k >= first output column) into scratch,
-// then X21 = -C^-1 T (C^-1 lower: k < last output row), 16x16 groups per warp.
-__device__ void block_trtri_dmma(double* S, unsigned long long* ctl_dbg) {
+// doubling: the sixteen 8x8 diagonal inverses (inv8; from8: already left at
+// XD by block_potrf), then for s = 8, 16, 32, 64 every pair [[A,0],[B,C]] ->
+// [[A^-1,0],[-C^-1 B A^-1, C^-1]] with the products on DMMA. Strict upper
+// part of S must be zero on entry. Per level s and pair c, T = B A^-1 (A^-1
+// lower: k >= first output column) into scratch, then X21 = -C^-1 T (C^-1
+// lower: k < last output row), 16x16 groups per warp.
+__device__ void block_trtri_dmma(double* S, unsigned long long* ctl_dbg, bool from8 = false) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int TLD = 65;
   double* Tb = S + BLK * SLD;  // T of every pair of a level: pair c at Tb + c * s * TLD
@@ -953,16 +951,46 @@ __device__ void block_trtri_dmma(double* S, unsigned long long* ctl_dbg) {
     tq = now;
     ++pk;
   };
+  if (!from8) {  // the 16 diagonal 8x8 inverses (block_potrf leaves them at XD when it ran just before)
+    if (tid < BLK / 8) {
+      double l[8][8], x[8][8];
+      const int p0 = 8 * tid;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) l[i][j] = j <= i ? S[(p0 + i) * SLD + p0 + j] : 0.0;
+      inv8(l, x);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) S[BLK * SLD + XD_OFF + 64 * tid + 8 * i + j] = j <= i ? x[i][j] : 0.0;
+    }
+    cons_bar();
+  }
   {
-    const int p0 = 16 * warp, i = lane & 15;
-    double r[16], x[16];
+    // 16x16 diagonal inverses from the 8x8 ones (warp w = pair of 8x8 blocks
+    // 2w, 2w + 1): X21 = -C^-1 (B A^-1), two 8x8 DMMA tiles
+    const double* XD = S + BLK * SLD + XD_OFF;
+    double* T = S + BLK * SLD + XT_OFF + 64 * warp;
+    const int p0 = 16 * warp, g = lane >> 2, tg = lane & 3;
+    const double* Ai = XD + 128 * warp;
+    const double* Ci = Ai + 64;
+    double acc[2] = {0.0, 0.0};
 #pragma unroll
-    for (int j = 0; j < 16; ++j) r[j] = j <= i ? S[(p0 + i) * SLD + p0 + j] : 0.0;
-    warp_inv16(r, x);
+    for (int k = 0; k < 8; k += 4) dmma(acc, S[(p0 + 8 + g) * SLD + p0 + k + tg], Ai[(k + tg) * 8 + g]);
+    T[g * 8 + 2 * tg] = acc[0];
+    T[g * 8 + 2 * tg + 1] = acc[1];
     __syncwarp();
-    if (lane < 16) {
+    acc[0] = acc[1] = 0.0;
 #pragma unroll
-      for (int k = 0; k < 16; ++k) S[(p0 + k) * SLD + p0 + lane] = x[k];
+    for (int k = 0; k < 8; k += 4) dmma(acc, Ci[g * 8 + k + tg], T[(k + tg) * 8 + g]);
+    S[(p0 + 8 + g) * SLD + p0 + 2 * tg] = -acc[0];
+    S[(p0 + 8 + g) * SLD + p0 + 2 * tg + 1] = -acc[1];
+    for (int e = lane; e < 64; e += 32) {
+      const int i = e >> 3, j = e & 7;
+      S[(p0 + i) * SLD + p0 + j] = Ai[e];
+      S[(p0 + 8 + i) * SLD + p0 + 8 + j] = Ci[e];
+      S[(p0 + i) * SLD + p0 + 8 + j] = 0.0;
     }
   }
   cons_bar();
@@ -1045,7 +1073,7 @@ __device__ __noinline__ void run_special(const Job& jb, const ItemInfo& it, cons
       zero_upper_row(dst, d, R, bp);
       cons_bar();
       t1 = clock64();
-      block_trtri_dmma(S, ctl.dbg2);
+      block_trtri_dmma(S, ctl.dbg2, true);  // seeded by block_potrf's 8x8 inverses
       t2 = clock64();
       double* aux = P.pool + (int64_t)src_s * P.slot_elems;
       store_block_lower(S, aux + (int64_t)d * BLK * bp + d * BLK, bp);
