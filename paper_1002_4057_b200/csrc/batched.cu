@@ -476,9 +476,27 @@ __global__ void __launch_bounds__(NT, 3)
     const double sg = (double)op.sg;
     const int gr = op.oi * BB, gc = op.oj * BB;
     const bool diag = op.oi == op.oj;
+    // the row's two accumulator columns (2 tg, 2 tg + 1) as one 16-byte store
+    const bool pair = (n & 1) == 0 && (op.st == ST_FULL || (op.st == ST_SYM && !diag));
 #pragma unroll
     for (int sl = 0; sl < 4; ++sl) {
       if (quad[sl] < 0) continue;
+      if (pair) {
+#pragma unroll
+        for (int ti = 0; ti < 2; ++ti)
+#pragma unroll
+          for (int tj = 0; tj < 2; ++tj) {
+            const int r = 16 * (quad[sl] >> 2) + 8 * ti + g, c = 16 * (quad[sl] & 3) + 8 * tj + 2 * tg;
+            if (gr + r >= n || gc + c >= n) continue;
+            const double v0 = sg * acc[sl][ti][tj][0], v1 = sg * acc[sl][ti][tj][1];
+            *reinterpret_cast<double2*>(x + (int64_t)(gr + r) * n + gc + c) = make_double2(v0, v1);
+            if (op.st == ST_SYM) {
+              x[(int64_t)(gc + c) * n + gr + r] = v0;
+              x[(int64_t)(gc + c + 1) * n + gr + r] = v1;
+            }
+          }
+        continue;
+      }
 #pragma unroll
       for (int ti = 0; ti < 2; ++ti)
 #pragma unroll
