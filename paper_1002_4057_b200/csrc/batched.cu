@@ -530,32 +530,36 @@ __global__ void __launch_bounds__(NT, 3)
 cudaError_t launch_bsmall(const double* dA, double* dX, int64_t batch, int64_t n, int64_t stride, cudaStream_t st,
                           unsigned long long* dfail, int64_t id0) {
   // TINV_BSMALL_PROF=1: per-phase clock64 spans of thread 0, printed per launch
-  static int prof_mode = -1;
-  static unsigned long long* dprof = nullptr;
-  if (prof_mode < 0) {
-    const char* e = getenv("TINV_BSMALL_PROF");
-    cudaError_t r = cudaFuncSetAttribute(bsm::k_bsmall<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         bsm::SMEM_DYN);
+  // (process-wide state: like a context, this entry point is not thread-safe)
+  static const int prof_mode = getenv("TINV_BSMALL_PROF") && atoi(getenv("TINV_BSMALL_PROF")) ? 1 : 0;
+  static unsigned long long* dprof[64] = {};
+  static uint64_t attr_set = 0;  // devices whose kernel attributes are set
+  int dev = 0;
+  cudaError_t r = cudaGetDevice(&dev);
+  if (r != cudaSuccess) return r;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!(attr_set >> dev & 1)) {
+    r = cudaFuncSetAttribute(bsm::k_bsmall<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm::SMEM_DYN);
     if (r == cudaSuccess)
       r = cudaFuncSetAttribute(bsm::k_bsmall<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm::SMEM_DYN);
-    if (r == cudaSuccess && e && atoi(e)) r = cudaMalloc(&dprof, 4 * sizeof(unsigned long long));
+    if (r == cudaSuccess && prof_mode) r = cudaMalloc(&dprof[dev], 4 * sizeof(unsigned long long));
     if (r != cudaSuccess) return r;
-    prof_mode = e && atoi(e) ? 1 : 0;
+    attr_set |= 1ull << dev;
   }
   const int nb = (int)((n + bsm::BB - 1) / bsm::BB);
-  if (prof_mode) cudaMemsetAsync(dprof, 0, 4 * sizeof(unsigned long long), st);
+  if (prof_mode) cudaMemsetAsync(dprof[dev], 0, 4 * sizeof(unsigned long long), st);
   for (int64_t b0 = 0; b0 < batch; b0 += 0x7fffffff) {
     const int64_t cnt = batch - b0 < 0x7fffffff ? batch - b0 : 0x7fffffff;
     if (prof_mode)
       bsm::k_bsmall<true><<<(unsigned)cnt, bsm::NT, bsm::SMEM_DYN, st>>>(dA + b0 * stride, dX + b0 * stride, (int)n,
-                                                                         nb, stride, dfail, id0 + b0, dprof);
+                                                                         nb, stride, dfail, id0 + b0, dprof[dev]);
     else
       bsm::k_bsmall<false><<<(unsigned)cnt, bsm::NT, bsm::SMEM_DYN, st>>>(dA + b0 * stride, dX + b0 * stride, (int)n,
                                                                           nb, stride, dfail, id0 + b0, nullptr);
   }
   if (prof_mode) {
     unsigned long long h[4];
-    cudaMemcpyAsync(h, dprof, sizeof h, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(h, dprof[dev], sizeof h, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     fprintf(stderr, "[tinv bsmall] cycles per matrix: wait %.0f diag %.0f mma %.0f store %.0f\n", (double)h[0] / batch,
             (double)h[1] / batch, (double)h[2] / batch, (double)h[3] / batch);
@@ -625,6 +629,18 @@ int tinv_batch_small_host(const double* hA, double* hX, int64_t batch, int64_t n
   chunk = std::min<int64_t>(chunk, batch);
   const size_t need = (size_t)(chunk * mat_bytes);
   if (H.device != device) {
+    if (H.device >= 0 && cudaSetDevice(H.device) == cudaSuccess) {  // release the previous device's state
+      for (int s = 0; s < BsHost::NS; ++s) {
+        if (H.slot[s]) cudaFree(H.slot[s]);
+        if (H.h2d[s]) cudaEventDestroy(H.h2d[s]);
+        if (H.comp[s]) cudaEventDestroy(H.comp[s]);
+        if (H.d2h[s]) cudaEventDestroy(H.d2h[s]);
+      }
+      if (H.dfail) cudaFree(H.dfail);
+      for (cudaStream_t q : {H.sh, H.sc, H.sd})
+        if (q) cudaStreamDestroy(q);
+      BCK(cudaSetDevice(device));
+    }
     H = BsHost();
     H.device = device;
     BCK(cudaStreamCreateWithFlags(&H.sh, cudaStreamNonBlocking));
