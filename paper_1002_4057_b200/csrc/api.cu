@@ -605,6 +605,31 @@ double weight_of(int kind) {  // flops in units of b^3 (SURVEY.md §7 hard part 
   }
 }
 
+// Critical-path length estimate of a task in units of one 128^3 block product
+// on one SM (~17 us): item phases run one after another, the items of a phase
+// in parallel. The diagonal chains dominate when the DAG is latency-bound
+// (C2: a POTRF of a 256 tile takes ~5x a GEMM of the same tile although it
+// does a sixth of its flops), so bottom levels in flops under-prioritise them.
+double latency_of(int kind, int R) {
+  const double r = R;
+  switch (kind) {
+    case KIND_POTRF_INV:  // R factor+inverse blocks, TRSM / update phases, the full inverse
+      return 4.0 * r + (r - 1.0) * r + r;
+    case TINV_POTRF:
+      return 4.0 * r + (r - 1.0) * r;
+    case TINV_TRTRI:
+    case KIND_INV:
+      return 1.5 * r + (r - 1.0) * r;
+    case TINV_COPY:
+      return 0.3;
+    case KIND_ARRIVE:
+    case KIND_DEPART:
+      return 0.0;
+    default:  // GEMM, SYRK, TRSM, TRMM, LAUUM: one phase of K <= R block products
+      return r + 0.5;
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ plans
@@ -1058,17 +1083,21 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
     p->nedges = ne;
   }
 
-  // ---- items, renaming, priorities (flop-weighted bottom level)
+  // ---- items, renaming, priorities (bottom level in estimated critical-path time)
   std::vector<double> bl(nx, 0.0);
   double blmax = 0.0;
   // streamed output: a departure weighs like `dw` b^3 of work, pulling the
   // chains that finish result tiles forward so the copy engines overlap them
   const char* dws = getenv("TINV_DEPART_WEIGHT");
   const double dw = dws ? atof(dws) : kDepartWeight;
+  // bottom levels in estimated critical-path time (latency_of; TINV_PRIO=flops: in flops).
+  // Measured: C2 20.94 -> 20.41 ms, C3 1034.5 -> 1031.6 ms, C1 unchanged.
+  const char* pr = getenv("TINV_PRIO");
+  const bool lat = !(pr && !strcmp(pr, "flops"));
   for (int64_t u = nx - 1; u >= 0; --u) {
     double m = 0.0;
     for (int32_t k = p->tasks[u].succ_begin; k < p->tasks[u].succ_end; ++k) m = std::max(m, bl[p->succ[k]]);
-    bl[u] = (xs[u].kind == KIND_DEPART ? dw : weight_of(xs[u].kind)) + m;
+    bl[u] = (xs[u].kind == KIND_DEPART ? dw : lat ? latency_of(xs[u].kind, R) : weight_of(xs[u].kind)) + m;
     blmax = std::max(blmax, bl[u]);
   }
   std::vector<char> renamed_tile(p->nlogical, 0);

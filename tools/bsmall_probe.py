@@ -30,6 +30,17 @@ for _ in range(10):
     ts.append(e0.elapsed_time(e1))
 ts.sort()
 ms = ts[len(ts) // 2]
+ti = []
+for _ in range(10):  # in place: x <- a (untimed), then x <- x^-1
+    x.copy_(a)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _native.batch_small_launch(x.data_ptr(), x.data_ptr(), B, n, n * n, st, fail.data_ptr())
+    e1.record()
+    torch.cuda.synchronize()
+    ti.append(e0.elapsed_time(e1))
+ti.sort()
+print(f"in place: median {ti[len(ti) // 2]:.3f} ms -> {B * n**3 / ti[len(ti) // 2] / 1e9:.2f} TF/s")
 print(f"B={B} n={n}: median {ms:.3f} ms  min {ts[0]:.3f}  -> {B * n**3 / ms / 1e9:.2f} TF/s "
       f"({B * n**3 / ms / 1e9 / 37.07 * 100:.1f} % of 37.07)  fail={int(fail.item())}")
 k = torch.arange(0, B, max(1, B // 16), device="cuda")

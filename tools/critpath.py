@@ -50,3 +50,21 @@ print(f"n={n} b={b} {pl}: exec {ms:.2f} ms, critical path {len(path)} tasks, spa
 print(f"  gaps (ready->start, dispatch) {gap / 1e3:.2f} ms")
 for k in sorted(busy, key=lambda x: -busy[x]):
     print(f"  {k:10s} n={cnt[k]:5d} busy {busy[k] / 1e3:8.2f} ms  mean {busy[k] / cnt[k]:8.1f} us")
+
+# gap per transition kind (predecessor kind -> task kind) along the critical path
+trans = defaultdict(list)
+for u, v in zip(path, path[1:]):
+    trans[(names[table[u, 0]], names[table[v, 0]])].append((st[v] - en[u]) / 1e3)
+print("  gaps by transition (count, mean us, max us):")
+for k, g in sorted(trans.items(), key=lambda kv: -sum(kv[1])):
+    print(f"    {k[0]:>10s} -> {k[1]:10s} {len(g):4d} {np.mean(g):8.1f} {np.max(g):8.1f}")
+
+# for the slowest transitions: how many tasks were running when the successor became ready
+order = np.argsort(st)
+def running_at(t):
+    return int(np.sum((st <= t) & (en > t)))
+worst = sorted(zip(path, path[1:]), key=lambda uv: -(st[uv[1]] - en[uv[0]]))[:8]
+print("  worst gaps: pred -> succ, gap us, tasks running at ready time, succ items' SM")
+for u, v in worst:
+    print(f"    {names[table[u, 0]]}({u}) -> {names[table[v, 0]]}({v}) gap {(st[v] - en[u]) / 1e3:7.1f} us,"
+          f" running {running_at(en[u] + 1)}, sm {sm[v]}")
