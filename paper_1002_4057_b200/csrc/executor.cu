@@ -1204,33 +1204,56 @@ __device__ __noinline__ unsigned long long wait_entry(const ExecParams& P, const
   }
 }
 
+// A fetch-and-add ticket that overshot its level's tail: the position is
+// this CTA's (the item pushed there later can only be claimed by it), but the
+// producer does not block on it -- it keeps claiming elsewhere and takes the
+// owned item on a later pop once it has been pushed. (A blocked producer
+// idled its SM for the rest of a draining level: C2's step-3 tail.)
+struct OwnedTicket {
+  int lev = -1, pos = 0;
+};
+
 // Claim attempt over the priority levels (all 32 lanes; lane l holds the
-// head / tail snapshot of level l): the lowest non-empty level is claimed with
-// a CAS on its head. The entry is read speculatively alongside the CAS (queue
-// entries are written once per run), then ordered with an acquire fence.
-// Returns 0 when every level is (or turned out) empty.
+// head / tail snapshot of level l): first the CTA's owned ticket position if
+// its item has arrived, then the lowest non-empty level, by CAS on its head
+// or -- deep levels, no ticket outstanding -- by a fetch-and-add ticket. The
+// entry is read speculatively alongside the CAS (queue entries are written
+// once per run), then ordered with an acquire fence. Returns 0 when nothing
+// could be claimed.
 __device__ __forceinline__ unsigned long long claim_item(const ExecParams& P, int h, int t, int minback,
-                                                         bool tickets) {
+                                                         bool tickets, OwnedTicket* own) {
   const int lane = threadIdx.x & 31;
+  if (own && own->lev >= 0) {
+    unsigned long long v = 0;
+    if (lane == 0) v = ld_acquire_u64(P.queue + P.q_off[own->lev] + own->pos);
+    v = __shfl_sync(0xffffffffu, v, 0);
+    if (v) {
+      own->lev = -1;
+      return v;
+    }
+    tickets = false;  // one outstanding ticket per CTA
+  }
   unsigned m = __ballot_sync(0xffffffffu, t - h >= minback);
   while (m) {
     const int lev = __ffs(m) - 1;
     unsigned long long v = 0;
-    int got = 0;
+    int got = 0, owned = -1;
     if (lane == lev) {
       if (tickets && t - h >= P.ticket_min) {
         // deep level: a fetch-and-add ticket always succeeds in one round trip
         // (148 producers CAS-ing one head convoy at about one claim per round
-        // trip). Overshooting the tail needs ticket_min claims inside this
-        // window; if it happens the ticket still owns a unique position and
-        // waits for its push (or for the end of the run).
+        // trip). A ticket past the current tail is kept as the CTA's owned
+        // position (see OwnedTicket) unless no push can ever reach it.
         const int pos = atomicAdd(P.q_head + lev, 1);
         if (pos < P.q_off[lev + 1] - P.q_off[lev]) {
-          v = wait_entry(P, P.queue + P.q_off[lev] + pos);
-          got = 1;
-        } else {
-          h = t;  // past the level's capacity: no item will ever be pushed there
+          if (pos < ld_relaxed_s32(P.q_tail + lev) || !own) {  // pushed or reserved: the store is in flight
+            v = wait_entry(P, P.queue + P.q_off[lev] + pos);
+            got = 1;
+          } else {
+            owned = pos;
+          }
         }
+        h = t;  // drained by this claim round (or past the level's capacity)
       } else {
         const unsigned long long* slot = P.queue + P.q_off[lev] + h;
         v = ld_relaxed_u64(slot);
@@ -1246,6 +1269,12 @@ __device__ __forceinline__ unsigned long long claim_item(const ExecParams& P, in
     }
     const unsigned won = __ballot_sync(0xffffffffu, got);
     if (won) return __shfl_sync(0xffffffffu, v, __ffs(won) - 1);
+    owned = __shfl_sync(0xffffffffu, owned, lev);
+    if (owned >= 0) {
+      own->lev = lev;
+      own->pos = owned;
+      tickets = false;
+    }
     if (lane == lev && t - h < minback) m &= ~(1u << lev);
     m = __shfl_sync(0xffffffffu, m, lev);
   }
@@ -1264,12 +1293,12 @@ __device__ __forceinline__ unsigned long long try_pop(const ExecParams& P) {
     t = ld_relaxed_s32(P.q_tail + lane);
   }
   // CAS only: an overshooting ticket could wait for a push behind this CTA's own item
-  return claim_item(P, h, t, P.prefetch_min, false);
+  return claim_item(P, h, t, P.prefetch_min, false, nullptr);
 }
 
 // Blocking pop (all 32 lanes): spins until an item is claimed, every task is
 // complete, the run aborted, or the watchdog fires.
-__device__ unsigned long long pop_item(const ExecParams& P) {
+__device__ unsigned long long pop_item(const ExecParams& P, OwnedTicket& own) {
   const int lane = threadIdx.x & 31;
   unsigned last_prog = ld_relaxed_u32(P.progress);
   unsigned long long t_last = globaltimer();
@@ -1286,7 +1315,7 @@ __device__ unsigned long long pop_item(const ExecParams& P) {
       rem = ld_relaxed_s32(P.remaining);
     }
     if (__shfl_sync(0xffffffffu, ab || rem <= 0, 0)) return POP_EXIT;
-    const unsigned long long v = claim_item(P, h, t, 1, true);
+    const unsigned long long v = claim_item(P, h, t, 1, true, &own);
     if (v) return v;
     __nanosleep(spin < 64 ? 32 : 256);
     ++spin;
@@ -1639,11 +1668,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     };
     unsigned long long next = 0ull;  // item claimed ahead while streaming the previous one
+    OwnedTicket own;                 // overshot ticket position of this CTA
     for (unsigned itn = 0;; ++itn) {
       const int slot = itn & 1;
       mbar_wait(&ctl.item_empty[slot], ((itn >> 1) & 1) ^ 1);
       ptick(0);
-      const unsigned long long e = next ? next : pop_item(P);  // all 32 lanes
+      const unsigned long long e = next ? next : pop_item(P, own);  // all 32 lanes
       ptick(1);
       next = produce_item(e, slot, P, ctl, ring, tmK, tmM, R, ks, issued);
       ptick(2);

@@ -68,3 +68,12 @@ print("  worst gaps: pred -> succ, gap us, tasks running at ready time, succ ite
 for u, v in worst:
     print(f"    {names[table[u, 0]]}({u}) -> {names[table[v, 0]]}({v}) gap {(st[v] - en[u]) / 1e3:7.1f} us,"
           f" running {running_at(en[u] + 1)}, sm {sm[v]}")
+zero = defaultdict(int)
+for v in range(len(en)):
+    if en[v] <= st[v] or en[v] == 0:
+        zero[names[table[v, 0]]] += 1
+print("  tasks with an empty trace span:", dict(zero))
+# the worst successor's direct predecessors (reference DAG) with their end times
+u0, v0 = worst[0]
+print(f"  preds of {names[table[v0, 0]]}({v0}) start {st[v0] / 1e3:.1f} us:",
+      [(names[table[q, 0]], int(q), round(en[q] / 1e3, 1)) for q in pred[v0]])
