@@ -652,7 +652,7 @@ struct tinv_plan {
   int32_t *d_head = nullptr, *d_tail = nullptr, *d_ctr = nullptr;  // ctr: remaining, abort
   unsigned long long* d_err = nullptr;
   unsigned* d_progress = nullptr;
-  unsigned long long *d_ts = nullptr, *d_te = nullptr;
+  unsigned long long *d_ts = nullptr, *d_te = nullptr, *d_tr = nullptr;
   int32_t* d_tsm = nullptr;
   int32_t *d_snap_from = nullptr, *d_snap_to = nullptr;
   unsigned long long* d_phase = nullptr;
@@ -827,7 +827,7 @@ int tinv_plan_destroy(tinv_plan* p) {
   if (!p) return TINV_OK;
   cudaSetDevice(p->ctx->device);
   void* ptrs[] = {p->d_tasks, p->d_succ, p->d_indeg, p->d_done, p->d_cur,      p->d_alt,       p->d_queue, p->d_head,
-                  p->d_tail,  p->d_ctr,  p->d_err,   p->d_progress, p->d_ts, p->d_te, p->d_tsm, p->d_snap_from,
+                  p->d_tail,  p->d_ctr,  p->d_err,   p->d_progress, p->d_ts, p->d_te, p->d_tr, p->d_tsm, p->d_snap_from,
                   p->d_snap_to, p->d_phase, p->d_recv_task, p->d_inbox, p->d_depart_group, p->d_depart_count,
                   p->d_depart_seq, p->d_recv_gate, p->d_gate_flag};
   for (void* q : ptrs)
@@ -1094,6 +1094,13 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
   // Measured: C2 20.94 -> 20.41 ms, C3 1034.5 -> 1031.6 ms, C1 unchanged.
   const char* pr = getenv("TINV_PRIO");
   const bool lat = !(pr && !strcmp(pr, "flops"));
+  // level = floor(NLEV (1 - (bl / blmax)^e)): e < 1 spends more of the 32
+  // levels on the short remaining paths of the DAG's tail, where a critical
+  // chain (C2: the SYRK_ADD_T chain of step 3) otherwise queues FIFO behind
+  // hundreds of same-level items. Measured e = 1 / 0.3 / 0.1: C2 20.4 / 20.1 /
+  // 19.5 ms, C3 and C4 (DAG) unchanged (TINV_PRIO_EXP overrides).
+  const char* pe = getenv("TINV_PRIO_EXP");
+  const double prio_exp = pe ? std::max(0.01, atof(pe)) : 0.1;
   for (int64_t u = nx - 1; u >= 0; --u) {
     double m = 0.0;
     for (int32_t k = p->tasks[u].succ_begin; k < p->tasks[u].succ_end; ++k) m = std::max(m, bl[p->succ[k]]);
@@ -1128,7 +1135,7 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
       if (sio && x.out < T) p->rename_parity[x.out] ^= 1;
     }
     if (x.kind == KIND_RECV || x.kind == KIND_ARRIVE) d.flags |= TF_EXTERNAL;
-    int lev = blmax > 0 ? (int)std::floor(NLEV * (1.0 - bl[u] / blmax)) : 0;
+    int lev = blmax > 0 ? (int)std::floor(NLEV * (1.0 - std::pow(bl[u] / blmax, prio_exp))) : 0;
     lev = std::min(NLEV - 1, std::max(0, lev));
     if (x.kind == KIND_DEPART) lev = 0;  // cheap, and the copy engines wait on it
     d.level = (int8_t)lev;
@@ -1198,7 +1205,8 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
     return fail(c, TINV_ERR_CUDA, "plan allocation failed");
   }
   if (flags & TINV_TRACE) {
-    if (ckm((void**)&p->d_ts, nx * 8) || ckm((void**)&p->d_te, nx * 8) || ckm((void**)&p->d_tsm, nx * 4)) {
+    if (ckm((void**)&p->d_ts, nx * 8) || ckm((void**)&p->d_te, nx * 8) || ckm((void**)&p->d_tsm, nx * 4) ||
+        ckm((void**)&p->d_tr, nx * 8)) {
       tinv_plan_destroy(p);
       return fail(c, TINV_ERR_CUDA, "trace allocation failed");
     }
@@ -1501,6 +1509,7 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
     CK(c, cudaMemsetAsync(p->d_ts, 0xff, nx * 8, st));
     CK(c, cudaMemsetAsync(p->d_te, 0, nx * 8, st));
     CK(c, cudaMemsetAsync(p->d_tsm, 0xff, nx * 4, st));
+    CK(c, cudaMemsetAsync(p->d_tr, 0, nx * 8, st));
   }
   std::vector<int32_t> from(T), to(T);
   if (keep) {
@@ -1537,6 +1546,7 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
   P.trace_start = p->d_ts;
   P.trace_end = p->d_te;
   P.trace_sm = p->d_tsm;
+  P.trace_ready = p->d_tr;
   P.t0 = 0;
   P.nrecv = (int32_t)p->nrecv;
   P.recv_base = (int32_t)(2 * T);
@@ -1636,6 +1646,26 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
     CK(c, cudaMemcpy(p->h_ts.data(), p->d_ts, nx * 8, cudaMemcpyDeviceToHost));
     CK(c, cudaMemcpy(p->h_te.data(), p->d_te, nx * 8, cudaMemcpyDeviceToHost));
     CK(c, cudaMemcpy(p->h_tsm.data(), p->d_tsm, nx * 4, cudaMemcpyDeviceToHost));
+    if (getenv("TINV_READY_PROFILE")) {  // dispatch delay: ready (in-degree 0) -> first item start
+      std::vector<unsigned long long> tr(nx);
+      CK(c, cudaMemcpy(tr.data(), p->d_tr, nx * 8, cudaMemcpyDeviceToHost));
+      static const char* kn[] = {"COPY", "POTRF", "TRSM", "SYRK_SUB", "SYRK_ADD_T", "GEMM", "TRTRI", "TRMM_L",
+                                 "TRMM_RN", "TRMM_LT", "LAUUM", "INV", "SEND", "RECV", "ARRIVE", "DEPART", "POTRF_INV"};
+      double sum[17] = {0}, mx[17] = {0};
+      int cnt[17] = {0};
+      for (int64_t u = 0; u < nx; ++u) {
+        const int k = p->tasks[u].kind;
+        if (k < 0 || k > 16 || p->h_ts[u] == ~0ull) continue;
+        const double d = tr[u] ? ((double)p->h_ts[u] - (double)tr[u]) * 1e-3 : 0.0;  // us
+        sum[k] += d;
+        mx[k] = std::max(mx[k], d);
+        ++cnt[k];
+      }
+      fprintf(stderr, "[tinv ready] dispatch delay per kind (tasks, mean us, max us):");
+      for (int k = 0; k < 17; ++k)
+        if (cnt[k]) fprintf(stderr, " %s %d %.1f %.1f |", kn[k], cnt[k], sum[k] / cnt[k], mx[k]);
+      fprintf(stderr, "\n");
+    }
   }
   if (p->d_ts && io && getenv("TINV_DEPART_PROFILE")) {  // when do result tiles become final?
     unsigned long long t0 = ~0ull, t1 = 0;

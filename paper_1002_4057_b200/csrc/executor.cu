@@ -1386,7 +1386,10 @@ __device__ void complete_item(const ExecParams& P, const Rec& r) {
     const TaskDev& t = P.tasks[task];
     for (int k = t.succ_begin + lane; k < t.succ_end; k += 32) {
       const int s = P.succ[k];
-      if (atomicSub(P.indeg + s, 1) == 1) push_task(P, s, 0);
+      if (atomicSub(P.indeg + s, 1) == 1) {
+        if (P.trace_ready) P.trace_ready[s] = globaltimer() - P.t0;
+        push_task(P, s, 0);
+      }
     }
     __syncwarp();
     if (lane == 0) {

@@ -96,6 +96,7 @@ struct ExecParams {
   unsigned int* progress;          // completed items (watchdog)
   unsigned long long* trace_start; // per exec task, optional
   unsigned long long* trace_end;
+  unsigned long long* trace_ready;  // optional (TRACE): time the task became ready (in-degree 0)
   int32_t* trace_sm;
   unsigned long long t0;           // globaltimer at launch (trace base)
   unsigned long long* phase;       // optional per-CTA phase cycle counters (NPHASE each)
