@@ -623,9 +623,11 @@ int tinv_batch_small_host(const double* hA, double* hX, int64_t batch, int64_t n
   BCK(cudaSetDevice(device));
   BsHost& H = g_bs;
   const int64_t mat_bytes = n * n * 8;
-  // chunks of >= 2 waves of CTAs (2 per SM) and ~128 MB: PCIe time per chunk
-  // dwarfs the kernel, three slots keep both copy directions busy
-  int64_t chunk = std::max<int64_t>(4 * prop.multiProcessorCount, (128ll << 20) / mat_bytes);
+  // chunks of ~TINV_BSMALL_CHUNK_MB (default 64 MB, at least one wave of CTAs):
+  // PCIe time per chunk dwarfs the kernel, three slots keep both copy
+  // directions busy, and small chunks shorten the pipeline's fill and drain
+  static const int64_t chunk_mb = getenv("TINV_BSMALL_CHUNK_MB") ? atoll(getenv("TINV_BSMALL_CHUNK_MB")) : 64;
+  int64_t chunk = std::max<int64_t>(std::max<int64_t>(1, (chunk_mb << 20) / mat_bytes), 1);
   chunk = std::min<int64_t>(chunk, batch);
   const size_t need = (size_t)(chunk * mat_bytes);
   if (H.device != device) {
