@@ -1098,9 +1098,12 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
   // levels on the short remaining paths of the DAG's tail, where a critical
   // chain (C2: the SYRK_ADD_T chain of step 3) otherwise queues FIFO behind
   // hundreds of same-level items. Measured e = 1 / 0.3 / 0.1: C2 20.4 / 20.1 /
-  // 19.5 ms, C3 and C4 (DAG) unchanged (TINV_PRIO_EXP overrides).
+  // 19.5 ms, C3 and C4 (DAG) unchanged. Streamed plans keep e = 1: the
+  // compressed curve defers the chains that finish result tiles, so the
+  // device -> host copies pile up at the end (C3 e2e 1062 -> 1218 ms).
+  // TINV_PRIO_EXP overrides both.
   const char* pe = getenv("TINV_PRIO_EXP");
-  const double prio_exp = pe ? std::max(0.01, atof(pe)) : 0.1;
+  const double prio_exp = pe ? std::max(0.01, atof(pe)) : (sio ? 1.0 : 0.1);
   for (int64_t u = nx - 1; u >= 0; --u) {
     double m = 0.0;
     for (int32_t k = p->tasks[u].succ_begin; k < p->tasks[u].succ_end; ++k) m = std::max(m, bl[p->succ[k]]);
