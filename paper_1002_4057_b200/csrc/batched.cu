@@ -255,13 +255,35 @@ __device__ __forceinline__ void load_blk(double* S, const double* G, int n, int 
   cp_commit();
 }
 
-// In-place Cholesky of the lower 64x64 block in S (8-wide panels, 4 warps):
-// warps 0-1 factor the 8x8 diagonal block in registers and solve the panel
-// rows below it; all warps update the trailing lower 8x8 tiles on DMMA. The
-// 8x8 diagonal inverses go to X (zeroed here). Strict upper of S zero on entry.
+// Row block R of X = L^-1 by bordering (warp wl of nw, 8x8 tiles c < R):
+// X_Rc = -X_RR (sum_{k=c}^{R-1} L_Rk X_kc). Needs L's row block R (final once
+// panels < R are done), X's rows < R and X_RR. The partial sum is staged in
+// X's strictly upper block (c, R) (zero in the result) and cleared after use.
+__device__ __forceinline__ void border_row(const double* S, double* X, int R, int wl, int nw) {
+  const int lane = threadIdx.x & 31;
+  for (int c = wl; c < R; c += nw) {
+    const int r0 = 8 * R, c0 = 8 * c;
+    tile8([&](int i, int k) { return S[sw(r0 + i, c0 + k)]; }, [&](int k, int j) { return X[sw(c0 + k, c0 + j)]; },
+          [&](int i, int j, double v) { X[sw(c0 + i, r0 + j)] = v; }, 8 * (R - c), 1.0);
+    __syncwarp();
+    tile8([&](int i, int k) { return X[sw(r0 + i, r0 + k)]; }, [&](int k, int j) { return X[sw(c0 + k, r0 + j)]; },
+          [&](int i, int j, double v) { X[sw(r0 + i, c0 + j)] = v; }, 8, -1.0);
+    __syncwarp();
+    for (int e = lane; e < 64; e += 32) X[sw(c0 + (e >> 3), r0 + (e & 7))] = 0.0;
+  }
+}
+
+// In-place Cholesky of the lower 64x64 block in S (8-wide panels, 4 warps)
+// and X = L^-1: warps 0-1 factor the panel's 8x8 diagonal block in registers
+// (its inverse -> X's diagonal) and solve the panel rows below it, while
+// warps 2-3 border X with the previous row block; then all warps update the
+// trailing lower 8x8 tiles on DMMA. X is zeroed here; S's strict upper part
+// must be zero on entry (its 8x8 diagonal blocks are left unfactored: only
+// the off-diagonal factor blocks and L^-1 are used).
 __device__ void factor64(double* S, double* X, int* fail) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
   for (int e = tid; e < BUFD; e += NT) X[e] = 0.0;
+  __syncthreads();
   for (int P = 0; P < 8; ++P) {
     const int p0 = 8 * P;
     if (warp < 2) {
@@ -289,6 +311,8 @@ __device__ void factor64(double* S, double* X, int* fail) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) S[sw(q, p0 + k)] = v[k];
       }
+    } else if (P >= 2) {
+      border_row(S, X, P - 1, warp - 2, 2);  // row block P - 1 of the inverse
     }
     __syncthreads();
     if (P == 7) break;
@@ -308,39 +332,10 @@ __device__ void factor64(double* S, double* X, int* fail) {
     }
     __syncthreads();
   }
+  border_row(S, X, 7, warp, NT / 32);  // the last row block
+  __syncthreads();
 }
 
-// X = L^-1 (64x64) by recursive doubling from the 8x8 diagonal inverses in X;
-// T_c = B A^-1 of pair c at level s is staged in X's strictly upper block
-// [a0, a0 + s) x [b0, b0 + s) of the pair and zeroed after use.
-__device__ void trtri64(const double* L, double* X) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int s = 8; s < BB; s *= 2) {
-    const int per = (s / 8) * (s / 8), total = (BB / (2 * s)) * per;
-    for (int tt = warp; tt < total; tt += NT / 32) {
-      const int c = tt / per, ti = (tt % per) / (s / 8), tj = tt % (s / 8);
-      const int a0 = 2 * c * s, b0 = a0 + s, r0 = 8 * ti, c0 = 8 * tj;
-      tile8([&](int i, int k) { return L[sw(b0 + r0 + i, a0 + k)]; },
-            [&](int k, int j) { return X[sw(a0 + k, a0 + c0 + j)]; },
-            [&](int i, int j, double v) { X[sw(a0 + r0 + i, b0 + c0 + j)] = v; }, s, 1.0);
-    }
-    __syncthreads();
-    for (int tt = warp; tt < total; tt += NT / 32) {
-      const int c = tt / per, ti = (tt % per) / (s / 8), tj = tt % (s / 8);
-      const int a0 = 2 * c * s, b0 = a0 + s, r0 = 8 * ti, c0 = 8 * tj;
-      tile8([&](int i, int k) { return X[sw(b0 + r0 + i, b0 + k)]; },
-            [&](int k, int j) { return X[sw(a0 + k, b0 + c0 + j)]; },
-            [&](int i, int j, double v) { X[sw(b0 + r0 + i, a0 + c0 + j)] = v; }, s, -1.0);
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < (BB / (2 * s)) * s * s; e += NT) {  // clear the staged T_c
-      const int c = e / (s * s), i = (e % (s * s)) / s, j = e % s;
-      X[sw(2 * c * s + i, 2 * c * s + s + j)] = 0.0;
-    }
-    __syncthreads();
-  }
-  (void)lane;
-}
 
 template <bool PROF>
 __global__ void __launch_bounds__(NT, 3)
@@ -394,7 +389,6 @@ __global__ void __launch_bounds__(NT, 3)
         if (tid == 0) atomicMin(fail, ((unsigned long long)(id0 + mat) << 32) | (unsigned)(gr + sfail));
         return;
       }
-      trtri64(S, Xs);
       for (int e = tid; e < BUFD; e += NT) {
         const int r = e >> 6, c = e & 63;
         if (gr + r < n && gr + c < n) x[(int64_t)(gr + r) * n + gr + c] = Xs[sw(r, c)];
