@@ -658,8 +658,8 @@ __device__ __forceinline__ void run_gemm(const Job& jb, const ExecParams& P, Sme
 }
 
 // ---------------------------------------------------------------- consumers: diagonal phases
-// A 128x128 diagonal block in shared memory uses row stride 129 doubles.
-constexpr int SLD = BLK + 1;
+// A 128x128 diagonal block in shared memory uses row stride SLD = 132 doubles.
+constexpr int SLD = BLK + 4;  // = 4 mod 16 doubles: m8n8k4 fragment loads (rows g, cols tg) hit distinct banks
 // after the 128x128 block (row stride SLD): [0, 64) block_potrf's staging of
 // the factored 8x8 block, [XD_OFF, XD_OFF + 1024) the 8x8 diagonal inverses,
 // then 8 x 64 doubles of level-8 products (all inside block_trtri_dmma's T area)
@@ -941,7 +941,7 @@ __device__ __forceinline__ void dmma_group16x32(const double* L, int lld, int lr
 // lower: k < last output row), 16x16 groups per warp.
 __device__ void block_trtri_dmma(double* S, unsigned long long* ctl_dbg, bool from8 = false) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int TLD = 65;
+  constexpr int TLD = 68;
   double* Tb = S + BLK * SLD;  // T of every pair of a level: pair c at Tb + c * s * TLD
   long long tq = clock64();
   int pk = 3;
