@@ -1463,6 +1463,7 @@ __device__ __forceinline__ unsigned long long produce_item(unsigned long long e,
     const Job& jb = ctl.jobs[slot][jn < MAXJ ? jn : MAXJ + 1];
     if (jb.type == J_SPECIAL) {  // it uses the ring as scratch: no loads until it is done
       while (ld_acquire_cta_u32(&ctl.jobs_done) < issued + 1) {
+        __nanosleep(200);  // a special job (diagonal chain) runs: leave the issue slots to it
       }
       fence_proxy_async();
       continue;
