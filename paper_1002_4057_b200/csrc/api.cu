@@ -287,8 +287,9 @@ int tinv_get_dense_device(tinv_ctx* c, double* dev, int64_t lda, int mode) {
   int rc = sync_slots(c);
   if (rc) return rc;
   const int sym = mode == TINV_DENSE_SYMMETRIZE;
+  // SYMMETRIZE on the device: each lower tile read once, written with its mirror (mode 2)
   CK(c, launch_get(dev, lda, 0, c->pool, c->slot_elems, c->d_a_slot, (int)c->b, (int)c->bp, (int)c->t, -1, 0,
-                   sym ? c->nmat * c->t * c->t : c->T, sym, c->st, c->T1, c->n * lda));
+                   c->T, sym ? 2 : 0, c->st, c->T1, c->n * lda));
   CK(c, cudaStreamSynchronize(c->st));
   return TINV_OK;
 }

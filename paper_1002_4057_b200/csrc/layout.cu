@@ -9,8 +9,8 @@
 // get: destination-driven gather into a dense row-major matrix; mode LOWER
 // writes the lower tiles verbatim (to_dense on authoritative tiles), mode
 // SYMMETRIZE writes the full matrix with the upper triangle mirrored from the
-// lower one (symmetrize_lower(to_dense(tm)), tile_matrix.py:117-119), the
-// transposed sub-blocks staged through shared memory for coalescing.
+// lower one (symmetrize_lower(to_dense(tm)), tile_matrix.py:117-119), 64x64
+// sub-blocks staged through shared memory (16-byte loads and stores).
 // Both are HBM-bound: 8 bytes read + 8 written per element moved.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -53,36 +53,42 @@ __global__ void __launch_bounds__(256) k_put(const double* __restrict__ src, int
   }
 }
 
-// One 32x32 destination sub-block per CTA (blockDim 32 x 8).
-// grid.x: destination tiles; for panel gathers the tile row I is fixed
-// (`panel_i` >= 0) and J = blockIdx.x; otherwise (I, J) enumerates the lower
-// tiles (LOWER) or the full t x t grid (SYMMETRIZE). grid.y: sub-block index.
+// One 64x64 destination sub-block per CTA (256 threads, 16 elements each):
+// the source sub-block is read row-wise with 16-byte loads into shared memory
+// and written row-wise with 16-byte stores, read back transposed for the
+// mirrored (upper) part. grid.x: destination tiles; for panel gathers the tile
+// row I is fixed (`panel_i` >= 0) and J = blockIdx.x; otherwise (I, J)
+// enumerates the lower tiles (LOWER) or the full t x t grid (SYMMETRIZE).
+// grid.y: sub-block index. `vec`: b, bp and ldd even (16-byte alignment).
+constexpr int GSB = 64;
 __global__ void __launch_bounds__(256) k_get(double* __restrict__ dst, int64_t ldd, int64_t row0,
                                             const double* __restrict__ pool, int64_t slot_elems,
                                             const int32_t* __restrict__ slot_of, int b, int bp, int t,
                                             int panel_i, int64_t tile_lo, int symmetrize, int64_t T1,
-                                            int64_t mstride) {
-  __shared__ double sm[32][33];
+                                            int64_t mstride, int vec) {
+  __shared__ double sm[GSB][GSB + 1];
   int I, J;
   int64_t m = 0;
   if (panel_i >= 0) {
     I = panel_i;
     J = (int)(tile_lo + blockIdx.x);
-  } else if (symmetrize) {
+  } else if (symmetrize == 1) {
     const int64_t x = tile_lo + blockIdx.x;
     m = x / ((int64_t)t * t);
     const int64_t loc = x - m * t * t;
     I = (int)(loc / t);
     J = (int)(loc % t);
-  } else {
+  } else {  // LOWER, or MIRROR (2: lower tiles, each sub-block also written transposed into tile (J, I))
     const int64_t x = tile_lo + blockIdx.x;
     m = x / T1;
     tri_decode(x - m * T1, I, J);
   }
   dst += m * mstride;
-  const int nsb = (b + 31) / 32;
+  const int nsb = (b + GSB - 1) / GSB;
   const int sr = blockIdx.y / nsb, sc = blockIdx.y % nsb;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int tid = threadIdx.x;
+  const bool mirror = symmetrize == 2;
+  if (mirror && I == J && sr < sc) return;  // written as the mirror of sub-block (sc, sr)
   // source tile and whether the sub-block is read transposed
   bool transp;
   int si, sj;
@@ -99,23 +105,62 @@ __global__ void __launch_bounds__(256) k_get(double* __restrict__ dst, int64_t l
     transp = symmetrize && (sr < sc);
   }
   const double* tile = pool + (int64_t)slot_of[m * T1 + (int64_t)si * (si + 1) / 2 + sj] * slot_elems;
-  // source sub-block coordinates
-  const int br = transp ? sc : sr, bc = transp ? sr : sc;
-  for (int k = ty; k < 32; k += 8) {
-    const int r = br * 32 + k, c = bc * 32 + tx;
-    sm[k][tx] = (r < b && c < b) ? tile[(int64_t)r * bp + c] : 0.0;
+  const int br = transp ? sc : sr, bc = transp ? sr : sc;  // source sub-block
+  if (vec) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = tid + 256 * u, k = idx >> 5, c2 = 2 * (idx & 31);
+      const int r = br * GSB + k, c = bc * GSB + c2;
+      double2 v = make_double2(0.0, 0.0);
+      if (r < b && c < b) v = __ldcs(reinterpret_cast<const double2*>(tile + (int64_t)r * bp + c));
+      sm[k][c2] = v.x;
+      sm[k][c2 + 1] = v.y;
+    }
+  } else {
+    for (int idx = tid; idx < GSB * GSB; idx += 256) {
+      const int k = idx >> 6, cc = idx & 63, r = br * GSB + k, c = bc * GSB + cc;
+      sm[k][cc] = (r < b && c < b) ? tile[(int64_t)r * bp + c] : 0.0;
+    }
   }
   __syncthreads();
   const bool diag_mix = symmetrize && I == J && sr == sc;
-  for (int k = ty; k < 32; k += 8) {
-    const int r = sr * 32 + k, c = sc * 32 + tx;  // destination element within tile (I, J)
-    if (r >= b || c >= b) continue;
-    double v;
-    if (diag_mix)
-      v = (k >= tx) ? sm[k][tx] : sm[tx][k];
-    else
-      v = transp ? sm[tx][k] : sm[k][tx];
-    dst[((int64_t)I * b + r - row0) * ldd + (int64_t)J * b + c] = v;
+  if (mirror && !diag_mix) {  // the transposed copy into tile (J, I), sub-block (sc, sr)
+    if (vec) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = tid + 256 * u, k = idx >> 5, c2 = 2 * (idx & 31);
+        const int r = sc * GSB + k, c = sr * GSB + c2;
+        if (r >= b || c >= b) continue;
+        *reinterpret_cast<double2*>(dst + ((int64_t)J * b + r - row0) * ldd + (int64_t)I * b + c) =
+            make_double2(sm[c2][k], sm[c2 + 1][k]);
+      }
+    } else {
+      for (int idx = tid; idx < GSB * GSB; idx += 256) {
+        const int k = idx >> 6, cc = idx & 63, r = sc * GSB + k, c = sr * GSB + cc;
+        if (r >= b || c >= b) continue;
+        dst[((int64_t)J * b + r - row0) * ldd + (int64_t)I * b + c] = sm[cc][k];
+      }
+    }
+  }
+  auto val = [&](int k, int cc) -> double {  // destination element (k, cc) of the sub-block
+    if (diag_mix) return cc <= k ? sm[k][cc] : sm[cc][k];
+    return transp ? sm[cc][k] : sm[k][cc];
+  };
+  if (vec) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = tid + 256 * u, k = idx >> 5, c2 = 2 * (idx & 31);
+      const int r = sr * GSB + k, c = sc * GSB + c2;  // destination element within tile (I, J)
+      if (r >= b || c >= b) continue;
+      *reinterpret_cast<double2*>(dst + ((int64_t)I * b + r - row0) * ldd + (int64_t)J * b + c) =
+          make_double2(val(k, c2), val(k, c2 + 1));
+    }
+  } else {
+    for (int idx = tid; idx < GSB * GSB; idx += 256) {
+      const int k = idx >> 6, cc = idx & 63, r = sr * GSB + k, c = sc * GSB + cc;
+      if (r >= b || c >= b) continue;
+      dst[((int64_t)I * b + r - row0) * ldd + (int64_t)J * b + c] = val(k, cc);
+    }
   }
 }
 
@@ -132,10 +177,12 @@ cudaError_t launch_get(double* dst, int64_t ldd, int64_t row0, const double* poo
                        const int32_t* slot_of, int b, int bp, int t, int panel_i, int64_t tile_lo,
                        int64_t ntiles, int symmetrize, cudaStream_t st, int64_t T1, int64_t mstride) {
   if (ntiles <= 0) return cudaSuccess;
-  const int nsb = (b + 31) / 32;
+  const int nsb = (b + GSB - 1) / GSB;
+  const int vec = ((ldd | b | bp | row0) & 1) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 &&
+                  ((mstride & 1) == 0);
   dim3 grid((unsigned)ntiles, (unsigned)(nsb * nsb));
   k_get<<<grid, 256, 0, st>>>(dst, ldd, row0, pool, slot_elems, slot_of, b, bp, t, panel_i, tile_lo, symmetrize, T1,
-                              mstride);
+                              mstride, vec);
   return cudaGetLastError();
 }
 
