@@ -1140,27 +1140,28 @@ __device__ __noinline__ void run_special(const Job& jb, const ItemInfo& it, cons
       const int br = d / R, bc = d % R;
       const bool diag = (aux1 >> 16) == (aux1 & 0xffff);
       if (diag && br < bc) break;  // covered by the transposed copy of block (bc, br)
+      constexpr int DLD = BLK + 1;  // odd stride: the transposed (column) reads below are conflict-free
       const double* src = P.pool + (int64_t)src_s * P.slot_elems + (int64_t)br * BLK * bp + bc * BLK;
       double* stg = P.pool + (int64_t)(P.stage_base + aux0) * P.slot_elems;
       for (int e = threadIdx.x; e < BLK * BLK / 2; e += 256) {
         const int y = e >> 6, x2 = (e & 63) * 2;
         const double2 v = __ldcg(reinterpret_cast<const double2*>(src + (int64_t)y * bp + x2));
-        S[y * SLD + x2] = v.x;
-        S[y * SLD + x2 + 1] = v.y;
+        S[y * DLD + x2] = v.x;
+        S[y * DLD + x2 + 1] = v.y;
       }
       cons_bar();
       if (diag) {  // block (br, bc) of the mirrored tile: verbatim (diagonal block: mirrored inside)
         double* o = stg + (int64_t)br * BLK * bp + bc * BLK;
         for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
           const int y = e >> 7, x = e & (BLK - 1);
-          o[(int64_t)y * bp + x] = (br == bc && x > y) ? S[x * SLD + y] : S[y * SLD + x];
+          o[(int64_t)y * bp + x] = (br == bc && x > y) ? S[x * DLD + y] : S[y * DLD + x];
         }
       }
       if (!diag || br > bc) {  // transposed block -> (bc, br)
         double* o = stg + (int64_t)bc * BLK * bp + br * BLK;
         for (int e = threadIdx.x; e < BLK * BLK; e += 256) {
           const int x = e >> 7, y = e & (BLK - 1);
-          o[(int64_t)x * bp + y] = S[y * SLD + x];
+          o[(int64_t)x * bp + y] = S[y * DLD + x];
         }
       }
       cons_bar();
