@@ -389,9 +389,18 @@ __global__ void __launch_bounds__(NT, 3)
         if (tid == 0) atomicMin(fail, ((unsigned long long)(id0 + mat) << 32) | (unsigned)(gr + sfail));
         return;
       }
-      for (int e = tid; e < BUFD; e += NT) {
-        const int r = e >> 6, c = e & 63;
-        if (gr + r < n && gr + c < n) x[(int64_t)(gr + r) * n + gr + c] = Xs[sw(r, c)];
+      if ((n & 1) == 0) {  // X_pp = Linv_pp -> global, 16-byte stores
+        for (int e = tid; e < BUFD / 2; e += NT) {
+          const int r = e >> 5, c = 2 * (e & 31);
+          if (gr + r < n && gr + c < n)
+            *reinterpret_cast<double2*>(x + (int64_t)(gr + r) * n + gr + c) =
+                make_double2(Xs[sw(r, c)], Xs[sw(r, c + 1)]);
+        }
+      } else {
+        for (int e = tid; e < BUFD; e += NT) {
+          const int r = e >> 6, c = e & 63;
+          if (gr + r < n && gr + c < n) x[(int64_t)(gr + r) * n + gr + c] = Xs[sw(r, c)];
+        }
       }
       tag0 = 0;
       tag1 = tagof(1, p, p);
