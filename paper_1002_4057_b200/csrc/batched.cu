@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(NT, 3)
     const int gr = op.oi * BB, gc = op.oj * BB;
     const bool diag = op.oi == op.oj;
     // the row's two accumulator columns (2 tg, 2 tg + 1) as one 16-byte store
-    const bool pair = (n & 1) == 0 && (op.st == ST_FULL || (op.st == ST_SYM && !diag));
+    const bool pair = (n & 1) == 0 && (op.st == ST_FULL || op.st == ST_LOWER || (op.st == ST_SYM && !diag));
 #pragma unroll
     for (int sl = 0; sl < 4; ++sl) {
       if (quad[sl] < 0) continue;
@@ -492,6 +492,10 @@ __global__ void __launch_bounds__(NT, 3)
             const int r = 16 * (quad[sl] >> 2) + 8 * ti + g, c = 16 * (quad[sl] & 3) + 8 * tj + 2 * tg;
             if (gr + r >= n || gc + c >= n) continue;
             const double v0 = sg * acc[sl][ti][tj][0], v1 = sg * acc[sl][ti][tj][1];
+            if (op.st == ST_LOWER && c + 1 > r) {  // on / above the diagonal: lower entries only
+              if (c <= r) x[(int64_t)(gr + r) * n + gc + c] = v0;
+              continue;
+            }
             *reinterpret_cast<double2*>(x + (int64_t)(gr + r) * n + gc + c) = make_double2(v0, v1);
             if (op.st == ST_SYM) {
               x[(int64_t)(gc + c) * n + gr + r] = v0;
