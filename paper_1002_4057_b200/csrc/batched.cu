@@ -133,12 +133,16 @@ __device__ int gen_program(BOp* ops, int nb) {
       mma(1, i, i, 1, i, j, F_ZERO, KR_LT_ROW, ST_FULL, i, j, -1);  // X_ij = -X_ii T
     }
   // step 3: A^-1 = X^T X (LAUUM), lower blocks with their mirrors
+  // (chains of one row i alternate the q direction: the first operand pair of
+  // the next chain, X(q, i) with the q the previous chain ended on, is still
+  // in shared memory)
   for (int i = 0; i < nb; ++i)
     for (int j = 0; j <= i; ++j)
-      for (int q = i; q < nb; ++q) {
-        mma(1, q, i, 1, q, j, F_TA | (q == i ? F_ZERO : 0) | (i == j ? F_SKIPU : 0),
-            q == i ? (j == i ? KR_GE_BOTH : KR_GE_ROW) : KR_FULL, q == nb - 1 ? ST_SYM : ST_NONE, i, j, 1);
-        if (i != j) ops[k - 1].map = MAP_ROW;  // the chain's map (its first operation is GE_ROW)
+      for (int s = 0; s < nb - i; ++s) {
+        const int q = (j & 1) ? nb - 1 - s : i + s;
+        mma(1, q, i, 1, q, j, F_TA | (s == 0 ? F_ZERO : 0) | (i == j ? F_SKIPU : 0),
+            q == i ? (j == i ? KR_GE_BOTH : KR_GE_ROW) : KR_FULL, s == nb - i - 1 ? ST_SYM : ST_NONE, i, j, 1);
+        if (i != j) ops[k - 1].map = MAP_ROW;  // the chain's map (its q == i operation is GE_ROW)
       }
   return k;
 }
