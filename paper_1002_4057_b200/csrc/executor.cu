@@ -566,14 +566,21 @@ __device__ __forceinline__ void run_gemm(const Job& jb, const ExecParams& P, Sme
       const char* sA = ring + st * STAGE_BYTES;
       const char* sB = sA + STAGE_BYTES / 2;
       const int kb16 = ch * KCH;
-      if (!ma && !mb)
+      if (!ma && !mb) {
         chunk_mma<V, false, false>(sA, sB, acc, wm, wn, g, tg, kb16);
-      else if (ma && !mb)
-        chunk_mma<V, true, false>(sA, sB, acc, wm, wn, g, tg, kb16);
-      else if (!ma && mb)
-        chunk_mma<V, false, true>(sA, sB, acc, wm, wn, g, tg, kb16);
-      else
-        chunk_mma<V, true, true>(sA, sB, acc, wm, wn, g, tg, kb16);
+      } else {
+        // on a triangular operand's diagonal block, a chunk whose masked part
+        // covers this warp's whole tile contributes nothing: skip its DMMAs
+        const bool za = ma && ((V == V_TN) ? (64 * wm > kb16 + KCH - 1) : (kb16 > 64 * wm + 63));
+        const bool zb = mb && ((V == V_NT) ? (kb16 > 32 * wn + 31) : (32 * wn > kb16 + KCH - 1));
+        if (za || zb) {
+        } else if (ma && !mb)
+          chunk_mma<V, true, false>(sA, sB, acc, wm, wn, g, tg, kb16);
+        else if (!ma && mb)
+          chunk_mma<V, false, true>(sA, sB, acc, wm, wn, g, tg, kb16);
+        else
+          chunk_mma<V, true, true>(sA, sB, acc, wm, wn, g, tg, kb16);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&ctl.empty[st]);
     }
