@@ -215,7 +215,9 @@ int tinv_run(tinv_ctx* ctx, const int32_t* table, int64_t ntasks, int32_t stream
  * inverse to dX + k * stride (dX may equal dA). Asynchronous on cuda_stream
  * (null = legacy default stream). *dfail is a device u64 the caller sets to
  * all ones; it receives min over failing matrices of (k << 32 | column), the
- * column being POTRF's NotPositiveDefiniteError index (kernels.py:68-71). */
+ * column being POTRF's NotPositiveDefiniteError index (kernels.py:68-71).
+ * For even n, dA and dX must be 16-byte aligned and stride even (16-byte row
+ * accesses); otherwise the call returns TINV_ERR_BAD_ARG without launching. */
 int tinv_batch_small_launch(const double* dA, double* dX, int64_t batch, int64_t n, int64_t stride,
                             void* cuda_stream, unsigned long long* dfail);
 /* tinv_batch_small_host: host buffers (page-locked for overlap), blocking.

@@ -9,10 +9,12 @@
 
 #include <algorithm>
 #include <array>
+#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <map>
 #include <unordered_map>
 #include <vector>
 
@@ -397,14 +399,18 @@ int tinv_put_tile(tinv_ctx* c, int64_t i, int64_t j, const double* host) {
   CK(c, cudaSetDevice(c->device));
   int rc = sync_slots(c);
   if (rc) return rc;
-  double* tmp = nullptr;
-  CK(c, cudaMalloc(&tmp, (size_t)c->b * c->b * 8));
-  CK(c, cudaMemcpyAsync(tmp, host, (size_t)c->b * c->b * 8, cudaMemcpyHostToDevice, c->st));
-  const int64_t x = tri_index(i, j);
-  CK(c, launch_put(tmp - i * c->b * c->b - j * c->b, c->b, 0, c->pool, c->slot_elems, c->d_a_slot, (int)c->b,
-                   (int)c->bp, x, 1, c->st, c->T1, 0));
+  const int64_t b = c->b, bp = c->bp, x = tri_index(i, j);
+  double* slot = c->pool + (int64_t)c->a_slot[x] * c->slot_elems;
+  // the b x b tile straight into its slot; a padded slot (bp > b) gets the
+  // closure padding (identity on a diagonal tile, 0 elsewhere) around it
+  if (bp != b) {
+    if (i == j)  // one-tile pad launch: slot_of = this tile's slot entry, decoded as a diagonal tile
+      CK(c, launch_pad(c->pool, c->slot_elems, c->d_a_slot + x, (int)b, (int)bp, 1, 1, c->st));
+    else
+      CK(c, cudaMemset2DAsync(slot, bp * 8, 0, bp * 8, bp, c->st));
+  }
+  CK(c, cudaMemcpy2DAsync(slot, bp * 8, host, b * 8, b * 8, b, cudaMemcpyHostToDevice, c->st));
   CK(c, cudaStreamSynchronize(c->st));
-  cudaFree(tmp);
   return TINV_OK;
 }
 
@@ -737,10 +743,13 @@ int tinv_dist_stream(const int32_t* table, int64_t n, int32_t t, int32_t P, int3
   };
   // pass 1: consumer ranks of every (tile, version), version = writer task (-1: initial)
   std::unordered_map<int64_t, int32_t> last;
-  std::unordered_map<int64_t, uint64_t> need;  // (tile key, version) -> rank mask
-  std::vector<int64_t> init_order;             // tiles whose initial version travels, first-use order
-  auto vkey = [](int64_t tk, int32_t ver) { return (tk * 1000003ll) ^ ((int64_t)(ver + 1) << 1); };
-  std::unordered_map<int64_t, std::pair<int64_t, int32_t>> vinfo;  // vkey -> (tile key, version)
+  // (tile key, version) pairs are exact keys: an ordered map on the pair (no
+  // hashing into one int64, which could merge two versions' rank masks)
+  typedef std::pair<int64_t, int32_t> VKey;
+  std::map<VKey, uint64_t> need;   // (tile key, version) -> rank mask
+  std::vector<int64_t> init_order;  // tiles whose initial version travels, first-use order
+  auto vkey = [](int64_t tk, int32_t ver) { return VKey(tk, ver); };
+  std::map<VKey, std::pair<int64_t, int32_t>> vinfo;  // vkey -> (tile key, version)
   for (int64_t v = 0; v < n; ++v) {
     const int32_t* f = table + v * TINV_TASK_FIELDS;
     const int rv = own(f[F_OR], f[F_OC]);
@@ -750,7 +759,7 @@ int tinv_dist_stream(const int32_t* table, int64_t n, int32_t t, int32_t P, int3
       const int64_t tk = key(f, x + 1);
       auto it = last.find(tk);
       const int32_t ver = it == last.end() ? -1 : it->second;
-      const int64_t vk = vkey(tk, ver);
+      const VKey vk = vkey(tk, ver);
       if (!vinfo.count(vk)) {
         vinfo[vk] = {tk, ver};
         if (ver < 0) init_order.push_back(tk);
@@ -762,7 +771,7 @@ int tinv_dist_stream(const int32_t* table, int64_t n, int32_t t, int32_t P, int3
   // pass 2: emit
   std::vector<Tk> res;
   std::vector<int32_t> ow, de, rf;
-  std::unordered_map<int64_t, int32_t> recv_label;  // vkey * 64 + rank -> label
+  std::map<std::pair<VKey, int>, int32_t> recv_label;  // (vkey, rank) -> label
   int32_t next_label = 64;
   std::unordered_map<int64_t, std::array<int32_t, 3>> tile_of;  // tile key -> (label, row, col)
   auto emit_sends = [&](int64_t tk, int32_t ver, int lab, int r, int c) {
@@ -771,7 +780,7 @@ int tinv_dist_stream(const int32_t* table, int64_t n, int32_t t, int32_t P, int3
     for (int d = 0; d < 64; ++d)
       if (it->second >> d & 1) {
         const int32_t lbl = next_label++;
-        recv_label[vkey(tk, ver) * 64 + d] = lbl;
+        recv_label[{vkey(tk, ver), d}] = lbl;
         Tk cp = {{TINV_COPY, TINV_STEP_COPY, r, c, -1, lbl, r, c, 2, 1, lab, r, c, -1, -1, -1}};
         res.push_back(cp);
         ow.push_back(own(r, c));
@@ -803,7 +812,9 @@ int tinv_dist_stream(const int32_t* table, int64_t n, int32_t t, int32_t P, int3
       const int64_t tk = tile_key(f[o], f[o + 1], f[o + 2]);
       auto it = last.find(tk);
       const int32_t ver = it == last.end() ? -1 : it->second;
-      f[o] = recv_label.at(vkey(tk, ver) * 64 + rv);
+      const auto rl = recv_label.find({vkey(tk, ver), rv});
+      if (rl == recv_label.end()) return fail(nullptr, TINV_ERR_INTERNAL, "dist_stream: missing receive label");
+      f[o] = rl->second;
     }
     res.push_back(task);
     ow.push_back(rv);
@@ -1614,14 +1625,25 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
     P.phase = p->d_phase;
   }
   CK(c, cudaEventRecord(p->ev0, st));
+  if (io) {
+    // Arrival copies (and their gate-flag writes) are enqueued BEFORE the
+    // persistent executor, which spins on those flags: they depend only on the
+    // state reset (ev0), never on the kernel, so they complete even when the
+    // launch is serialised (CUDA_LAUNCH_BLOCKING, a profiler's kernel replay,
+    // one hardware connection) -- forward progress by construction.
+    CK(c, cudaStreamWaitEvent(c->st2, p->ev0, 0));
+    const int rc2 = enqueue_arrivals(c, p, *io, run_first, p->d_gate_flag, c->st2);
+    if (rc2) {
+      cudaDeviceSynchronize();
+      return rc2;
+    }
+  }
   CK(c, launch_exec(c->tmK, c->tmM, c->tmE, P, (int)c->b, c->nsm, st));
   CK(c, cudaEventRecord(p->ev1, st));
   if (io)  // executor done (or aborted): release every copy group still waiting
     CK(c, cudaMemsetAsync(p->d_depart_count, 0x7f, T * 4, st));
-  if (io) {  // copy engines, after the state reset above (ev0), concurrent with the executor
-    CK(c, cudaStreamWaitEvent(c->st2, p->ev0, 0));
-    int rc2 = enqueue_arrivals(c, p, *io, run_first, p->d_gate_flag, c->st2);
-    if (!rc2) rc2 = enqueue_departures(c, p, *io, grp_first, grp_size, backup_base, p->ev0);
+  if (io) {  // departure copies wait on counters the executor bumps; the kernel never waits on them
+    const int rc2 = enqueue_departures(c, p, *io, grp_first, grp_size, backup_base, p->ev0);
     if (rc2) {
       cudaStreamSynchronize(st);
       cudaDeviceSynchronize();

@@ -589,6 +589,11 @@ int tinv_batch_small_launch(const double* dA, double* dX, int64_t batch, int64_t
   if (!dA || !dX || !dfail) return set_error(TINV_ERR_BAD_ARG, "null pointer");
   if (batch < 0 || n < 1 || n > bsm::NBMAX * bsm::BB || stride < n * n)
     return set_error(TINV_ERR_BAD_ARG, "batched small inversion needs 1 <= n <= 256 and stride >= n*n");
+  // even n: the engine moves matrix rows with 16-byte accesses (cp.async and
+  // double2 stores at A/X + k*stride), so the bases must be 16-byte aligned and
+  // the stride even -- a misaligned access would be a sticky context fault
+  if ((n & 1) == 0 && (((uintptr_t)dA | (uintptr_t)dX) & 15 || (stride & 1)))
+    return set_error(TINV_ERR_BAD_ARG, "batched small inversion with even n needs 16-byte aligned A/X and an even stride");
   if (batch == 0) return TINV_OK;
   const cudaError_t e = launch_bsmall(dA, dX, batch, n, stride, (cudaStream_t)cuda_stream, dfail, 0);
   if (e != cudaSuccess) return set_error(TINV_ERR_CUDA, std::string("k_bsmall: ") + cudaGetErrorString(e));

@@ -258,6 +258,9 @@ def execute_multi_gpu(stream: TaskStream, a, grid=None):
         cause = _cause(e, "")
         raise ExecutionError(stream.tasks[int(tid)], cause) from cause
     x = torch.zeros((a.n, a.n), dtype=torch.float64, device="cuda")
+    # the zero fill runs on torch's stream, the gather on the context's own
+    # (non-blocking) stream: order them (get_dense_device syncs its stream on return)
+    torch.cuda.current_stream().synchronize()
     ctx.get_dense_device(x.data_ptr(), a.n, _native.DENSE_LOWER)
     x *= owned_mask(a.n, a.b, mg.grid, mg.rank, "cuda")
     dist.all_reduce(x)

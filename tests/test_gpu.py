@@ -488,3 +488,37 @@ def test_streamed_failure_reports_task():
     assert str(ei.value.task) == str(ej.value.task)
     assert ei.value.cause.index == ej.value.cause.index
     P.clear_plan_cache()
+
+
+_SERIALISED_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_1002_4057_b200 as P
+from oracle import tileinv_oracle as O
+n, b = 768, 128
+a = O.spd_matrix(n, 11, 0.5)
+cfg = P.VariantConfig(P.Placement.OUT_OF_PLACE, "UDU", True)
+ha = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
+hx = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
+ha[...] = a
+P.invert_host(ha, b, cfg, out=hx)
+ref = P.invert(a, b, cfg)
+assert np.array_equal(hx, ref), "streamed != staged"
+print("SERIALISED_OK")
+"""
+
+
+@pytest.mark.parametrize("env", [{"CUDA_LAUNCH_BLOCKING": "1"}, {"CUDA_DEVICE_MAX_CONNECTIONS": "1"}])
+def test_streamed_host_path_under_serialised_launches(env):
+    """The streamed path must make forward progress when kernel launches are
+    serialised (a profiler's replay, CUDA_LAUNCH_BLOCKING, one hardware
+    connection): the persistent executor spins on arrival flags, so the
+    arrival copies are enqueued before it launches (api.cu plan_exec_impl)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-c", _SERIALISED_SCRIPT.format(root=root)], env=e, capture_output=True,
+                       text=True, timeout=240)
+    assert r.returncode == 0 and "SERIALISED_OK" in r.stdout, r.stdout + r.stderr
