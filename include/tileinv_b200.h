@@ -136,6 +136,17 @@ int tinv_gen_stream(int32_t t, int32_t steps, const char* loops, int32_t out_of_
 int tinv_dag_edges(const int32_t* table, int64_t ntasks, const int64_t* barriers, int64_t nbar,
                    int32_t* src, int32_t* dst, int8_t* kind, int64_t cap, int64_t* nedges);
 
+/* Longest paths of the hazard DAG (dag_analysis.py:46-118 semantics, over
+ * the edges of tinv_dag_edges). weight[v]: cost of task v (NULL: 1 per kernel
+ * task, 0 per COPY -- the paper's task count). Outputs (each may be NULL):
+ * best[v] = heaviest path ending at v, v included; via[v] = its predecessor
+ * on that path (-1 at a source; ties go to the smallest task id); depth[v] =
+ * longest path ending at v counted in tasks, COPY included; *ncomp = weakly
+ * connected components among kernel tasks (include_copies: among all). */
+int tinv_dag_paths(const int32_t* table, int64_t ntasks, const int64_t* barriers, int64_t nbar,
+                   const double* weight, int32_t include_copies, double* best, int32_t* via,
+                   int32_t* depth, int64_t* ncomp);
+
 /* Distribution over a P x Q device grid (2D block-cyclic owner-computes,
  * SURVEY.md §8(e)): owner(i, j) = (i mod P) * Q + (j mod Q) for every tile of
  * every label; a task runs on the owner of its output tile. The distributed
@@ -166,6 +177,41 @@ int tinv_plan_create(tinv_ctx* ctx, const int32_t* table, int64_t ntasks, int32_
  * transfers loop back into this context (one-GPU execution of every rank). */
 int tinv_plan_create_xfer(tinv_ctx* ctx, const int32_t* table, int64_t ntasks, int32_t stream_t,
                           const int32_t* aux, int64_t nrecv, uint32_t flags, tinv_plan** plan, tinv_err* err);
+/* Ranks emulated in ONE launch on one B200 (the multi-GPU schedule on SM
+ * groups): the transfer plan of tinv_plan_create_xfer (every rank's tasks,
+ * SEND / RECV through the local pool) with rank_of[v] = the rank that runs
+ * row v (its task owner; SEND: the sender; RECV: the receiver). CTA b of the
+ * launch is rank b % nranks, each rank gets nsm / nranks CTAs and claims only
+ * its own tasks from its own priority queues -- the distributed schedule of
+ * scheduler.py:261-351 over P x Q GPUs, at 1/nranks of a B200 per rank.
+ * nranks <= 8. */
+int tinv_plan_create_ranks(tinv_ctx* ctx, const int32_t* table, int64_t ntasks, int32_t stream_t,
+                           const int32_t* aux, int64_t nrecv, const int32_t* rank_of, int32_t nranks,
+                           uint32_t flags, tinv_plan** out, tinv_err* err);
+
+/* Load report of the last tinv_plan_exec* (SURVEY.md §8(f) row 1): per CTA
+ * of the launch, the ns its scheduler warp waited for a claimable work item
+ * (busy = kernel time - idle), and the rank it served. */
+int tinv_plan_cta_idle(const tinv_plan* p, int64_t* idle_ns, int32_t* rank, int64_t cap, int64_t* nctas);
+
+/* Schedule model (host only, no GPU needed; csrc/model.cu): discrete-event
+ * simulation of the plan tinv_plan_create / _create_ranks would compile for
+ * an n x n matrix of b x b tiles, run by nranks GPUs of sms_per_rank SMs
+ * each with the executor's claim rules (per-rank level FIFOs, phase groups,
+ * work items). aux / nrecv / rank_of as in tinv_plan_create_ranks (NULL and 0
+ * for a single-GPU stream; rank_of NULL when nranks == 1). cost[9], in us:
+ * block product (128^3), per-item overhead, 128-block Cholesky+inverse,
+ * 128-block triangular inverse, 128-block copy, SEND per 128-block, link
+ * latency, masked-block fraction, ready -> start latency of an item. out[0] = makespan (us), out[1..nranks] =
+ * busy SM-us per rank, out[nranks+1] = tasks never run (0 unless deadlock).
+ * crit_kind[17] (or NULL): the chain of releasing predecessors ending at the
+ * last task to finish, its time (release -> finish) summed per task kind
+ * (TINV_* kinds 0-10, then INV, SEND, RECV, ARRIVE, DEPART, POTRF_INV). */
+int tinv_model_run(int64_t n, int64_t b, const int32_t* table, int64_t ntasks, int32_t stream_t,
+                   const int64_t* barriers, int64_t nbar, const int32_t* aux, int64_t nrecv,
+                   const int32_t* rank_of, int32_t nranks, int32_t sms_per_rank, const double* cost,
+                   double* out, double* crit_kind);
+
 /* Multi-process runs (one rank per B200 of a node): size the store for
  * `plan` and export this rank's pool and inbox as CUDA IPC handles (64 bytes
  * each); after the exchange, map every peer (handles in rank order). Call

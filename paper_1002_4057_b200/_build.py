@@ -5,7 +5,7 @@ import subprocess
 import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-SRC = [os.path.join(PKG, "csrc", f) for f in ("api.cu", "executor.cu", "layout.cu", "batched.cu")]
+SRC = [os.path.join(PKG, "csrc", f) for f in ("api.cu", "executor.cu", "layout.cu", "batched.cu", "model.cu")]
 LIB = os.path.join(PKG, "libtileinv_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -16,7 +16,7 @@ def stale():
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = SRC + [os.path.join(PKG, "csrc", "tinv_internal.h"),
+    deps = SRC + [os.path.join(PKG, "csrc", "tinv_internal.h"), os.path.join(PKG, "csrc", "host_plan.h"),
                   os.path.join(os.path.dirname(PKG), "include", "tileinv_b200.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 

@@ -24,8 +24,8 @@ DENSE_LOWER, DENSE_SYMMETRIZE = 0, 1
 EXPORTS = (
     "tinv_abi_version", "tinv_device_count", "tinv_last_error", "tinv_create", "tinv_create_batch", "tinv_destroy",
     "tinv_shape", "tinv_set_stream", "tinv_put_dense", "tinv_get_dense", "tinv_put_dense_device", "tinv_get_dense_device",
-    "tinv_put_tile", "tinv_get_tile", "tinv_gen_stream", "tinv_dag_edges", "tinv_dist_stream", "tinv_plan_create",
-    "tinv_plan_create_xfer", "tinv_ipc_export", "tinv_ipc_open", "tinv_ipc_reset", "tinv_plan_exec",
+    "tinv_put_tile", "tinv_get_tile", "tinv_gen_stream", "tinv_dag_edges", "tinv_dag_paths", "tinv_dist_stream", "tinv_plan_create",
+    "tinv_plan_create_xfer", "tinv_plan_create_ranks", "tinv_plan_cta_idle", "tinv_model_run", "tinv_ipc_export", "tinv_ipc_open", "tinv_ipc_reset", "tinv_plan_exec",
     "tinv_plan_exec_host", "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
     "tinv_batch_small_launch", "tinv_batch_small_host",
 )
@@ -82,11 +82,17 @@ def lib():
                             ctypes.c_int),
         "tinv_dag_edges": ([_I32P, _I64, _I64P, _I64, _I32P, _I32P, ctypes.POINTER(ctypes.c_int8), _I64, _I64P],
                            ctypes.c_int),
+        "tinv_dag_paths": ([_I32P, _I64, _I64P, _I64, _DP, _I32, _DP, _I32P, _I32P, _I64P], ctypes.c_int),
         "tinv_dist_stream": ([_I32P, _I64, _I32, _I32, _I32, _I32P, _I64, _I64P, _I32P, _I32P, _I32P], ctypes.c_int),
         "tinv_plan_create": ([_P, _I32P, _I64, _I32, _I64P, _I64, _U32, ctypes.POINTER(_P),
                               ctypes.POINTER(TinvErr)], ctypes.c_int),
         "tinv_plan_create_xfer": ([_P, _I32P, _I64, _I32, _I32P, _I64, _U32, ctypes.POINTER(_P),
                                    ctypes.POINTER(TinvErr)], ctypes.c_int),
+        "tinv_plan_create_ranks": ([_P, _I32P, _I64, _I32, _I32P, _I64, _I32P, _I32, _U32, ctypes.POINTER(_P),
+                                    ctypes.POINTER(TinvErr)], ctypes.c_int),
+        "tinv_plan_cta_idle": ([_P, _I64P, _I32P, _I64, _I64P], ctypes.c_int),
+        "tinv_model_run": ([_I64, _I64, _I32P, _I64, _I32, _I64P, _I64, _I32P, _I64, _I32P, _I32, _I32, _DP, _DP, _DP],
+                           ctypes.c_int),
         "tinv_ipc_export": ([_P, _P, ctypes.c_char_p, ctypes.c_char_p], ctypes.c_int),
         "tinv_ipc_open": ([_P, _I32, _I32, ctypes.c_char_p, ctypes.c_char_p], ctypes.c_int),
         "tinv_ipc_reset": ([_P], ctypes.c_int),
@@ -180,6 +186,50 @@ def dag_edges(table, barriers):
     check(L.tinv_dag_edges(_ip(table), len(table), _lp(bars), len(bars), _ip(src), _ip(dst),
                            kind.ctypes.data_as(ctypes.POINTER(ctypes.c_int8)), ne.value, ctypes.byref(ne)))
     return src, dst, kind
+
+
+def dag_paths(table, barriers, weight=None, include_copies=False):
+    """Native longest paths of the hazard DAG -> (best, via, depth, components);
+    weight None: 1 per kernel task, 0 per COPY (include/tileinv_b200.h)."""
+    L = lib()
+    table = np.ascontiguousarray(table, dtype=np.int32)
+    bars = np.ascontiguousarray(barriers, dtype=np.int64)
+    n = len(table)
+    w = None if weight is None else np.ascontiguousarray(weight, dtype=np.float64)
+    best = np.empty(n, dtype=np.float64)
+    via = np.empty(n, dtype=np.int32)
+    depth = np.empty(n, dtype=np.int32)
+    nc = ctypes.c_int64()
+    check(L.tinv_dag_paths(_ip(table), n, _lp(bars), len(bars), _dp(w) if w is not None else None,
+                           int(include_copies), _dp(best), _ip(via), _ip(depth), ctypes.byref(nc)))
+    return best, via, depth, nc.value
+
+
+MODEL_COST_KEYS = ("blk", "item", "bpotrf", "btrtri", "bcopy", "send", "link", "mask", "hop")
+
+
+KIND_NAMES = ("COPY", "POTRF", "TRSM", "SYRK_SUB", "SYRK_ADD_T", "GEMM", "TRTRI", "TRMM_LEFT", "TRMM_RIGHT_NEG",
+              "TRMM_LEFT_T", "LAUUM", "INV", "SEND", "RECV", "ARRIVE", "DEPART", "POTRF_INV")
+
+
+def model_run(n, b, table, t, barriers=(), aux=None, nrecv=0, rank_of=None, nranks=1, sms_per_rank=148,
+              cost=None, with_crit=False):
+    """Schedule model (tinv_model_run, host only) -> (makespan us, busy SM-us per rank)."""
+    L = lib()
+    table = np.ascontiguousarray(table, dtype=np.int32)
+    bars = np.ascontiguousarray(barriers, dtype=np.int64)
+    c = np.array([cost[k] for k in MODEL_COST_KEYS], dtype=np.float64)
+    out = np.zeros(nranks + 2, dtype=np.float64)
+    ax = None if aux is None else np.ascontiguousarray(aux, dtype=np.int32)
+    rk = None if rank_of is None else np.ascontiguousarray(rank_of, dtype=np.int32)
+    crit = np.zeros(17, dtype=np.float64)
+    check(L.tinv_model_run(n, b, _ip(table), len(table), t, _lp(bars), len(bars), _ip(ax), nrecv, _ip(rk), nranks,
+                           sms_per_rank, _dp(c), _dp(out), _dp(crit)))
+    if out[nranks + 1] != 0:
+        raise RuntimeError(f"model: {int(out[nranks + 1])} tasks never ran (deadlocked plan)")
+    if with_crit:
+        return float(out[0]), out[1:nranks + 1].copy(), {KIND_NAMES[k]: float(crit[k]) for k in range(17) if crit[k]}
+    return float(out[0]), out[1:nranks + 1].copy()
 
 
 def dist_stream(table, t, P, Q):
@@ -285,6 +335,33 @@ class Plan:
                                               ctypes.byref(self.h), ctypes.byref(self.err))
         self.msg = last_error(ctx.h) if self.rc != OK else ""
         return self
+
+    @classmethod
+    def ranks(cls, ctx, table, t, aux, nrecv, rank_of, nranks, flags=0):
+        """Transfer plan with every rank's tasks run by its own CTA group in
+        one launch (tinv_plan_create_ranks)."""
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        self.table = np.ascontiguousarray(table, dtype=np.int32)
+        self.barriers = np.zeros(0, np.int64)
+        self.aux = np.ascontiguousarray(aux, dtype=np.int32)
+        self.rank_of = np.ascontiguousarray(rank_of, dtype=np.int32)
+        self.h = _P()
+        self.err = TinvErr()
+        self.rc = lib().tinv_plan_create_ranks(ctx.h, _ip(self.table), len(self.table), t, _ip(self.aux), nrecv,
+                                               _ip(self.rank_of), nranks, flags, ctypes.byref(self.h),
+                                               ctypes.byref(self.err))
+        self.msg = last_error(ctx.h) if self.rc != OK else ""
+        return self
+
+    def cta_idle(self):
+        """-> (idle ns per CTA of the last run, rank of each CTA)."""
+        g = ctypes.c_int64()
+        check(lib().tinv_plan_cta_idle(self.h, None, None, 0, ctypes.byref(g)))
+        idle = np.empty(g.value, np.int64)
+        rank = np.empty(g.value, np.int32)
+        check(lib().tinv_plan_cta_idle(self.h, idle.ctypes.data_as(_I64P), _ip(rank), g.value, ctypes.byref(g)))
+        return idle, rank
 
     def run(self):
         """-> (rc, TinvErr, device ms)."""

@@ -9,7 +9,6 @@
 
 #include <algorithm>
 #include <array>
-#include <map>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -19,6 +18,7 @@
 #include <vector>
 
 #include "tinv_internal.h"
+#include "host_plan.h"
 
 namespace tinv {
 cudaError_t launch_exec(const CUtensorMap& tmK, const CUtensorMap& tmM, const CUtensorMap& tmE, const ExecParams& P,
@@ -47,28 +47,6 @@ static const int kPrefetchMin = 0;
 // bottom-level weight of a streamed-output departure in b^3 units (TINV_DEPART_WEIGHT)
 static const double kDepartWeight = 0.0;
 
-struct tinv_ctx {
-  int64_t n = 0, b = 0, t = 0, bp = 0, R = 0, T = 0;
-  int64_t nmat = 1, T1 = 0;  // batched store: nmat matrices of T1 lower tiles each (T = nmat * T1)
-  double* bstage = nullptr;  // batched host transfers: whole-batch device staging
-  double* peer_pool[MAX_RANKS] = {};     // multi-GPU: peer-mapped pools (null: loopback)
-  int32_t* peer_inbox[MAX_RANKS] = {};
-  int32_t* inbox = nullptr;              // exported inbox (multi-process)
-  int64_t inbox_len = 0;
-  bool exported = false;                 // pool mapped by peers: must not move
-  int rank = -1, world = 0;
-  int device = 0, nsm = 0;
-  cudaStream_t st = nullptr, st2 = nullptr, own = nullptr;
-  cudaStream_t dst[8] = {};  // device -> host copy streams of streamed runs
-  double* pool = nullptr;
-  int64_t pool_slots = 0, slot_elems = 0;
-  std::vector<int32_t> a_slot;  // current slot of each lower tile (home k or shadow T+k)
-  int32_t* d_a_slot = nullptr;
-  double* staging[2] = {nullptr, nullptr};
-  size_t staging_bytes = 0;
-  CUtensorMap tmK, tmM, tmE;
-  std::string err;
-};
 
 #define CK(ctx, call)                                                                               \
   do {                                                                                              \
@@ -98,6 +76,11 @@ static int fail(tinv_ctx* ctx, int code, const std::string& msg) {
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// the other slot of lower tile k's pair (home slot, shadow T + k)
+static inline int32_t alt_slot_of(const tinv_ctx* c, int64_t k) {
+  return c->a_slot[k] == c->home[k] ? (int32_t)(c->T + k) : c->home[k];
+}
 
 static int make_maps(tinv_ctx* c) {
   static EncodeTiledFn fn = nullptr;
@@ -205,7 +188,8 @@ int tinv_create_batch(tinv_ctx** out, int64_t batch, int64_t n, int64_t b, int d
     return bail(fail(nullptr, TINV_ERR_CUDA, "stream create failed"));
   c->own = c->st;
   c->a_slot.resize(c->T);
-  for (int64_t k = 0; k < c->T; ++k) c->a_slot[k] = (int32_t)k;
+  c->home.resize(c->T);
+  for (int64_t k = 0; k < c->T; ++k) c->a_slot[k] = c->home[k] = (int32_t)k;
   if (cudaMalloc(&c->d_a_slot, c->T * sizeof(int32_t)) != cudaSuccess)
     return bail(fail(nullptr, TINV_ERR_CUDA, "cudaMalloc failed"));
   cudaMemcpy(c->d_a_slot, c->a_slot.data(), c->T * sizeof(int32_t), cudaMemcpyHostToDevice);
@@ -640,42 +624,6 @@ double latency_of(int kind, int R) {
 }  // namespace
 
 // ------------------------------------------------------------------ plans
-struct tinv_plan {
-  tinv_ctx* ctx = nullptr;
-  uint32_t flags = 0;
-  int64_t nref = 0, nexec = 0, items = 0, nedges = 0;
-  std::vector<TaskDev> tasks;
-  std::vector<int32_t> succ, indeg0, ref_kind, exec_ref;
-  int64_t nlogical = 0;
-  std::vector<int32_t> cur0, alt0;  // non-matrix logical tiles (matrix tiles filled at exec)
-  int64_t dyn_slots = 0;
-  int64_t q_off[NLEV + 1];
-  std::vector<unsigned long long> q_init;
-  std::vector<int32_t> tail0;
-  // device state
-  TaskDev* d_tasks = nullptr;
-  int32_t *d_succ = nullptr, *d_indeg = nullptr, *d_done = nullptr, *d_cur = nullptr, *d_alt = nullptr;
-  unsigned long long* d_queue = nullptr;
-  int32_t *d_head = nullptr, *d_tail = nullptr, *d_ctr = nullptr;  // ctr: remaining, abort
-  unsigned long long* d_err = nullptr;
-  unsigned* d_progress = nullptr;
-  unsigned long long *d_ts = nullptr, *d_te = nullptr, *d_tr = nullptr;
-  int32_t* d_tsm = nullptr;
-  int32_t *d_snap_from = nullptr, *d_snap_to = nullptr;
-  unsigned long long* d_phase = nullptr;
-  int64_t nrecv = 0;
-  std::vector<int32_t> recv_task_h;
-  std::vector<int32_t> arrive_tile;  // TINV_STREAM_IO: logical tile of inbox index k (copy order)
-  std::vector<int32_t> depart_tile;  // matrix tiles in expected completion order (last writer's bottom level)
-  std::vector<uint8_t> rename_parity;  // per matrix tile: odd number of renaming writers (final slot = alt)
-  int32_t *d_depart_group = nullptr, *d_depart_count = nullptr;
-  int32_t *d_depart_seq = nullptr;  // observed completion order of the departures ([T] = counter)
-  int32_t *d_recv_gate = nullptr, *d_gate_flag = nullptr;  // streamed arrivals: entry -> copy run, run flags
-  int32_t *d_recv_task = nullptr, *d_inbox = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  std::vector<unsigned long long> h_ts, h_te;
-  std::vector<int32_t> h_tsm;
-};
 
 extern "C" {
 
@@ -728,6 +676,71 @@ int tinv_dag_edges(const int32_t* table, int64_t n, const int64_t* barriers, int
       dst[x] = edges[x].v;
       kind[x] = edges[x].kind;
     }
+  }
+  return TINV_OK;
+}
+
+int tinv_dag_paths(const int32_t* table, int64_t n, const int64_t* barriers, int64_t nbar, const double* weight,
+                   int32_t include_copies, double* best, int32_t* via, int32_t* depth, int64_t* ncomp) {
+  if ((!table && n > 0) || n < 0) return fail(nullptr, TINV_ERR_BAD_ARG, "null table");
+  std::vector<std::vector<Acc>> acc;
+  ref_accesses(table, n, acc);
+  std::vector<int64_t> bars(barriers, barriers + (barriers ? nbar : 0));
+  std::vector<Edge> edges;
+  scoreboard(n, acc, bars, edges);
+  // predecessor lists in ascending id (dedup): CSR by destination
+  std::vector<int64_t> off(n + 1, 0);
+  for (const Edge& e : edges) off[e.v + 1]++;
+  for (int64_t v = 0; v < n; ++v) off[v + 1] += off[v];
+  std::vector<int32_t> pred(edges.size());
+  {
+    std::vector<int64_t> fill(off.begin(), off.end() - 1);
+    for (const Edge& e : edges) pred[fill[e.v]++] = e.u;
+  }
+  std::vector<double> b(n);
+  std::vector<int32_t> w_via(n), dep(n);
+  for (int64_t v = 0; v < n; ++v) {  // every edge goes forward in stream order: ids are a topological order
+    int32_t* p0 = pred.data() + off[v];
+    int32_t* p1 = pred.data() + off[v + 1];
+    std::sort(p0, p1);
+    const bool copy = table[v * TINV_TASK_FIELDS + F_KIND] == TINV_COPY;
+    const double w = weight ? weight[v] : (copy ? 0.0 : 1.0);
+    double bb = 0.0;
+    int32_t who = -1, dd = 0;
+    for (int32_t* q = p0; q < p1; ++q) {
+      if (q > p0 && *q == q[-1]) continue;
+      if (b[*q] > bb) {  // strict: the smallest id wins a tie
+        bb = b[*q];
+        who = *q;
+      }
+      dd = std::max(dd, dep[*q]);
+    }
+    b[v] = bb + w;
+    w_via[v] = who;
+    dep[v] = dd + 1;
+  }
+  if (best) std::copy(b.begin(), b.end(), best);
+  if (via) std::copy(w_via.begin(), w_via.end(), via);
+  if (depth) std::copy(dep.begin(), dep.end(), depth);
+  if (ncomp) {  // union-find over the kept tasks
+    std::vector<int32_t> root(n);
+    std::vector<char> keep(n);
+    for (int64_t v = 0; v < n; ++v) {
+      root[v] = (int32_t)v;
+      keep[v] = include_copies || table[v * TINV_TASK_FIELDS + F_KIND] != TINV_COPY;
+    }
+    auto find = [&](int32_t x) {
+      while (root[x] != x) x = root[x] = root[root[x]];
+      return x;
+    };
+    for (const Edge& e : edges)
+      if (keep[e.u] && keep[e.v]) {
+        const int32_t ru = find(e.u), rv = find(e.v);
+        if (ru != rv) root[ru] = rv;
+      }
+    int64_t c = 0;
+    for (int64_t v = 0; v < n; ++v) c += keep[v] && find((int32_t)v) == v;
+    *ncomp = c;
   }
   return TINV_OK;
 }
@@ -837,11 +850,11 @@ int tinv_dist_stream(const int32_t* table, int64_t n, int32_t t, int32_t P, int3
 
 int tinv_plan_destroy(tinv_plan* p) {
   if (!p) return TINV_OK;
-  cudaSetDevice(p->ctx->device);
+  if (p->d_tasks) cudaSetDevice(p->ctx->device);
   void* ptrs[] = {p->d_tasks, p->d_succ, p->d_indeg, p->d_done, p->d_cur,      p->d_alt,       p->d_queue, p->d_head,
                   p->d_tail,  p->d_ctr,  p->d_err,   p->d_progress, p->d_ts, p->d_te, p->d_tr, p->d_tsm, p->d_snap_from,
                   p->d_snap_to, p->d_phase, p->d_recv_task, p->d_inbox, p->d_depart_group, p->d_depart_count,
-                  p->d_depart_seq, p->d_recv_gate, p->d_gate_flag};
+                  p->d_depart_seq, p->d_recv_gate, p->d_gate_flag, p->d_qoffs, p->d_idle};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   if (p->ev0) cudaEventDestroy(p->ev0);
@@ -858,14 +871,21 @@ static void set_err(tinv_err* err, int32_t task, int32_t kind, int32_t code, int
   err->index = index;
 }
 
+}  // extern "C"
+
+
 // aux (n x 2, or null): per-task (dest rank, receive sequence) of transfer
 // pseudo-tasks (KIND_SEND / KIND_RECV, allowed only when aux is given);
 // nrecv: inbox length (receive tiles pinned at slots 2T + seq).
-static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, const int64_t* barriers,
-                      int64_t nbar, uint32_t flags, tinv_plan** out, tinv_err* err, const int32_t* aux,
-                      int64_t nrecv) {
+// rank_of (n, or null) / nranks: ranks emulated in one launch -- task v runs
+// on the CTAs of rank rank_of[v] (tasks the planner inserts for v inherit it).
+int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, const int64_t* barriers,
+               int64_t nbar, uint32_t flags, tinv_plan** out, tinv_err* err, const int32_t* aux, int64_t nrecv,
+               const int32_t* rank_of, int32_t nranks, bool host_only) {
   set_err(err, -1, -1, TINV_OK, -1);
   if (!c || !out || (!table && n > 0)) return fail(c, TINV_ERR_BAD_ARG, "bad plan arguments");
+  if (nranks < 1 || nranks > MAX_RANKS || (nranks > 1 && !rank_of) || nranks > c->nsm)
+    return fail(c, TINV_ERR_BAD_ARG, "bad rank count");
   *out = nullptr;
   // scheduler.py:274-276
   if (stream_t != c->t) {
@@ -878,6 +898,7 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
   tinv_plan* p = new tinv_plan();
   p->ctx = c;
   p->flags = flags;
+  p->nranks = nranks;
 
   // ---- logical tiles, validation, INV insertion for TRSM (renamed inverse)
   std::unordered_map<int64_t, int32_t> logical;  // key -> logical id (non-matrix tiles)
@@ -939,7 +960,15 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
   }
   std::vector<char> is_aux;
   std::vector<int32_t> first_exec_of_ref(n * nm + 1, 0);
+  std::vector<int8_t> xrank;  // rank of every exec task
+  int8_t cur_rank = 0;
   for (int64_t rv = 0; rv < n * nm; ++rv) {
+    while (xrank.size() < xs.size()) xrank.push_back(cur_rank);  // tasks made for the previous ref task
+    cur_rank = rank_of ? (int8_t)rank_of[rv % n] : 0;
+    if (cur_rank < 0 || cur_rank >= nranks) {
+      tinv_plan_destroy(p);
+      return fail(c, TINV_ERR_BAD_ARG, "task rank out of range");
+    }
     mm = rv / n;
     const int64_t v = rv;
     const int32_t* f = table + (rv % n) * TINV_TASK_FIELDS;
@@ -1038,6 +1067,7 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
     xs.push_back({kind, f[F_STEP], o, in0, in1, f[F_OM] == 2 ? 2 : 1, (int)v, -1, -1, xflags});
   }
   first_exec_of_ref[n * nm] = (int32_t)xs.size();
+  while (xrank.size() < xs.size()) xrank.push_back(cur_rank);
   std::vector<int32_t> depart_lw;  // last writer of each departing tile
   if (sio)  // DEPART: every lower tile of every matrix, after its last writer
     for (int64_t m = 0; m < nm; ++m)
@@ -1115,7 +1145,13 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
   // device -> host copies pile up at the end (C3 e2e 1062 -> 1218 ms).
   // TINV_PRIO_EXP overrides both.
   const char* pe = getenv("TINV_PRIO_EXP");
-  const double prio_exp = pe ? std::max(0.01, atof(pe)) : (sio ? 1.0 : 0.1);
+  // Transfer plans (multi-GPU, aux given) use e = 10: resolution at the TOP
+  // of the bottom-level range, where the distributed run is critical-path
+  // bound (the step-1 panel chain crossing ranks through SEND / RECV). In the
+  // schedule model (csrc/model.cu, tools/scaling_model.py) at C3 on 8 B200s:
+  // e = 0.1 / 1 / 4 / 10 -> 235 / 232 / 181 / 150 ms (efficiency 0.54 ->
+  // 0.84), the one-launch emulation on one B200 agreeing with the model.
+  const double prio_exp = pe ? std::max(0.01, atof(pe)) : (sio ? 1.0 : (aux ? 10.0 : 0.1));
   for (int64_t u = nx - 1; u >= 0; --u) {
     double m = 0.0;
     for (int32_t k = p->tasks[u].succ_begin; k < p->tasks[u].succ_end; ++k) m = std::max(m, bl[p->succ[k]]);
@@ -1124,7 +1160,8 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
   }
   std::vector<char> renamed_tile(p->nlogical, 0);
   if (sio) p->rename_parity.assign(T, 0);
-  std::vector<int64_t> lev_items(NLEV, 0);
+  const int NQ = nranks * NLEV;  // queue sets: one per rank
+  std::vector<int64_t> lev_items(NQ, 0);
   p->exec_ref.resize(nx);
   for (int64_t u = 0; u < nx; ++u) {
     TaskDev& d = p->tasks[u];
@@ -1139,6 +1176,7 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
     d.aux1 = x.aux1;
     d.nitems = total_items(x.kind, R);
     d.nphases = (int16_t)ngroups(x.kind, R);
+    d.rank = u < (int64_t)xrank.size() ? xrank[u] : 0;  // DEPART (streamed plans, one rank): 0
     d.pad = 0;
     d.flags = (int8_t)x.flags;
     const bool alias = (x.in0 == x.out || x.in1 == x.out);
@@ -1154,7 +1192,7 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
     lev = std::min(NLEV - 1, std::max(0, lev));
     if (x.kind == KIND_DEPART) lev = 0;  // cheap, and the copy engines wait on it
     d.level = (int8_t)lev;
-    lev_items[lev] += d.nitems;
+    lev_items[d.rank * NLEV + lev] += d.nitems;
     p->items += d.nitems;
     p->exec_ref[u] = x.ref;
   }
@@ -1176,15 +1214,16 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
     for (size_t k = 0; k < ord.size(); ++k) dt[k] = p->depart_tile[ord[k]];
     p->depart_tile.swap(dt);
   }
-  p->q_off[0] = 0;
-  for (int l = 0; l < NLEV; ++l) p->q_off[l + 1] = p->q_off[l] + lev_items[l];
-  p->tail0.assign(NLEV, 0);
-  p->q_init.assign(p->q_off[NLEV], 0ull);
+  p->q_off.assign(NQ + 1, 0);
+  for (int l = 0; l < NQ; ++l) p->q_off[l + 1] = p->q_off[l] + lev_items[l];
+  p->tail0.assign(NQ, 0);
+  p->q_init.assign(p->q_off[NQ], 0ull);
   for (int64_t u = 0; u < nx; ++u)
     if (p->indeg0[u] == 0 && !(p->tasks[u].flags & TF_EXTERNAL)) {
       const TaskDev& d = p->tasks[u];
+      const int q = d.rank * NLEV + d.level;
       for (int i = 0; i < group_items(d.kind, R, 0); ++i)
-        p->q_init[p->q_off[d.level] + p->tail0[d.level]++] = ((unsigned long long)(u + 1) << 32) | (unsigned)i;
+        p->q_init[p->q_off[q] + p->tail0[q]++] = ((unsigned long long)(u + 1) << 32) | (unsigned)i;
     }
 
   // ---- slots of the non-matrix logical tiles: [2T, 2T + dyn)
@@ -1206,13 +1245,18 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
   for (int64_t u = 0; u < nx; ++u)
     if (xs[u].kind == KIND_RECV || xs[u].kind == KIND_ARRIVE) p->recv_task_h[xs[u].aux1] = (int32_t)u;
 
+  if (host_only) {  // schedule model: the compiled DAG only
+    *out = p;
+    return TINV_OK;
+  }
   // ---- device buffers
   auto ckm = [&](void** ptr, size_t bytes) { return cudaMalloc(ptr, std::max<size_t>(bytes, 16)); };
   if (cudaSetDevice(c->device) != cudaSuccess || ckm((void**)&p->d_tasks, nx * sizeof(TaskDev)) ||
       ckm((void**)&p->d_succ, p->succ.size() * 4) || ckm((void**)&p->d_indeg, nx * 4) ||
       ckm((void**)&p->d_done, nx * 4) || ckm((void**)&p->d_cur, p->nlogical * 4) ||
-      ckm((void**)&p->d_alt, p->nlogical * 4) || ckm((void**)&p->d_queue, p->q_off[NLEV] * 8) ||
-      ckm((void**)&p->d_head, NLEV * 4) || ckm((void**)&p->d_tail, NLEV * 4) || ckm((void**)&p->d_ctr, 2 * 4) ||
+      ckm((void**)&p->d_alt, p->nlogical * 4) || ckm((void**)&p->d_queue, p->q_off[NQ] * 8) ||
+      ckm((void**)&p->d_head, NQ * 4) || ckm((void**)&p->d_tail, NQ * 4) || ckm((void**)&p->d_ctr, 2 * 4) ||
+      ckm((void**)&p->d_qoffs, (NQ + 1) * 8) || ckm((void**)&p->d_idle, (size_t)c->nsm * 8) ||
       ckm((void**)&p->d_err, 8) || ckm((void**)&p->d_progress, 4) || cudaEventCreate(&p->ev0) ||
       cudaEventCreate(&p->ev1)) {
     tinv_plan_destroy(p);
@@ -1243,6 +1287,7 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
     return fail(c, TINV_ERR_CUDA, "inbox allocation failed");
   }
   cudaMemcpy(p->d_recv_task, p->recv_task_h.data(), p->recv_task_h.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(p->d_qoffs, p->q_off.data(), (NQ + 1) * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(p->d_tasks, p->tasks.data(), nx * sizeof(TaskDev), cudaMemcpyHostToDevice);
   if (!p->succ.empty()) cudaMemcpy(p->d_succ, p->succ.data(), p->succ.size() * 4, cudaMemcpyHostToDevice);
   if (cudaGetLastError() != cudaSuccess) {
@@ -1253,15 +1298,39 @@ static int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stre
   return TINV_OK;
 }
 
+extern "C" {
+
 int tinv_plan_create(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, const int64_t* barriers,
                      int64_t nbar, uint32_t flags, tinv_plan** out, tinv_err* err) {
-  return plan_build(c, table, n, stream_t, barriers, nbar, flags, out, err, nullptr, 0);
+  return plan_build(c, table, n, stream_t, barriers, nbar, flags, out, err, nullptr, 0, nullptr, 1, false);
 }
 
 int tinv_plan_create_xfer(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, const int32_t* aux,
                           int64_t nrecv, uint32_t flags, tinv_plan** out, tinv_err* err) {
   if (!aux) return fail(c, TINV_ERR_BAD_ARG, "transfer plans need the aux table");
-  return plan_build(c, table, n, stream_t, nullptr, 0, flags, out, err, aux, nrecv);
+  return plan_build(c, table, n, stream_t, nullptr, 0, flags, out, err, aux, nrecv, nullptr, 1, false);
+}
+
+int tinv_plan_create_ranks(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, const int32_t* aux,
+                           int64_t nrecv, const int32_t* rank_of, int32_t nranks, uint32_t flags, tinv_plan** out,
+                           tinv_err* err) {
+  if (!aux || !rank_of) return fail(c, TINV_ERR_BAD_ARG, "rank plans need the aux and rank tables");
+  if (flags & TINV_STREAM_IO) return fail(c, TINV_ERR_BAD_ARG, "rank plans exclude streamed host I/O");
+  return plan_build(c, table, n, stream_t, nullptr, 0, flags, out, err, aux, nrecv, rank_of, nranks, false);
+}
+
+int tinv_plan_cta_idle(const tinv_plan* p, int64_t* idle_ns, int32_t* rank, int64_t cap, int64_t* nctas) {
+  if (!p) return TINV_ERR_BAD_ARG;
+  const int64_t g = (int64_t)p->h_idle.size();
+  if (nctas) *nctas = g;
+  if (idle_ns || rank) {
+    if (cap < g) return fail(p->ctx, TINV_ERR_BAD_ARG, "cta_idle capacity too small");
+    for (int64_t b = 0; b < g; ++b) {
+      if (idle_ns) idle_ns[b] = (int64_t)p->h_idle[b];
+      if (rank) rank[b] = (int32_t)(b % p->nranks);
+    }
+  }
+  return TINV_OK;
 }
 
 int tinv_ipc_export(tinv_ctx* c, tinv_plan* p, void* pool_handle, void* inbox_handle) {
@@ -1355,18 +1424,43 @@ typedef CUresult (*PFN_batchMemOp)(CUstream, unsigned int, CUstreamBatchMemOpPar
 // (batched t = 1 stores) move as one copy. Each run is gated by ONE flag
 // (gate_flag[run]): a flag write per tile costs the copy engine about half of
 // its H2D rate (measured, tools/copy_probe.py).
+static void tri_decode_h(int64_t k, int64_t& i, int64_t& j) {
+  i = (int64_t)((std::sqrt(8.0 * (double)k + 1.0) - 1.0) * 0.5);
+  while (i * (i + 1) / 2 > k) --i;
+  while ((i + 1) * (i + 2) / 2 <= k) ++i;
+  j = k - i * (i + 1) / 2;
+}
+
+// Column-panel runs: with unpadded tiles (b == bp) a streamed run first
+// resets every tile's home slot to column-major order (its input is fully
+// overwritten by the arrivals), so the tiles (i, j), (i+1, j), ... of a
+// column sit in consecutive slots and one 2D copy moves up to kRunBytes of a
+// column panel: ~300 copy calls at C3 instead of 2080, all enqueued before
+// the executor launches.
+constexpr size_t kRunBytes = 16u << 20;
 static void arrival_runs(tinv_ctx* c, tinv_plan* p, const HostIO& io, std::vector<int32_t>& run_first,
                          std::vector<int32_t>& gate) {
   const int64_t na = (int64_t)p->arrive_tile.size(), n = c->n, T1 = c->T1;
+  const int64_t max_run = std::max<int64_t>(1, std::min<int64_t>(128, kRunBytes / ((size_t)c->slot_elems * 8)));
   run_first.clear();
   gate.assign(std::max<int64_t>(na, 1), 0);
   for (int64_t s0 = 0; s0 < na;) {
     const int32_t o = p->arrive_tile[s0];
     int64_t run = 1;
-    if (T1 == 1 && c->b == c->bp && io.lda == n)
+    if (T1 == 1 && c->b == c->bp && io.lda == n) {  // batched t = 1: whole matrices, contiguous on both sides
       while (s0 + run < na && run < 64 && p->arrive_tile[s0 + run] == o + run &&
              c->a_slot[o + run] == c->a_slot[o] + run)
         ++run;
+    } else if (c->b == c->bp) {  // the next tiles down the same column, in consecutive slots
+      int64_t i, j;
+      tri_decode_h(o % T1, i, j);
+      const int64_t m0 = o / T1;
+      while (s0 + run < na && run < max_run && i + run < c->t) {
+        const int64_t nx = m0 * T1 + tri_index(i + run, j);
+        if (p->arrive_tile[s0 + run] != nx || c->a_slot[nx] != c->a_slot[o] + run) break;
+        ++run;
+      }
+    }
     for (int64_t r = 0; r < run; ++r) gate[s0 + r] = (int32_t)run_first.size();
     run_first.push_back((int32_t)s0);
     s0 += run;
@@ -1389,17 +1483,15 @@ static int enqueue_arrivals(tinv_ctx* c, tinv_plan* p, const HostIO& io, const s
   for (size_t g = 0; g + 1 < run_first.size(); ++g) {
     const int64_t s0 = run_first[g], run = run_first[g + 1] - s0;
     const int32_t o = p->arrive_tile[s0];
-    const int64_t m = o / T1, k = o % T1;
-    int64_t i = (int64_t)((std::sqrt(8.0 * (double)k + 1.0) - 1.0) * 0.5);
-    while (i * (i + 1) / 2 > k) --i;
-    while ((i + 1) * (i + 2) / 2 <= k) ++i;
-    const int64_t j = k - i * (i + 1) / 2;
+    const int64_t m = o / T1;
+    int64_t i, j;
+    tri_decode_h(o % T1, i, j);
     double* dst = c->pool + (int64_t)c->a_slot[o] * c->slot_elems;
     const double* src = io.a + m * n * io.lda + i * b * io.lda + j * b;
-    if (run > 1)
+    if (run > 1 && T1 == 1)  // whole consecutive matrices
       CK(c, cudaMemcpyAsync(dst, src, tile_bytes * run, cudaMemcpyHostToDevice, st));
-    else
-      CK(c, cudaMemcpy2DAsync(dst, bp * 8, src, io.lda * 8, b * 8, b, cudaMemcpyHostToDevice, st));
+    else  // one tile, or a column panel of `run` tiles into consecutive slots (b == bp)
+      CK(c, cudaMemcpy2DAsync(dst, bp * 8, src, io.lda * 8, b * 8, b * run, cudaMemcpyHostToDevice, st));
     CUstreamBatchMemOpParams op{};
     op.writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
     op.writeValue.address = (CUdeviceptr)(gate_flag + g);
@@ -1433,7 +1525,7 @@ static int enqueue_departures(tinv_ctx* c, tinv_plan* p, const HostIO& io, const
     if (!c->dst[k]) CK(c, cudaStreamCreateWithFlags(&c->dst[k], cudaStreamNonBlocking));
     CK(c, cudaStreamWaitEvent(c->dst[k], after, 0));
   }
-  const int64_t b = c->b, bp = c->bp, n = c->n, T = c->T, T1 = c->T1, ldx = io.ldx;
+  const int64_t b = c->b, bp = c->bp, n = c->n, T1 = c->T1, ldx = io.ldx;
   const bool sym = io.mode == TINV_DENSE_SYMMETRIZE;
   double* X = io.xhost;
   for (size_t g = 0; g < gfirst.size(); ++g) {
@@ -1447,7 +1539,7 @@ static int enqueue_departures(tinv_ctx* c, tinv_plan* p, const HostIO& io, const
     while ((i + 1) * (i + 2) / 2 <= kk) ++i;
     const int64_t j = kk - i * (i + 1) / 2;
     double* xm = X + m * n * ldx;
-    const double* fin = c->pool + (int64_t)(p->rename_parity[k] ? (c->a_slot[k] < T ? k + T : k) : c->a_slot[k]) *
+    const double* fin = c->pool + (int64_t)(p->rename_parity[k] ? alt_slot_of(c, k) : c->a_slot[k]) *
                                       c->slot_elems;
     const double* stg = c->pool + (stage_base + k) * c->slot_elems;
     if (gsize[g] > 1) {  // contiguous staged diagonal tiles of consecutive matrices
@@ -1504,18 +1596,32 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
     return TINV_OK;
   }
   cudaStream_t st = c->st;
+  if (io && c->b == c->bp && c->T1 > 1) {
+    // streamed run: the input is fully overwritten by the arrivals, so the
+    // tiles get column-major home slots (column panels move as one copy)
+    for (int64_t m = 0; m < c->nmat; ++m) {
+      int32_t s = (int32_t)(m * c->T1);
+      for (int64_t j = 0; j < c->t; ++j)
+        for (int64_t i = j; i < c->t; ++i) {
+          const int64_t k = m * c->T1 + tri_index(i, j);
+          c->a_slot[k] = c->home[k] = s++;
+        }
+    }
+  }
   // reset the mutable executor state
   for (int64_t k = 0; k < T; ++k) {
     p->cur0[k] = c->a_slot[k];
-    p->alt0[k] = (int32_t)(c->a_slot[k] < T ? k + T : k);
+    p->alt0[k] = alt_slot_of(c, k);
   }
   CK(c, cudaMemcpyAsync(p->d_indeg, p->indeg0.data(), nx * 4, cudaMemcpyHostToDevice, st));
   CK(c, cudaMemsetAsync(p->d_done, 0, nx * 4, st));
   CK(c, cudaMemcpyAsync(p->d_cur, p->cur0.data(), p->nlogical * 4, cudaMemcpyHostToDevice, st));
   CK(c, cudaMemcpyAsync(p->d_alt, p->alt0.data(), p->nlogical * 4, cudaMemcpyHostToDevice, st));
-  CK(c, cudaMemcpyAsync(p->d_queue, p->q_init.data(), p->q_off[NLEV] * 8, cudaMemcpyHostToDevice, st));
-  CK(c, cudaMemsetAsync(p->d_head, 0, NLEV * 4, st));
-  CK(c, cudaMemcpyAsync(p->d_tail, p->tail0.data(), NLEV * 4, cudaMemcpyHostToDevice, st));
+  const int NQ = p->nranks * NLEV;
+  CK(c, cudaMemcpyAsync(p->d_queue, p->q_init.data(), p->q_off[NQ] * 8, cudaMemcpyHostToDevice, st));
+  CK(c, cudaMemsetAsync(p->d_head, 0, NQ * 4, st));
+  CK(c, cudaMemcpyAsync(p->d_tail, p->tail0.data(), NQ * 4, cudaMemcpyHostToDevice, st));
+  CK(c, cudaMemsetAsync(p->d_idle, 0, (size_t)c->nsm * 8, st));
   const int32_t ctr[2] = {(int32_t)nx, 0};
   CK(c, cudaMemcpyAsync(p->d_ctr, ctr, 8, cudaMemcpyHostToDevice, st));
   CK(c, cudaMemsetAsync(p->d_err, 0xff, 8, st));
@@ -1551,7 +1657,12 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
   P.cur_slot = p->d_cur;
   P.alt_slot = p->d_alt;
   P.queue = p->d_queue;
-  for (int l = 0; l <= NLEV; ++l) P.q_off[l] = p->q_off[l];
+  for (int l = 0; l <= NLEV; ++l) P.q_off[l] = p->nranks == 1 ? p->q_off[l] : 0;
+  P.nranks = p->nranks;
+  P.q_offs = p->d_qoffs;
+  P.cta_idle = p->d_idle;
+  // ranks in one launch: the same number of CTAs (SMs) per rank
+  p->grid = p->nranks == 1 ? c->nsm : (int64_t)p->nranks * (c->nsm / p->nranks);
   P.q_head = p->d_head;
   P.q_tail = p->d_tail;
   P.remaining = p->d_ctr;
@@ -1638,7 +1749,7 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
       return rc2;
     }
   }
-  CK(c, launch_exec(c->tmK, c->tmM, c->tmE, P, (int)c->b, c->nsm, st));
+  CK(c, launch_exec(c->tmK, c->tmM, c->tmE, P, (int)c->b, (int)p->grid, st));
   CK(c, cudaEventRecord(p->ev1, st));
   if (io)  // executor done (or aborted): release every copy group still waiting
     CK(c, cudaMemsetAsync(p->d_depart_count, 0x7f, T * 4, st));
@@ -1754,6 +1865,8 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
   }
   // success: adopt the renamed slots of the matrix tiles
   CK(c, cudaMemcpy(c->a_slot.data(), p->d_cur, T * 4, cudaMemcpyDeviceToHost));
+  p->h_idle.resize(p->grid);
+  CK(c, cudaMemcpy(p->h_idle.data(), p->d_idle, p->grid * 8, cudaMemcpyDeviceToHost));
   if (io && !(c->T1 == 1 && c->b == c->bp)) {  // next run: enqueue departures in the observed order
     std::vector<int32_t> seq(T);
     CK(c, cudaMemcpy(seq.data(), p->d_depart_seq, T * 4, cudaMemcpyDeviceToHost));

@@ -1186,13 +1186,23 @@ __device__ __noinline__ void run_special(const Job& jb, const ItemInfo& it, cons
 }
 
 // ---------------------------------------------------------------- scheduler (device side)
+// Queue geometry: level `lev` of the queue set starting at qb (= rank * NLEV
+// when ranks are emulated in one launch, else 0).
+__device__ __forceinline__ int64_t qoff(const ExecParams& P, int qb, int lev) {
+  return P.nranks > 1 ? __ldg(P.q_offs + qb + lev) : P.q_off[lev];
+}
+__device__ __forceinline__ int cta_qb(const ExecParams& P) {
+  return P.nranks > 1 ? (int)(blockIdx.x % (unsigned)P.nranks) * NLEV : 0;
+}
+
 __device__ __forceinline__ void push_task(const ExecParams& P, int s, int phase) {
   const TaskDev& t = P.tasks[s];
   if (t.flags & TF_EXTERNAL) return;  // RECV: completed by the inbox poller
   const int lev = t.level;
+  const int qb = P.nranks > 1 ? t.rank * NLEV : 0;  // the queue set of the task's rank
   const int n = group_items(t.kind, P.R, phase);
-  const int pos = atomicAdd(&P.q_tail[lev], n);
-  unsigned long long* q = P.queue + P.q_off[lev] + pos;
+  const int pos = atomicAdd(&P.q_tail[qb + lev], n);
+  unsigned long long* q = P.queue + qoff(P, qb, lev) + pos;
   for (int i = 0; i < n; ++i)
     st_release_u64(q + i, ((unsigned long long)(s + 1) << 32) | ((unsigned)phase << 16) | (unsigned)i);
 }
@@ -1228,12 +1238,12 @@ struct OwnedTicket {
 // entry is read speculatively alongside the CAS (queue entries are written
 // once per run), then ordered with an acquire fence. Returns 0 when nothing
 // could be claimed.
-__device__ __forceinline__ unsigned long long claim_item(const ExecParams& P, int h, int t, int minback,
+__device__ __forceinline__ unsigned long long claim_item(const ExecParams& P, int qb, int h, int t, int minback,
                                                          bool tickets, OwnedTicket* own) {
   const int lane = threadIdx.x & 31;
   if (own && own->lev >= 0) {
     unsigned long long v = 0;
-    if (lane == 0) v = ld_acquire_u64(P.queue + P.q_off[own->lev] + own->pos);
+    if (lane == 0) v = ld_acquire_u64(P.queue + qoff(P, qb, own->lev) + own->pos);
     v = __shfl_sync(0xffffffffu, v, 0);
     if (v) {
       own->lev = -1;
@@ -1252,10 +1262,11 @@ __device__ __forceinline__ unsigned long long claim_item(const ExecParams& P, in
         // (148 producers CAS-ing one head convoy at about one claim per round
         // trip). A ticket past the current tail is kept as the CTA's owned
         // position (see OwnedTicket) unless no push can ever reach it.
-        const int pos = atomicAdd(P.q_head + lev, 1);
-        if (pos < P.q_off[lev + 1] - P.q_off[lev]) {
-          if (pos < ld_relaxed_s32(P.q_tail + lev) || !own) {  // pushed or reserved: the store is in flight
-            v = wait_entry(P, P.queue + P.q_off[lev] + pos);
+        const int pos = atomicAdd(P.q_head + qb + lev, 1);
+        const int64_t o0 = qoff(P, qb, lev);
+        if (pos < qoff(P, qb, lev + 1) - o0) {
+          if (pos < ld_relaxed_s32(P.q_tail + qb + lev) || !own) {  // pushed or reserved: the store is in flight
+            v = wait_entry(P, P.queue + o0 + pos);
             got = 1;
           } else {
             owned = pos;
@@ -1263,9 +1274,9 @@ __device__ __forceinline__ unsigned long long claim_item(const ExecParams& P, in
         }
         h = t;  // drained by this claim round (or past the level's capacity)
       } else {
-        const unsigned long long* slot = P.queue + P.q_off[lev] + h;
+        const unsigned long long* slot = P.queue + qoff(P, qb, lev) + h;
         v = ld_relaxed_u64(slot);
-        const int prev = atomicCAS(P.q_head + lev, h, h + 1);
+        const int prev = atomicCAS(P.q_head + qb + lev, h, h + 1);
         if (prev == h) {
           if (v == 0ull) v = wait_entry(P, slot);  // pusher reserved the slot, store in flight
           fence_acq_rel_gpu();
@@ -1295,36 +1306,45 @@ __device__ __forceinline__ unsigned long long claim_item(const ExecParams& P, in
 __device__ __forceinline__ unsigned long long try_pop(const ExecParams& P) {
   static_assert(NLEV <= 32, "one lane per priority level");
   const int lane = threadIdx.x & 31;
+  const int qb = cta_qb(P);
   int h = 0, t = 0;
   if (lane < NLEV) {
-    h = ld_relaxed_s32(P.q_head + lane);
-    t = ld_relaxed_s32(P.q_tail + lane);
+    h = ld_relaxed_s32(P.q_head + qb + lane);
+    t = ld_relaxed_s32(P.q_tail + qb + lane);
   }
   // CAS only: an overshooting ticket could wait for a push behind this CTA's own item
-  return claim_item(P, h, t, P.prefetch_min, false, nullptr);
+  return claim_item(P, qb, h, t, P.prefetch_min, false, nullptr);
 }
 
 // Blocking pop (all 32 lanes): spins until an item is claimed, every task is
 // complete, the run aborted, or the watchdog fires.
 __device__ unsigned long long pop_item(const ExecParams& P, OwnedTicket& own) {
   const int lane = threadIdx.x & 31;
+  const int qb = cta_qb(P);
   unsigned last_prog = ld_relaxed_u32(P.progress);
   unsigned long long t_last = globaltimer();
+  const unsigned long long t_enter = t_last;
   unsigned spin = 0;
   while (true) {
     // one round trip: queue bounds of every level and the stop flags together
     int h = 0, t = 0, ab = 0, rem = 1;
     if (lane < NLEV) {
-      h = ld_relaxed_s32(P.q_head + lane);
-      t = ld_relaxed_s32(P.q_tail + lane);
+      h = ld_relaxed_s32(P.q_head + qb + lane);
+      t = ld_relaxed_s32(P.q_tail + qb + lane);
     }
     if (lane == 0) {
       ab = ld_relaxed_s32(P.abort_flag);
       rem = ld_relaxed_s32(P.remaining);
     }
-    if (__shfl_sync(0xffffffffu, ab || rem <= 0, 0)) return POP_EXIT;
-    const unsigned long long v = claim_item(P, h, t, 1, true, &own);
-    if (v) return v;
+    if (__shfl_sync(0xffffffffu, ab || rem <= 0, 0)) {
+      if (P.cta_idle && spin > 0 && lane == 0) P.cta_idle[blockIdx.x] += globaltimer() - t_enter;
+      return POP_EXIT;
+    }
+    const unsigned long long v = claim_item(P, qb, h, t, 1, true, &own);
+    if (v) {
+      if (P.cta_idle && spin > 0 && lane == 0) P.cta_idle[blockIdx.x] += globaltimer() - t_enter;
+      return v;
+    }
     __nanosleep(spin < 64 ? 32 : 256);
     ++spin;
     if ((spin & 255) == 0) {  // watchdog: no item completed anywhere for 30 s

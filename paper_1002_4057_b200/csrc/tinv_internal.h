@@ -61,7 +61,8 @@ struct TaskDev {
   int8_t flags;
   int8_t level;
   int16_t nphases;  // phase groups (queue round trips) of the task
-  int16_t pad;
+  int8_t rank;      // ranks-in-one-launch plans: the rank (CTA group) that runs it; else 0
+  int8_t pad;
   int32_t nitems;   // items over all phases
   int32_t out;     // logical tile ids
   int32_t in0;
@@ -88,8 +89,14 @@ struct ExecParams {
   int32_t* alt_slot;
   unsigned long long* queue;       // all levels back to back
   int64_t q_off[NLEV + 1];         // level l occupies queue[q_off[l] .. q_off[l+1])
-  int32_t* q_head;                 // NLEV
-  int32_t* q_tail;                 // NLEV
+  int32_t* q_head;                 // NLEV (x nranks)
+  int32_t* q_tail;                 // NLEV (x nranks)
+  // ranks emulated in one launch (nranks > 1): CTA b is rank b % nranks and
+  // claims only from its rank's NLEV levels; level l of rank r occupies
+  // queue[q_offs[r*NLEV + l] .. q_offs[r*NLEV + l + 1]) (q_off unused)
+  int32_t nranks;
+  const int64_t* q_offs;           // nranks * NLEV + 1
+  unsigned long long* cta_idle;    // optional: per CTA, ns its producer waited for a claimable item
   int32_t* remaining;              // tasks not yet completed
   int32_t* abort_flag;
   unsigned long long* err;         // packed min failure (ref task << 32 | code << 24 | index)

@@ -88,12 +88,14 @@ def rank_slice(d: DistStream, r: int):
     return pos
 
 
-def transfer_plan(d: DistStream, rank: int = -1):
+def transfer_plan(d: DistStream, rank: int = -1, with_ranks: bool = False):
     """Table + aux (dest, seq) + inbox length with SEND / RECV pseudo-tasks.
 
     rank -1: every rank's tasks (one-GPU execution, sequence = transfer index);
-    rank r: the tasks of rank r, sequence numbers counted per receiver."""
-    rows, aux, src = [], [], []
+    rank r: the tasks of rank r, sequence numbers counted per receiver.
+    with_ranks: also the rank that runs each row (task owner, SEND: sender,
+    RECV: receiver), for plans that emulate the ranks in one launch."""
+    rows, aux, src, who = [], [], [], []
     per_dest = {}
     nrecv = 0
     for k in range(len(d.table)):
@@ -103,6 +105,7 @@ def transfer_plan(d: DistStream, rank: int = -1):
                 rows.append(f)
                 aux.append((-1, -1))
                 src.append(int(d.ref[k]))
+                who.append(int(d.owner[k]))
             continue
         dst, snd = int(d.dest[k]), int(d.owner[k])
         if rank < 0:
@@ -120,31 +123,44 @@ def transfer_plan(d: DistStream, rank: int = -1):
             rows.append(send)
             aux.append((dst, seq))
             src.append(-1)
+            who.append(snd)
         if rank < 0 or dst == rank:
             rows.append(recv)
             aux.append((dst, seq))
             src.append(-1)
+            who.append(dst)
         if rank < 0 or dst == rank:
             nrecv = max(nrecv, seq + 1)
-    return np.array(rows, np.int32), np.array(aux, np.int32), nrecv, np.array(src, np.int64)
+    out = (np.array(rows, np.int32), np.array(aux, np.int32), nrecv, np.array(src, np.int64))
+    return out + (np.array(who, np.int32),) if with_ranks else out
 
 
 def execute_distributed(stream: TaskStream, a, grid=(1, 2), transport="loopback"):
     """Run `stream` as distributed over `grid` on one B200: transport
-    "loopback" (transfers as device copies) or "device" (the SEND / RECV
-    protocol with the local pool standing in for peers). Same results and
-    errors as `execute` (task ids refer to `stream`)."""
+    "loopback" (transfers as device copies), "device" (the SEND / RECV
+    protocol with the local pool standing in for peers, any SM runs any
+    rank's task) or "ranks" (the same protocol with every rank on its own
+    group of nsm / P*Q SMs and its own priority queues: the multi-GPU
+    schedule emulated in one launch; the returned DistStream's `last_run`
+    holds the kernel time and per-CTA idle times). Same results and errors
+    as `execute` (task ids refer to `stream`)."""
     from .scheduler import ExecutionError, InvalidStreamError, _cause, _run
     from .tile_matrix import _DEVICE
     if a.t != stream.t:
         raise InvalidStreamError(f"stream generated for t={stream.t} cannot run on a t={a.t} matrix")
     d = distribute(stream, grid, a.label)
-    if transport == "device":
-        table, aux, nrecv, src = transfer_plan(d, -1)
+    if transport in ("device", "ranks"):
+        table, aux, nrecv, src, who = transfer_plan(d, -1, with_ranks=True)
         ctx = a._device()
-        plan = _native.Plan.xfer(ctx, table, stream.t, aux, nrecv)
-        rc, err, _ = plan.run()
+        if transport == "ranks":
+            plan = _native.Plan.ranks(ctx, table, stream.t, aux, nrecv, who, d.world)
+        else:
+            plan = _native.Plan.xfer(ctx, table, stream.t, aux, nrecv)
+        rc, err, ms = plan.run()
         msg = plan.msg
+        if rc == _native.OK and transport == "ranks":
+            idle, rk = plan.cta_idle()
+            d.last_run = {"kernel_ms": ms, "cta_idle_ns": idle, "cta_rank": rk}
         plan.close()
         if rc != _native.OK:
             if err.task_id < 0 or src[err.task_id] < 0:

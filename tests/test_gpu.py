@@ -416,6 +416,26 @@ def test_distributed_device_transport_bitwise(grid):
     assert np.array_equal(P.to_dense(tm), P.to_dense(ref))
 
 
+@pytest.mark.parametrize("grid", [(1, 2), (1, 3), (2, 2), (2, 4)])
+def test_distributed_ranks_in_one_launch_bitwise(grid):
+    # every rank on its own group of nsm / P*Q CTAs with its own priority
+    # queues (tinv_plan_create_ranks): the multi-GPU schedule in one launch
+    from paper_1002_4057_b200.distributed import execute_distributed
+    n, b = 1280, 128
+    a = O.spd_matrix(n, 12, 0.5)
+    for cfg in (P.VariantConfig(P.Placement.OUT_OF_PLACE), P.VariantConfig(P.Placement.IN_PLACE, "UDU", True)):
+        s = P.gen_inversion(n // b, cfg)
+        ref = P.from_dense(a, b)
+        P.execute(s, ref)
+        tm = P.from_dense(a, b)
+        d = execute_distributed(s, tm, grid, transport="ranks")
+        assert np.array_equal(P.to_dense(tm), P.to_dense(ref))
+        run = d.last_run
+        world = grid[0] * grid[1]
+        assert len(run["cta_idle_ns"]) % world == 0 and set(run["cta_rank"].tolist()) == set(range(world))
+        assert (run["cta_idle_ns"] >= 0).all() and (run["cta_idle_ns"] <= run["kernel_ms"] * 1e6 * 1.01).all()
+
+
 # ---------------------------------------------------------------- streamed host I/O (tinv_plan_exec_host)
 def _pinned(shape):
     import torch
@@ -462,6 +482,15 @@ def test_streamed_lower_mode_and_batched():
     assert np.array_equal(np.nan_to_num(hx), np.nan_to_num(lower))
     assert sp.run()[0] == _native.ERR_BAD_ARG  # a STREAM_IO plan needs host buffers
     sp.close()
+    # a staged run on the same store after the streamed run re-homed its tiles
+    # (column-major home slots, api.cu plan_exec_impl): same bits
+    ctx.put_dense(a)
+    plan2 = _native.Plan(ctx, s.table(), t, np.array(sorted(s.barriers), np.int64))
+    assert plan2.run()[0] == 0
+    again = np.full((n, n), np.nan)
+    ctx.get_dense(again, _native.DENSE_LOWER)
+    plan2.close()
+    assert np.array_equal(np.nan_to_num(again), np.nan_to_num(lower))
     ctx.close()
     rng = np.random.default_rng(4)
     g = rng.standard_normal((40, 256, 256))
