@@ -63,6 +63,8 @@ def parse():
     p.add_argument("--no-steps", action="store_true", help="skip the per-step / barriered breakdown")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-load", action="store_true",
+                   help="skip the load report (per-SM busy, 2x4 ranks emulated in one launch, schedule model)")
     p.add_argument("--cpu-sample-n", type=int, default=None)
     p.add_argument("--cpu-worker", action="store_true", help=argparse.SUPPRESS)
     p.add_argument("--shift", type=float, default=None, help=argparse.SUPPRESS)
@@ -249,7 +251,11 @@ def main():
     n = args.n or wl[0]
     nb = args.nb or wl[1]
     if args.loops is None:
-        args.loops = "DDU" if args.workload == "c3" else "UDU"
+        # one GPU at c3: DDU (result tiles final progressively: the streamed e2e
+        # overlaps its device->host copies; kernel time = UDU's). Distributed
+        # (N > 1): UDU -- step 1 under D chains ~t^2/2 GEMMs on the critical
+        # path (tools/scaling_model.py: 180 vs 62 ms at c3).
+        args.loops = "DDU" if args.workload == "c3" and world == 1 else "UDU"
     batch = args.batch or wl[2]
     if args.cpu_sample_n is None:
         args.cpu_sample_n = min(n, 8192) if batch == 1 else n
@@ -446,6 +452,20 @@ def main():
     jobs = 1 if mg is not None else world  # distributed: all ranks share one matrix per step
     value = jobs * flops / (ms_step * 1e-3) / 1e9
     kern_avg = max_over_ranks(statistics.mean(kern_ms))
+    # measured load: per-CTA scheduler idle time of the
+    # last timed launch -> busy fraction per SM (per rank when distributed)
+    load = None
+    if not fused and not args.no_load:
+        idle, _ = plan.cta_idle()
+        busy = 1.0 - idle * 1e-6 / max(kern_ms[-1], 1e-9)
+        load = {"kernel_ms": kern_ms[-1], "sms": int(len(idle)),
+                "sm_busy_frac": {"min": float(busy.min()), "mean": float(busy.mean()), "max": float(busy.max())},
+                "source": "per-CTA idle ns of the executor's scheduler warp (tinv_plan_cta_idle), last timed step"}
+        if dist is not None:
+            v = torch.tensor([float(busy.mean())], dtype=torch.float64, device="cuda")
+            allb = [torch.zeros_like(v) for _ in range(world)]
+            dist.all_gather(allb, v)
+            load["rank_busy_frac"] = [float(x.item()) for x in allb]
     achieved = flops / (world if mg is not None else 1) / (kern_avg * 1e-3) / 1e12
     if mg is not None:  # gather the owned tiles for the check below
         x *= owned_mask(n, nb, mg.grid, rank, "cuda")
@@ -471,9 +491,41 @@ def main():
                                                         * torch.linalg.matrix_norm(xc, 1) * eps)).max())
         sym_err = float((xc - xc.transpose(-1, -2)).abs().max())
         del r, eye, ac, xc
-    if batch == 1 and world == 1 and t >= 8:  # per-GPU flop-load balance of the 2D block-cyclic distribution
-        from paper_1002_4057_b200.distributed import distribute
-        config["load_max_over_mean_if_2x4"] = round(distribute(s, (2, 4)).stats(nb)["load_max_over_mean"], 4)
+
+    # the multi-GPU schedule on this one B200: 2x4 ranks in ONE launch, each on
+    # 18 SMs with its own queues, tile versions through SEND / RECV (measured);
+    # and the schedule model's prediction for a real 8 x B200 node
+    if load is not None and batch == 1 and world == 1 and t >= 16 and mg is None:
+        from paper_1002_4057_b200.distributed import distribute, transfer_plan
+        s_u = P.gen_inversion(t, P.VariantConfig(P.Placement(args.placement), "UDU", True))
+        d8 = distribute(s_u, (2, 4))
+        tb, ax, nrv, _, who = transfer_plan(d8, -1, with_ranks=True)
+        bp = -(-nb // 128) * 128
+        fits = torch.cuda.mem_get_info()[0] > 1.2 * nrv * bp * bp * 8 + (1 << 30)  # receive tiles
+        pr = _native.Plan.ranks(ctx, tb, t, ax, nrv, who, 8) if fits else None
+        if pr is None:
+            load["emulated_2x4"] = {"note": f"not run: {nrv} receive tiles exceed free HBM"}
+        elif pr.rc == 0:
+            ctx.put_dense_device(a.data_ptr(), n)
+            rc8, _, ms8 = pr.run()
+            if rc8 == 0:
+                idle8, rk8 = pr.cta_idle()
+                rb = [float(ms8 - idle8[rk8 == r].mean() * 1e-6) for r in range(8)]
+                load["emulated_2x4"] = {
+                    "kernel_ms": ms8, "sms_per_rank": int((rk8 == 0).sum()), "rank_busy_ms": rb,
+                    "busy_max_over_mean": max(rb) / statistics.mean(rb),
+                    "flop_load_max_over_mean": d8.stats(nb)["load_max_over_mean"], "transfers": nrv,
+                    "loops": "UDU"}
+        if pr is not None:
+            pr.close()
+        try:
+            t1m, _ = _native.model_run(n, nb, s_u.table(), t, sorted(s_u.barriers))
+            t8m, b8 = _native.model_run(n, nb, tb, t, aux=ax, nrecv=nrv, rank_of=who, nranks=8)
+            load["model_8gpu"] = {"t1_ms": t1m / 1e3, "t8_ms": t8m / 1e3, "efficiency": t1m / (8 * t8m),
+                                  "source": "csrc/model.cu schedule model, 8 x 148 SMs, _native.MODEL_COST "
+                                            "(validated against the one-launch emulation, profiles/r02)"}
+        except Exception as exc:  # noqa: BLE001
+            load["model_8gpu"] = {"error": repr(exc)[:200]}
 
     # per-step device times (each step on the previous one's
     # output, same store) and pipelined vs barriered full inversion
@@ -613,6 +665,8 @@ def main():
             "clocks": clk.summary(),
             "e2e": e2e, "cpu_baseline": cpu,
         }
+        if load is not None:
+            out["load"] = load
         if steps_breakdown is not None:
             out["steps_breakdown"] = steps_breakdown
         print(json.dumps(out))

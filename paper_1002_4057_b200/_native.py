@@ -206,6 +206,9 @@ def dag_paths(table, barriers, weight=None, include_copies=False):
 
 
 MODEL_COST_KEYS = ("blk", "item", "bpotrf", "btrtri", "bcopy", "send", "link", "mask", "hop")
+# Item costs (us) of the schedule model, calibrated on the B200 (tools/scaling_model.py)
+MODEL_COST = {"blk": 16.8, "item": 3.2, "bpotrf": 65.0, "btrtri": 10.7, "bcopy": 1.0, "send": 1.5, "link": 3.0,
+              "mask": 0.6, "hop": 10.0}
 
 
 KIND_NAMES = ("COPY", "POTRF", "TRSM", "SYRK_SUB", "SYRK_ADD_T", "GEMM", "TRTRI", "TRMM_LEFT", "TRMM_RIGHT_NEG",
@@ -218,6 +221,7 @@ def model_run(n, b, table, t, barriers=(), aux=None, nrecv=0, rank_of=None, nran
     L = lib()
     table = np.ascontiguousarray(table, dtype=np.int32)
     bars = np.ascontiguousarray(barriers, dtype=np.int64)
+    cost = MODEL_COST if cost is None else cost
     c = np.array([cost[k] for k in MODEL_COST_KEYS], dtype=np.float64)
     out = np.zeros(nranks + 2, dtype=np.float64)
     ax = None if aux is None else np.ascontiguousarray(aux, dtype=np.int32)

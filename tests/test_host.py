@@ -218,3 +218,32 @@ def test_fused_batched_engine_selection_and_abi_validation():
     assert L.tinv_batch_small_host(fake, fake, 1, 257, 0, ctypes.byref(fm), ctypes.byref(fi), None) == \
         _native.ERR_BAD_ARG
     assert (fm.value, fi.value) == (-1, -1)
+
+
+def test_schedule_model_host_only():
+    """csrc/model.cu: the executor's schedule simulated on the host (no GPU):
+    deadlock-free on single-GPU and transfer plans, busy SM-time independent of
+    the SM count, makespan bounded below by busy/SMs and by the unlimited-SM run."""
+    from paper_1002_4057_b200.distributed import distribute, transfer_plan
+    n, b = 2048, 256
+    t = n // b
+    s = P.gen_inversion(t, P.VariantConfig(P.Placement.OUT_OF_PLACE, "UDU", True))
+    mk, busy = _native.model_run(n, b, s.table(), t, sorted(s.barriers), sms_per_rank=148)
+    mk4, busy4 = _native.model_run(n, b, s.table(), t, sorted(s.barriers), sms_per_rank=4)
+    cp, _ = _native.model_run(n, b, s.table(), t, sorted(s.barriers), sms_per_rank=100000)
+    assert abs(busy[0] - busy4[0]) < 1e-6 * busy[0]
+    assert mk4 >= busy4[0] / 4 - 1e-6 and mk >= cp - 1e-6 and mk4 >= mk - 1e-6
+    for grid in ((1, 2), (2, 2), (2, 4)):
+        d = distribute(s, grid)
+        table, aux, nrecv, _, who = transfer_plan(d, -1, with_ranks=True)
+        w = grid[0] * grid[1]
+        mkd, bd, crit = _native.model_run(n, b, table, t, aux=aux, nrecv=nrecv, rank_of=who, nranks=w,
+                                          sms_per_rank=148 // w, with_crit=True)
+        assert len(bd) == w and (bd > 0).all() and mkd > 0
+        assert abs(sum(crit.values()) - mkd) < 1e-6 * mkd  # the critical chain spans the run
+
+
+def test_rank_plan_rejects_bad_ranks():
+    with pytest.raises(_native.NativeError):
+        s = P.gen_inversion(4, P.VariantConfig())
+        _native.model_run(512, 128, s.table(), 4, sorted(s.barriers), nranks=9, rank_of=np.zeros(len(s), np.int32))

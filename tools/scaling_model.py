@@ -28,8 +28,7 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-COST = {"blk": 16.8, "item": 3.2, "bpotrf": 65.0, "btrtri": 10.7, "bcopy": 1.0, "send": 1.5, "link": 3.0,
-        "mask": 0.6, "hop": 10.0}
+from paper_1002_4057_b200._native import MODEL_COST as COST  # noqa: E402
 CONFIGS = {"c1": (1024, 128, "out", "UDU"), "c2": (8192, 256, "out", "UDU"), "c3": (32768, 512, "out", "UDU"),
            "c5": (65536, 1024, "out", "UDU")}
 
