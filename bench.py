@@ -63,6 +63,8 @@ def parse():
     p.add_argument("--no-steps", action="store_true", help="skip the per-step / barriered breakdown")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--share-slots", action="store_true",
+                   help="memory-constrained renaming: working tiles share store slots by live range")
     p.add_argument("--no-load", action="store_true",
                    help="skip the load report (per-SM busy, 2x4 ranks emulated in one launch, schedule model)")
     p.add_argument("--cpu-sample-n", type=int, default=None)
@@ -405,7 +407,8 @@ def main():
         config["parallelism"] = f"2d-block-cyclic {mg.grid[0]}x{mg.grid[1]} (tile versions over NVLink peer memory)"
         config["load_max_over_mean"] = st["load_max_over_mean"]
         config["transfers"] = st["transfers"]
-    plan = None if fused else mg.plan if mg is not None else _native.Plan(ctx, table, t, bars)
+    plan = None if fused else mg.plan if mg is not None else _native.Plan(
+        ctx, table, t, bars, _native.SHARE_SLOTS if args.share_slots else 0)
     if plan is not None and plan.rc != 0:
         raise RuntimeError(plan.msg)
     stats = {"engine": "fused", "ctas": batch, "block_ops_per_matrix": 56 if n > 192 else None} if fused \
@@ -452,6 +455,7 @@ def main():
     jobs = 1 if mg is not None else world  # distributed: all ranks share one matrix per step
     value = jobs * flops / (ms_step * 1e-3) / 1e9
     kern_avg = max_over_ranks(statistics.mean(kern_ms))
+    store_bytes = ctx.store_bytes() if ctx is not None else None
     # measured load: per-CTA scheduler idle time of the
     # last timed launch -> busy fraction per SM (per rank when distributed)
     load = None
@@ -660,6 +664,7 @@ def main():
                                         f"{DGEMM_TFLOPS} TF/s for context; MEASURED_PEAKS.json has no FP64 entry"},
             "pct_fp64_peak": 100.0 * value / world / 1e3 / DMMA_PEAK_TFLOPS,  # per GPU
             "kernel_ms": kern_avg, "plan": stats,
+            "store_bytes": None if ctx is None else store_bytes, "share_slots": bool(args.share_slots),
             "residual": res, "symmetry_err": sym_err,
             "gpu_launches": (1 if fused else 3) * args.steps,
             "clocks": clk.summary(),

@@ -76,6 +76,8 @@ extern "C" {
 #define TINV_TRACE 2u           /* record per-task device timestamps          */
 #define TINV_KEEP_ON_FAILURE 4u /* snapshot the matrix; restore it if a task fails */
 #define TINV_STREAM_IO 8u       /* plan for tinv_plan_exec_host: tile arrivals and departures are tasks */
+#define TINV_SHARE_SLOTS 16u    /* memory-constrained renaming: working tiles (B / C copies, aux) share
+                                   slots by live range in stream order, reuse ordered by added edges */
 
 /* tinv_get_dense modes */
 #define TINV_DENSE_LOWER_TILES 0 /* write only the lower tiles (to_dense on them) */
@@ -107,6 +109,8 @@ int tinv_create(tinv_ctx** ctx, int64_t n, int64_t b, int device);
 int tinv_create_batch(tinv_ctx** ctx, int64_t batch, int64_t n, int64_t b, int device);
 int tinv_destroy(tinv_ctx* ctx);
 int tinv_shape(const tinv_ctx* ctx, int64_t* n, int64_t* b, int64_t* t, int64_t* padded_b);
+/* bytes of the context's device tile store (grows to the largest plan run on it) */
+int tinv_store_bytes(const tinv_ctx* ctx, int64_t* bytes);
 /* run the context's device work on a caller-owned cudaStream_t (NULL restores
  * the context's own stream), so callers can time it with their own events */
 int tinv_set_stream(tinv_ctx* ctx, void* cuda_stream);
@@ -198,19 +202,20 @@ int tinv_plan_cta_idle(const tinv_plan* p, int64_t* idle_ns, int32_t* rank, int6
  * simulation of the plan tinv_plan_create / _create_ranks would compile for
  * an n x n matrix of b x b tiles, run by nranks GPUs of sms_per_rank SMs
  * each with the executor's claim rules (per-rank level FIFOs, phase groups,
- * work items). aux / nrecv / rank_of as in tinv_plan_create_ranks (NULL and 0
+ * work items). flags: 0 or TINV_SHARE_SLOTS. aux / nrecv / rank_of as in tinv_plan_create_ranks (NULL and 0
  * for a single-GPU stream; rank_of NULL when nranks == 1). cost[9], in us:
  * block product (128^3), per-item overhead, 128-block Cholesky+inverse,
  * 128-block triangular inverse, 128-block copy, SEND per 128-block, link
  * latency, masked-block fraction, ready -> start latency of an item. out[0] = makespan (us), out[1..nranks] =
- * busy SM-us per rank, out[nranks+1] = tasks never run (0 unless deadlock).
+ * busy SM-us per rank, out[nranks+1] = tasks never run (0 unless deadlock),
+ * out[nranks+2] = tile slots the plan's device store needs (2T + working).
  * crit_kind[17] (or NULL): the chain of releasing predecessors ending at the
  * last task to finish, its time (release -> finish) summed per task kind
  * (TINV_* kinds 0-10, then INV, SEND, RECV, ARRIVE, DEPART, POTRF_INV). */
 int tinv_model_run(int64_t n, int64_t b, const int32_t* table, int64_t ntasks, int32_t stream_t,
                    const int64_t* barriers, int64_t nbar, const int32_t* aux, int64_t nrecv,
-                   const int32_t* rank_of, int32_t nranks, int32_t sms_per_rank, const double* cost,
-                   double* out, double* crit_kind);
+                   const int32_t* rank_of, int32_t nranks, int32_t sms_per_rank, uint32_t flags,
+                   const double* cost, double* out, double* crit_kind);
 
 /* Multi-process runs (one rank per B200 of a node): size the store for
  * `plan` and export this rank's pool and inbox as CUDA IPC handles (64 bytes

@@ -17,13 +17,13 @@ LIB_PATH = os.environ.get("TINV_LIB") or os.path.join(_PKG, "libtileinv_b200.so"
 
 TASK_FIELDS = 16
 OK, ERR_NOT_SPD, ERR_SINGULAR, ERR_BAD_ARG, ERR_CUDA, ERR_STREAM, ERR_NO_DEVICE, ERR_INTERNAL = range(8)
-SERIAL, TRACE, KEEP_ON_FAILURE, STREAM_IO = 1, 2, 4, 8
+SERIAL, TRACE, KEEP_ON_FAILURE, STREAM_IO, SHARE_SLOTS = 1, 2, 4, 8, 16
 DENSE_LOWER, DENSE_SYMMETRIZE = 0, 1
 
 # every symbol include/tileinv_b200.h declares
 EXPORTS = (
     "tinv_abi_version", "tinv_device_count", "tinv_last_error", "tinv_create", "tinv_create_batch", "tinv_destroy",
-    "tinv_shape", "tinv_set_stream", "tinv_put_dense", "tinv_get_dense", "tinv_put_dense_device", "tinv_get_dense_device",
+    "tinv_shape", "tinv_store_bytes", "tinv_set_stream", "tinv_put_dense", "tinv_get_dense", "tinv_put_dense_device", "tinv_get_dense_device",
     "tinv_put_tile", "tinv_get_tile", "tinv_gen_stream", "tinv_dag_edges", "tinv_dag_paths", "tinv_dist_stream", "tinv_plan_create",
     "tinv_plan_create_xfer", "tinv_plan_create_ranks", "tinv_plan_cta_idle", "tinv_model_run", "tinv_ipc_export", "tinv_ipc_open", "tinv_ipc_reset", "tinv_plan_exec",
     "tinv_plan_exec_host", "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
@@ -71,6 +71,7 @@ def lib():
         "tinv_create_batch": ([ctypes.POINTER(_P), _I64, _I64, _I64, ctypes.c_int], ctypes.c_int),
         "tinv_destroy": ([_P], ctypes.c_int),
         "tinv_shape": ([_P, _I64P, _I64P, _I64P, _I64P], ctypes.c_int),
+        "tinv_store_bytes": ([_P, _I64P], ctypes.c_int),
         "tinv_set_stream": ([_P, _P], ctypes.c_int),
         "tinv_put_dense": ([_P, _DP, _I64], ctypes.c_int),
         "tinv_get_dense": ([_P, _DP, _I64, ctypes.c_int], ctypes.c_int),
@@ -91,7 +92,8 @@ def lib():
         "tinv_plan_create_ranks": ([_P, _I32P, _I64, _I32, _I32P, _I64, _I32P, _I32, _U32, ctypes.POINTER(_P),
                                     ctypes.POINTER(TinvErr)], ctypes.c_int),
         "tinv_plan_cta_idle": ([_P, _I64P, _I32P, _I64, _I64P], ctypes.c_int),
-        "tinv_model_run": ([_I64, _I64, _I32P, _I64, _I32, _I64P, _I64, _I32P, _I64, _I32P, _I32, _I32, _DP, _DP, _DP],
+        "tinv_model_run": ([_I64, _I64, _I32P, _I64, _I32, _I64P, _I64, _I32P, _I64, _I32P, _I32, _I32, _U32, _DP, _DP,
+                            _DP],
                            ctypes.c_int),
         "tinv_ipc_export": ([_P, _P, ctypes.c_char_p, ctypes.c_char_p], ctypes.c_int),
         "tinv_ipc_open": ([_P, _I32, _I32, ctypes.c_char_p, ctypes.c_char_p], ctypes.c_int),
@@ -216,21 +218,22 @@ KIND_NAMES = ("COPY", "POTRF", "TRSM", "SYRK_SUB", "SYRK_ADD_T", "GEMM", "TRTRI"
 
 
 def model_run(n, b, table, t, barriers=(), aux=None, nrecv=0, rank_of=None, nranks=1, sms_per_rank=148,
-              cost=None, with_crit=False):
+              cost=None, with_crit=False, flags=0):
     """Schedule model (tinv_model_run, host only) -> (makespan us, busy SM-us per rank)."""
     L = lib()
     table = np.ascontiguousarray(table, dtype=np.int32)
     bars = np.ascontiguousarray(barriers, dtype=np.int64)
     cost = MODEL_COST if cost is None else cost
     c = np.array([cost[k] for k in MODEL_COST_KEYS], dtype=np.float64)
-    out = np.zeros(nranks + 2, dtype=np.float64)
+    out = np.zeros(nranks + 3, dtype=np.float64)
     ax = None if aux is None else np.ascontiguousarray(aux, dtype=np.int32)
     rk = None if rank_of is None else np.ascontiguousarray(rank_of, dtype=np.int32)
     crit = np.zeros(17, dtype=np.float64)
     check(L.tinv_model_run(n, b, _ip(table), len(table), t, _lp(bars), len(bars), _ip(ax), nrecv, _ip(rk), nranks,
-                           sms_per_rank, _dp(c), _dp(out), _dp(crit)))
+                           sms_per_rank, flags, _dp(c), _dp(out), _dp(crit)))
     if out[nranks + 1] != 0:
         raise RuntimeError(f"model: {int(out[nranks + 1])} tasks never ran (deadlocked plan)")
+    model_run.last_slots = int(out[nranks + 2])  # tile slots of the plan's device store
     if with_crit:
         return float(out[0]), out[1:nranks + 1].copy(), {KIND_NAMES[k]: float(crit[k]) for k in range(17) if crit[k]}
     return float(out[0]), out[1:nranks + 1].copy()
@@ -274,6 +277,11 @@ class Context:
             self.close()
         except Exception:  # noqa: BLE001 - interpreter shutdown
             pass
+
+    def store_bytes(self):
+        v = ctypes.c_int64()
+        check(lib().tinv_store_bytes(self.h, ctypes.byref(v)), self.h)
+        return v.value
 
     def set_stream(self, stream_ptr):
         """Launch on a caller-owned cudaStream_t (int handle); 0 -> own stream."""

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <string>
 #include <map>
+#include <queue>
 #include <unordered_map>
 #include <vector>
 
@@ -227,6 +228,12 @@ int tinv_destroy(tinv_ctx* c) {
 int tinv_set_stream(tinv_ctx* c, void* stream) {
   if (!c) return TINV_ERR_BAD_ARG;
   c->st = stream ? (cudaStream_t)stream : c->own;
+  return TINV_OK;
+}
+
+int tinv_store_bytes(const tinv_ctx* c, int64_t* bytes) {
+  if (!c || !bytes) return TINV_ERR_BAD_ARG;
+  *bytes = c->pool_slots * c->slot_elems * 8;
   return TINV_OK;
 }
 
@@ -879,6 +886,94 @@ static void set_err(tinv_err* err, int32_t task, int32_t kind, int32_t code, int
 // nrecv: inbox length (receive tiles pinned at slots 2T + seq).
 // rank_of (n, or null) / nranks: ranks emulated in one launch -- task v runs
 // on the CTAs of rank rank_of[v] (tasks the planner inserts for v inherit it).
+namespace {
+struct XTouch {  // per exec task: the logical tiles it reads and writes, and whether its output is renamed
+  int32_t in0, in1, out;
+  bool renamed;
+};
+}  // namespace
+
+// does kind `k` write its output to the alternate (renamed) slot? (same rule as the item / priority loop)
+static bool renames(int kind, bool alias) {
+  return kind == TINV_TRMM_LEFT || kind == TINV_TRMM_RIGHT_NEG || kind == TINV_TRMM_LEFT_T || kind == TINV_LAUUM ||
+         kind == TINV_TRSM || kind == TINV_TRTRI ||
+         (alias && (kind == TINV_GEMM || kind == TINV_SYRK_SUB || kind == TINV_SYRK_ADD_T));
+}
+
+template <class XS>
+static std::vector<XTouch> xs_touch(const XS& xs, int64_t nx) {
+  std::vector<XTouch> v(nx);
+  for (int64_t u = 0; u < nx; ++u)
+    v[u] = {xs[u].in0, xs[u].in1, xs[u].out, renames(xs[u].kind, xs[u].in0 == xs[u].out || xs[u].in1 == xs[u].out)};
+  return v;
+}
+
+// Memory-constrained renaming (PAPER.md's closing open problem: performance
+// under a memory constraint). Working tiles (the B / C copies of the
+// out-of-place placement, INV and POTRF aux tiles) get slots by interval
+// coloring over their live ranges in stream order -- [first task that touches
+// the tile, last one] -- instead of one slot (pair) each. A tile that takes
+// over a slot group gets edges from every task that touched the previous
+// occupant to its first writer, so the reuse is safe under ANY schedule the
+// executor picks (all those tasks precede it in stream order: the DAG stays
+// acyclic). Out-of-place, B dies within step 2 and C is born in step 3, so
+// C reuses B's slots: the store shrinks from 4T to 3T tiles.
+template <class XS>
+static void share_slots_pass(const std::vector<XTouch>& tv, int64_t T, int64_t nlogical,
+                             const std::unordered_map<int32_t, int32_t>& pinned, const XS& xs,
+                             std::vector<int32_t>& group, std::vector<int32_t>& width, std::vector<Edge>& edges) {
+  (void)xs;
+  const int64_t nw = nlogical - T;
+  std::vector<int64_t> first(nw, -1), last(nw, -1);
+  std::vector<char> ren(nw, 0);
+  std::vector<std::vector<int32_t>> touch(nw);
+  auto see = [&](int32_t l, int64_t u) {
+    if (l < T) return;
+    const int64_t w = l - T;
+    if (first[w] < 0) first[w] = u;
+    last[w] = u;
+    if (touch[w].empty() || touch[w].back() != (int32_t)u) touch[w].push_back((int32_t)u);
+  };
+  for (int64_t u = 0; u < (int64_t)tv.size(); ++u) {
+    see(tv[u].in0, u);
+    see(tv[u].in1, u);
+    see(tv[u].out, u);
+    if (tv[u].out >= T && tv[u].renamed) ren[tv[u].out - T] = 1;
+  }
+  group.assign(nw, -1);
+  width.clear();
+  std::vector<int64_t> order;
+  for (int64_t w = 0; w < nw; ++w)
+    if (first[w] >= 0 && !pinned.count((int32_t)(w + T))) order.push_back(w);
+  std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return first[a] < first[b]; });
+  // free groups per width: min-heap on the stream position their occupant was last touched
+  typedef std::pair<int64_t, int32_t> Fr;  // (last touch, group)
+  std::priority_queue<Fr, std::vector<Fr>, std::greater<Fr>> freeq[2];
+  std::vector<int64_t> occupant;  // group -> current working tile
+  std::priority_queue<Fr, std::vector<Fr>, std::greater<Fr>> busy[2];  // (last touch, group) of live occupants
+  for (int64_t w : order) {
+    const int k = ren[w] ? 1 : 0;
+    while (!busy[k].empty() && busy[k].top().first < first[w]) {  // occupants dead before w is born
+      freeq[k].push(busy[k].top());
+      busy[k].pop();
+    }
+    int32_t g;
+    if (!freeq[k].empty()) {
+      g = freeq[k].top().second;
+      freeq[k].pop();
+      const int64_t prev = occupant[g];
+      for (int32_t u : touch[prev]) edges.push_back({u, (int32_t)first[w], 1});  // slot reuse: WAR on the slot
+      occupant[g] = w;
+    } else {
+      g = (int32_t)width.size();
+      width.push_back(k ? 2 : 1);
+      occupant.push_back(w);
+    }
+    group[w] = g;
+    busy[k].push({last[w], g});
+  }
+}
+
 int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, const int64_t* barriers,
                int64_t nbar, uint32_t flags, tinv_plan** out, tinv_err* err, const int32_t* aux, int64_t nrecv,
                const int32_t* rank_of, int32_t nranks, bool host_only) {
@@ -1082,6 +1177,9 @@ int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, c
   p->nlogical = next_logical;
   const int64_t nx = p->nexec;
 
+  // ---- memory-constrained renaming (TINV_SHARE_SLOTS): working tiles share slots
+  std::vector<int32_t> share_group;  // non-matrix logical tile - T -> slot group (-1: own slots)
+  std::vector<int32_t> share_width;  // slots per group (1, or 2 for a renamed tile's cur / alt pair)
   // ---- hazard DAG over exec tasks (+ barrier edges at translated positions)
   {
     std::vector<std::vector<Acc>> acc(nx);
@@ -1105,6 +1203,8 @@ int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, c
     scoreboard(nx, acc, bars, edges);
     if (flags & TINV_SERIAL)
       for (int64_t v = 0; v + 1 < nx; ++v) edges.push_back({(int32_t)v, (int32_t)(v + 1), 3});
+    if (flags & TINV_SHARE_SLOTS) share_slots_pass(xs_touch(xs, nx), T, next_logical, recv_pin, xs, share_group,
+                                                   share_width, edges);
     std::vector<std::vector<int32_t>> adj(nx);
     for (const Edge& e : edges) adj[e.u].push_back(e.v);
     p->indeg0.assign(nx, 0);
@@ -1230,10 +1330,21 @@ int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, c
   p->cur0.assign(p->nlogical, -1);
   p->alt0.assign(p->nlogical, -1);
   int64_t next_slot = 2 * T + nrecv;  // receive tiles pinned at 2T + seq (same on every rank)
+  std::vector<int32_t> group_slot(share_width.size(), -1);
   for (int64_t l = T; l < p->nlogical; ++l) {
     auto pin = recv_pin.find((int32_t)l);
     if (pin != recv_pin.end()) {
       p->cur0[l] = p->alt0[l] = (int32_t)(2 * T + pin->second);
+      continue;
+    }
+    const int32_t gr = l - T < (int64_t)share_group.size() ? share_group[l - T] : -1;
+    if (gr >= 0) {  // a slot group shared by working tiles with disjoint live ranges
+      if (group_slot[gr] < 0) {
+        group_slot[gr] = (int32_t)next_slot;
+        next_slot += share_width[gr];
+      }
+      p->cur0[l] = group_slot[gr];
+      p->alt0[l] = renamed_tile[l] ? group_slot[gr] + 1 : p->cur0[l];
       continue;
     }
     p->cur0[l] = (int32_t)next_slot++;

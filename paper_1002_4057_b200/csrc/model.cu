@@ -110,7 +110,8 @@ extern "C" {
 // Model run: see include/tileinv_b200.h (tinv_model_run).
 int tinv_model_run(int64_t n, int64_t b, const int32_t* table, int64_t ntasks, int32_t stream_t,
                    const int64_t* barriers, int64_t nbar, const int32_t* aux, int64_t nrecv, const int32_t* rank_of,
-                   int32_t nranks, int32_t sms_per_rank, const double* cost, double* out, double* crit_kind) {
+                   int32_t nranks, int32_t sms_per_rank, uint32_t flags, const double* cost, double* out,
+                   double* crit_kind) {
   if (n < 1 || b < 1 || n % b || !cost || !out || nranks < 1 || nranks > MAX_RANKS || sms_per_rank < 1)
     return tinv::set_error(TINV_ERR_BAD_ARG, "bad model arguments");
   tinv_ctx c;  // shape only: no device, no store
@@ -125,7 +126,8 @@ int tinv_model_run(int64_t n, int64_t b, const int32_t* table, int64_t ntasks, i
   c.nsm = sms_per_rank * nranks;
   tinv_plan* p = nullptr;
   tinv_err err;
-  int rc = plan_build(&c, table, ntasks, stream_t, barriers, nbar, 0, &p, &err, aux, nrecv,
+  if (flags & ~(uint32_t)TINV_SHARE_SLOTS) return tinv::set_error(TINV_ERR_BAD_ARG, "model: unsupported plan flags");
+  int rc = plan_build(&c, table, ntasks, stream_t, barriers, nbar, flags, &p, &err, aux, nrecv,
                       nranks > 1 ? rank_of : nullptr, nranks, true);
   if (rc) return tinv::set_error(rc, "model: " + c.err);
   const int R = (int)c.R;
@@ -216,6 +218,7 @@ int tinv_model_run(int64_t n, int64_t b, const int32_t* table, int64_t ntasks, i
   out[0] = makespan;
   for (int r = 0; r < nranks; ++r) out[1 + r] = busy[r];
   out[1 + nranks] = (double)remaining;  // 0 unless the plan deadlocks
+  out[2 + nranks] = (double)(2 * c.T + p->dyn_slots + c.nsm);  // tile slots of the device store
   if (crit_kind) {  // time along the chain of releasing predecessors ending at the last task, per kind
     for (int k = 0; k < 17; ++k) crit_kind[k] = 0.0;
     int32_t u = -1;

@@ -10,11 +10,38 @@ from .taskgen import Placement, VariantConfig, gen_inversion, gen_step1, gen_ste
 from .tile_matrix import from_dense, to_dense, to_dense_symmetric
 
 
-def invert(a: np.ndarray, nb: int, config: VariantConfig = VariantConfig()) -> np.ndarray:
+def invert(a: np.ndarray, nb: int, config: VariantConfig = VariantConfig(), *,
+           share_slots: bool = False) -> np.ndarray:
     """A^-1 of an SPD matrix: symmetrize_lower(to_dense(execute(gen_inversion(...))))."""
     tm = from_dense(a, nb)
-    execute(gen_inversion(tm.t, config), tm)
+    execute(gen_inversion(tm.t, config), tm, share_slots=share_slots)
     return to_dense_symmetric(tm)
+
+
+def plan_under_memory(n: int, nb: int, budget_bytes: float, loops=None, sms: int = 148):
+    """Performance under a memory constraint (PAPER.md's closing open problem):
+    among the placements (out-of-place = the reference's array renaming into
+    B / C, in-place = none), the loop orders, and slot sharing (memory-
+    constrained renaming, TINV_SHARE_SLOTS), the variant the schedule model
+    (csrc/model.cu, calibrated on the B200) predicts fastest whose device store
+    fits `budget_bytes`. Host only. -> dict(config, share_slots, store_bytes,
+    model_ms) or None when nothing fits."""
+    from . import _native
+
+    t = n // nb
+    bp = -(-nb // 128) * 128
+    best = None
+    for pl in (Placement.OUT_OF_PLACE, Placement.IN_PLACE):
+        for lo in ([loops] if loops else ("UDU", "DDU", "UDD")):
+            cfg = VariantConfig(pl, lo, True)
+            s = gen_inversion(t, cfg)
+            for share in (False, True):
+                mk, _ = _native.model_run(n, nb, s.table(), t, sorted(s.barriers), sms_per_rank=sms,
+                                          flags=_native.SHARE_SLOTS if share else 0)
+                store = _native.model_run.last_slots * bp * bp * 8
+                if store <= budget_bytes and (best is None or mk < best["model_ms"] * 1e3 * 0.999):
+                    best = {"config": cfg, "share_slots": share, "store_bytes": store, "model_ms": mk / 1e3}
+    return best
 
 
 def step_potrf(a: np.ndarray, nb: int, direction: str = "U") -> np.ndarray:

@@ -186,20 +186,24 @@ def _run(stream: TaskStream, a: TileMatrix, table, barriers, flags, ref_ids=None
     return a
 
 
-def execute(stream: TaskStream, a: TileMatrix, workers: int = 1, trace_path=None) -> TileMatrix:
+def execute(stream: TaskStream, a: TileMatrix, workers: int = 1, trace_path=None, *,
+            share_slots: bool = False) -> TileMatrix:
     """Run the stream's DAG on the B200 (scheduler.py:261-351), updating `a`.
 
     `workers` is validated as in the reference; the device executor always
     uses every SM. On failure the smallest failing task id is raised as
     ExecutionError and `a` keeps its pre-call content. With trace_path set,
     writes `task_id,kind,indices,worker,start_ns,end_ns` per task from device
-    timestamps (worker = SM id)."""
+    timestamps (worker = SM id). share_slots (off by default): memory-
+    constrained renaming -- working tiles (B / C copies, aux tiles) share
+    device slots by live range (TINV_SHARE_SLOTS; out-of-place 4T -> 3T tiles)."""
     if workers < 1:
         raise ValueError(f"workers must be >= 1, got {workers}")
     if a.t != stream.t:
         raise InvalidStreamError(f"stream generated for t={stream.t} cannot run on a t={a.t} matrix")
     table = stream.table(a.label)
-    return _run(stream, a, table, np.array(sorted(stream.barriers), dtype=np.int64), 0, trace_path=trace_path)
+    flags = _native.SHARE_SLOTS if share_slots else 0
+    return _run(stream, a, table, np.array(sorted(stream.barriers), dtype=np.int64), flags, trace_path=trace_path)
 
 
 def run_in_order(stream: TaskStream, a: TileMatrix, order=None) -> TileMatrix:

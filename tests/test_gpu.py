@@ -551,3 +551,32 @@ def test_streamed_host_path_under_serialised_launches(env):
     r = subprocess.run([sys.executable, "-c", _SERIALISED_SCRIPT.format(root=root)], env=e, capture_output=True,
                        text=True, timeout=240)
     assert r.returncode == 0 and "SERIALISED_OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("n,b,placement,loops", [(1280, 128, "out", "UDU"), (1024, 256, "out", "DDU"),
+                                                 (1000, 200, "in", "UDU"), (1536, 128, "out", "UUU")])
+def test_share_slots_bitwise_and_smaller(n, b, placement, loops):
+    """Memory-constrained renaming (TINV_SHARE_SLOTS): working tiles share
+    slots by live range, reuse ordered by added edges -- same bits, smaller
+    store (out-of-place: C reuses B's slots)."""
+    a = O.spd_matrix(n, 13, 0.5)
+    cfg = P.VariantConfig(P.Placement(placement), loops, True)
+    t = n // b
+    s = P.gen_inversion(t, cfg)
+    outs, sizes = [], []
+    for fl in (0, _native.SHARE_SLOTS):
+        ctx = _native.Context(n, b)
+        ctx.put_dense(a)
+        plan = _native.Plan(ctx, s.table(), t, np.array(sorted(s.barriers), np.int64), fl)
+        assert plan.run()[0] == 0, plan.msg
+        x = np.zeros((n, n))
+        ctx.get_dense(x, _native.DENSE_SYMMETRIZE)
+        sizes.append(ctx.store_bytes())
+        plan.close()
+        ctx.close()
+        outs.append(x)
+    assert np.array_equal(outs[0], outs[1])
+    assert O.normwise_diff(outs[1], O.invert(a, b, loops, placement == "out", True)) <= 1e-10 * np.linalg.cond(a)
+    if placement == "out":
+        assert sizes[1] < sizes[0]
+    assert np.array_equal(P.invert(a, b, cfg, share_slots=True), outs[0])

@@ -137,8 +137,8 @@ def test_c5_conditioning_vs_cusolver_one_gpu():
 
     n, b = 65536, 1024
     free, _ = torch.cuda.mem_get_info()
-    if free < 160e9:
-        pytest.skip(f"C5 needs ~160 GB of free HBM, {free / 1e9:.0f} GB free")
+    if free < 140e9:
+        pytest.skip(f"C5 needs ~140 GB of free HBM, {free / 1e9:.0f} GB free")
     gen = torch.Generator(device="cuda").manual_seed(0)
     a = torch.empty(n, n, dtype=torch.float64, device="cuda")
     blk = 8192  # A = G G^T / n in row blocks of G (G itself: 34 GB)
@@ -157,12 +157,15 @@ def test_c5_conditioning_vs_cusolver_one_gpu():
     cfg = P.VariantConfig(P.Placement.OUT_OF_PLACE, "UDU", True)
     ctx = _native.Context(n, b)
     s = P.gen_inversion(t, cfg)
-    plan = _native.Plan(ctx, s.table(), t, np.array(sorted(s.barriers), np.int64))
+    # memory-constrained renaming: C reuses B's slots (store 4T -> 3T tiles, 71.6 -> 53.6 GB at C5)
+    plan = _native.Plan(ctx, s.table(), t, np.array(sorted(s.barriers), np.int64), _native.SHARE_SLOTS)
     assert plan.rc == 0, plan.msg
     ctx.put_dense_device(a.data_ptr(), n)
     rc, err, ms = plan.run()
     assert rc == 0, plan.msg
     plan.close()
+    store = ctx.store_bytes()
+    assert store < 60e9
     x = torch.empty_like(a)
     ctx.get_dense_device(x.data_ptr(), n, _native.DENSE_SYMMETRIZE)
     ctx.close()
@@ -182,7 +185,7 @@ def test_c5_conditioning_vs_cusolver_one_gpu():
     cond = float(a.abs().sum(0).max() * ref.abs().sum(0).max())
     assert cond > 1e3  # the config's hard conditioning (~4e3 in the 2-norm; the 1-norm estimate is larger)
     rel = float((x - ref).abs().max() / ref.abs().max())
-    print(f"C5 1-GPU: exec {ms:.0f} ms, normwise vs blocked cuSOLVER/cuBLAS {rel:.3e} (tol {1e-10 * cond:.2e}), "
+    print(f"C5 1-GPU: exec {ms:.0f} ms (store {store / 1e9:.1f} GB), normwise vs blocked cuSOLVER/cuBLAS {rel:.3e} (tol {1e-10 * cond:.2e}), "
           f"residual(2048 cols) {res:.3e}, cond1 {cond:.3e}")
     assert rel <= 1e-10 * cond
 
