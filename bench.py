@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--batch", type=int, default=None)
     p.add_argument("--engine", default="auto", choices=["auto", "fused", "dag"],
                    help="batched workloads: fused per-matrix kernel (nb == n <= 256) or the DAG executor")
+    p.add_argument("--fused-engine", default=None, choices=["cta", "pipe"],
+                   help="fused batched engine: one CTA per matrix (default) or the pipelined persistent engine")
     p.add_argument("--placement", default="out", choices=["in", "out"])
     p.add_argument("--loops", default=None,
                    help="loop orders of the three steps; default DDU at c3 (result tiles become final "
@@ -373,8 +375,14 @@ def main():
     fused = batch > 1 and args.engine != "dag" and nb == n <= _native.BATCH_SMALL_MAX_N
     if args.engine == "fused" and not fused:
         raise SystemExit("--engine fused needs a batched workload with nb == n <= 256")
-    config["engine"] = ("fused: one CTA per matrix runs gen_inversion(1) = POTRF -> TRTRI -> LAUUM "
-                        "(tinv_batch_small_launch)" if fused else "DAG executor (tinv_plan_exec)")
+    if fused and args.fused_engine:
+        _native.batch_engine(args.fused_engine)
+    feng = _native.batch_engine() if fused else None
+    config["engine"] = (("fused: one CTA per matrix runs gen_inversion(1) = POTRF -> TRTRI -> LAUUM "
+                         "(tinv_batch_small_launch, engine cta)") if feng == "cta" else
+                        ("fused, pipelined: one persistent CTA per SM, several matrices in flight, 64x64 block jobs "
+                         "of gen_inversion(1) over a DAG in shared memory (tinv_batch_small_launch, engine pipe)")
+                        if feng == "pipe" else "DAG executor (tinv_plan_exec)")
     ctx = None if fused else _native.Context(n, nb, local, batch=batch)
     if ctx is not None:
         ctx.set_stream(stream.cuda_stream)
@@ -641,7 +649,8 @@ def main():
     tpath = os.path.join(ROOT, "profiles", "exec_c3_traffic.json")
     if fused:
         tpath = os.path.join(ROOT, "profiles", "bsmall_c4_traffic.json")
-    if os.path.exists(tpath) and ((n, nb, args.placement) == (32768, 512, "out") or (fused and (n, batch) == (256, 8192))):
+    if os.path.exists(tpath) and ((n, nb, args.placement) == (32768, 512, "out") or
+                                  (feng == "cta" and (n, batch) == (256, 8192))):
         with open(tpath) as fh:
             traffic = json.load(fh)["traffic_bytes"]
 
@@ -657,7 +666,9 @@ def main():
                                            "dram__bytes_read.sum + dram__bytes_write.sum of one exec_kernel "
                                            "launch, ncu application replay (profiles/exec_c3_traffic.json)",
                          "kernel": "tinv::bsm::k_bsmall (one CTA per matrix: fused POTRF -> TRTRI -> LAUUM, "
-                                   "64x64 DMMA.8x8x4 block program)" if fused else
+                                   "64x64 DMMA.8x8x4 block program)" if feng == "cta" else
+                                   ("tinv::bpl::k_bpipe (persistent, warp-specialized: TMA operand ring, "
+                                    "DMMA.8x8x4 64x64 block jobs over an in-CTA DAG)") if feng == "pipe" else
                                    "tinv::exec_kernel (persistent DAG executor, DMMA.8x8x4)",
                          "algorithmic": f"n^3 = {flops:.3e} flop per launch",
                          "peak_source": "measured FP64 DMMA peak (tools/fp64_peak.cu); cuBLAS DGEMM "

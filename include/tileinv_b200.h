@@ -278,6 +278,18 @@ int tinv_batch_small_launch(const double* dA, double* dX, int64_t batch, int64_t
  * *ms (optional) = wall time of the device work. */
 int tinv_batch_small_host(const double* hA, double* hX, int64_t batch, int64_t n, int device,
                           int64_t* fail_matrix, int64_t* fail_index, double* ms);
+/* tinv_batch_small_engine: the engine the two calls above use (process-wide;
+ * initial value from the environment, TINV_BSMALL_ENGINE=cta|pipe):
+ *   TINV_BSMALL_CTA  (0) one thread block per matrix running the fused block
+ *                        program (csrc/batched.cu), any 1 <= n <= 256;
+ *   TINV_BSMALL_PIPE (1) one persistent block per SM keeping several matrices
+ *                        in flight, their 64x64 block jobs scheduled over a
+ *                        DAG in shared memory (csrc/batched_pipe.cu); even
+ *                        64 <= n <= 256 (other n run on TINV_BSMALL_CTA).
+ * engine < 0 only queries. Returns the engine in effect before the call. */
+#define TINV_BSMALL_CTA 0
+#define TINV_BSMALL_PIPE 1
+int tinv_batch_small_engine(int engine);
 
 #ifdef __cplusplus
 }

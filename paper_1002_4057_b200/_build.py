@@ -5,7 +5,7 @@ import subprocess
 import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-SRC = [os.path.join(PKG, "csrc", f) for f in ("api.cu", "executor.cu", "layout.cu", "batched.cu", "model.cu")]
+SRC = [os.path.join(PKG, "csrc", f) for f in ("api.cu", "executor.cu", "layout.cu", "batched.cu", "batched_pipe.cu", "model.cu")]
 LIB = os.path.join(PKG, "libtileinv_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

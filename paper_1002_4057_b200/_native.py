@@ -27,7 +27,7 @@ EXPORTS = (
     "tinv_put_tile", "tinv_get_tile", "tinv_gen_stream", "tinv_dag_edges", "tinv_dag_paths", "tinv_dist_stream", "tinv_plan_create",
     "tinv_plan_create_xfer", "tinv_plan_create_ranks", "tinv_plan_cta_idle", "tinv_model_run", "tinv_ipc_export", "tinv_ipc_open", "tinv_ipc_reset", "tinv_plan_exec",
     "tinv_plan_exec_host", "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
-    "tinv_batch_small_launch", "tinv_batch_small_host",
+    "tinv_batch_small_launch", "tinv_batch_small_host", "tinv_batch_small_engine",
 )
 BATCH_SMALL_MAX_N = 256  # tinv_batch_small_*: 1 <= n <= 256
 
@@ -108,6 +108,7 @@ def lib():
         "tinv_batch_small_launch": ([_P, _P, _I64, _I64, _I64, _P, _P], ctypes.c_int),
         "tinv_batch_small_host": ([_P, _P, _I64, _I64, ctypes.c_int, _I64P, _I64P, ctypes.POINTER(ctypes.c_double)],
                                   ctypes.c_int),
+        "tinv_batch_small_engine": ([ctypes.c_int], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -148,6 +149,16 @@ def device_count():
 def batch_small_launch(a_ptr, x_ptr, batch, n, stride, stream_ptr, fail_ptr):
     """Asynchronous fused batched inversion on device buffers (tinv_batch_small_launch)."""
     check(lib().tinv_batch_small_launch(a_ptr, x_ptr, batch, n, stride, stream_ptr, fail_ptr))
+
+
+BATCH_ENGINES = {"cta": 0, "pipe": 1}
+
+
+def batch_engine(name=None):
+    """Select the fused batched engine ("cta" | "pipe", tinv_batch_small_engine);
+    returns the previous one. None only queries."""
+    prev = lib().tinv_batch_small_engine(-1 if name is None else BATCH_ENGINES[name])
+    return {v: k for k, v in BATCH_ENGINES.items()}[prev]
 
 
 def batch_small_host(a_ptr, x_ptr, batch, n, device=0):

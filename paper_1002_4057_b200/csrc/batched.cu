@@ -538,8 +538,18 @@ __global__ void __launch_bounds__(NT, 3)
 
 }  // namespace bsm
 
+cudaError_t launch_bpipe(const double* dA, double* dX, int64_t batch, int64_t n, int64_t stride, cudaStream_t st,
+                         unsigned long long* dfail, int64_t id0);
+
 cudaError_t launch_bsmall(const double* dA, double* dX, int64_t batch, int64_t n, int64_t stride, cudaStream_t st,
                           unsigned long long* dfail, int64_t id0) {
+  // TINV_BSMALL_ENGINE=pipe (even 64 <= n <= 256): the pipelined persistent
+  // engine of csrc/batched_pipe.cu; default: the one-CTA-per-matrix program
+  // below (measured 2-3 % faster at C4, profiles/r02/c4_engines.md)
+  {
+    const cudaError_t e = launch_bpipe(dA, dX, batch, n, stride, st, dfail, id0);
+    if (e != cudaErrorNotSupported) return e;
+  }
   // TINV_BSMALL_PROF=1: per-phase clock64 spans of thread 0, printed per launch
   // (process-wide state: like a context, this entry point is not thread-safe)
   static const int prof_mode = getenv("TINV_BSMALL_PROF") && atoi(getenv("TINV_BSMALL_PROF")) ? 1 : 0;

@@ -324,8 +324,17 @@ def _spd_batch(batch, n, seed, shift=1.0):
     return np.tril(a) + np.transpose(np.tril(a, -1), (0, 2, 1))
 
 
+@pytest.fixture(params=["cta", "pipe"])
+def batch_engine(request):
+    """Both fused engines (tinv_batch_small_engine): one block per matrix, and the
+    pipelined persistent engine (even 64 <= n <= 256; other n fall back to cta)."""
+    prev = _native.batch_engine(request.param)
+    yield request.param
+    _native.batch_engine(prev)
+
+
 @pytest.mark.parametrize("n", [1, 2, 5, 33, 64, 65, 100, 128, 130, 191, 200, 255, 256])
-def test_fused_batched_vs_oracle(n):
+def test_fused_batched_vs_oracle(n, batch_engine):
     """gen_inversion(1) per matrix fused in one CTA: parity with the oracle's
     POTRF -> TRTRI -> LAUUM of the single tile (odd n: synchronous loads;
     n % 64 != 0: identity-padded blocks)."""
@@ -339,7 +348,7 @@ def test_fused_batched_vs_oracle(n):
     assert np.array_equal(P.invert_batched(a, n, engine="fused"), x)  # deterministic
 
 
-def test_fused_batched_matches_dag_engine_and_device_api():
+def test_fused_batched_matches_dag_engine_and_device_api(batch_engine):
     import torch
 
     a = _spd_batch(300, 256, 7)
@@ -366,8 +375,24 @@ def test_fused_batched_matches_dag_engine_and_device_api():
     assert np.array_equal(hy, np.concatenate([xf] * 4))
 
 
+def test_fused_engines_agree():
+    """The two fused engines run the same block algorithm (64x64 blocks, the
+    same per-element summation order is NOT guaranteed): normwise agreement."""
+    a = _spd_batch(150, 256, 11)
+    prev = _native.batch_engine("cta")
+    try:
+        xc = P.invert_batched(a, 256)
+        _native.batch_engine("pipe")
+        xp = P.invert_batched(a, 256)
+    finally:
+        _native.batch_engine(prev)
+    assert np.array_equal(xp, np.transpose(xp, (0, 2, 1)))
+    for k in range(0, 150, 37):
+        assert rel(xp[k], xc[k]) <= 1e-10 * np.linalg.cond(a[k])
+
+
 @pytest.mark.parametrize("n,col", [(256, 10), (256, 200), (100, 70), (33, 0)])
-def test_fused_batched_failure_reports_matrix_and_column(n, col):
+def test_fused_batched_failure_reports_matrix_and_column(n, col, batch_engine):
     a = _spd_batch(9, n, 3)
     a[6, col, col] = -5.0
     a[4, col, col] = -5.0  # the lowest failing matrix is reported

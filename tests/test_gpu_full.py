@@ -112,7 +112,8 @@ def test_full_size_steps_vs_cusolver():
     ctx.close()
 
 
-def test_full_size_batched_c4_vs_cusolver():
+@pytest.mark.parametrize("engine", ["cta", "pipe"])
+def test_full_size_batched_c4_vs_cusolver(engine):
     """BASELINE config 4 (8192 x n=256) through the fused engine: bitwise
     symmetric and reproducible, normwise against cuSOLVER's batched inverse."""
     B, n = 8192, 256
@@ -125,12 +126,14 @@ def test_full_size_batched_c4_vs_cusolver():
     fail = torch.full((1,), -1, dtype=torch.int64, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
     xs = []
+    prev = _native.batch_engine(engine)
     for _ in range(2):
         x = torch.empty_like(a)
         _native.batch_small_launch(a.data_ptr(), x.data_ptr(), B, n, n * n, st, fail.data_ptr())
         torch.cuda.synchronize()
         assert int(fail.item()) == -1
         xs.append(x)
+    _native.batch_engine(prev)
     x = xs[0]
     assert torch.equal(x, xs[1])
     assert torch.equal(x, x.transpose(1, 2))

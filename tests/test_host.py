@@ -218,6 +218,12 @@ def test_fused_batched_engine_selection_and_abi_validation():
     assert L.tinv_batch_small_host(fake, fake, 1, 257, 0, ctypes.byref(fm), ctypes.byref(fi), None) == \
         _native.ERR_BAD_ARG
     assert (fm.value, fi.value) == (-1, -1)
+    # engine selection is host state (no device needed)
+    prev = _native.batch_engine("pipe")
+    assert _native.batch_engine() == "pipe"
+    assert _native.batch_engine("cta") == "pipe"
+    assert L.tinv_batch_small_engine(7) == 0 and _native.batch_engine() == "cta"  # unknown values only query
+    _native.batch_engine(prev)
 
 
 def test_schedule_model_host_only():
