@@ -1176,6 +1176,30 @@ int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, c
   p->nexec = (int64_t)xs.size();
   p->nlogical = next_logical;
   const int64_t nx = p->nexec;
+  // SYRK_SUB whose tile is next written by a POTRF, through SYRK_SUBs only
+  // (step 1's trailing diagonal chain): POTRF reads the lower triangle and
+  // zeroes the rest, so its strict upper part is dead -- the task reduce-adds
+  // its lower blocks with the TMA epilogue instead of mirroring through the
+  // generic one (C2: SYRK_SUB 60 -> ~40 us on the critical path).
+  {
+    std::vector<std::vector<int32_t>> users(next_logical);
+    for (int64_t u = 0; u < nx; ++u)
+      for (int32_t tl : {xs[u].in0, xs[u].in1, xs[u].out})
+        if (tl >= 0 && (users[tl].empty() || users[tl].back() != (int32_t)u)) users[tl].push_back((int32_t)u);
+    for (int64_t u = 0; u < nx; ++u) {
+      if (xs[u].kind != TINV_SYRK_SUB || xs[u].in0 == xs[u].out || xs[u].in1 == xs[u].out) continue;
+      const auto& us = users[xs[u].out];
+      auto it = std::upper_bound(us.begin(), us.end(), (int32_t)u);
+      bool dead = false;
+      for (; it != us.end(); ++it) {
+        const auto& w = xs[*it];
+        if (w.kind == TINV_SYRK_SUB && w.out == xs[u].out && w.in0 != w.out && w.in1 != w.out) continue;
+        dead = (w.kind == TINV_POTRF || w.kind == KIND_POTRF_INV) && w.out == xs[u].out;
+        break;
+      }
+      if (dead) xs[u].flags |= TF_NO_MIRROR;
+    }
+  }
 
   // ---- memory-constrained renaming (TINV_SHARE_SLOTS): working tiles share slots
   std::vector<int32_t> share_group;  // non-matrix logical tile - T -> slot group (-1: own slots)

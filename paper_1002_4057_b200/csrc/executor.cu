@@ -322,7 +322,7 @@ __device__ __forceinline__ void get_job_phase(const ItemInfo& it, int n, int R, 
       return;
     case TINV_SYRK_SUB:
       gemm_job(j, V_NT, x, r, 0, x, c, 0, 0, R, w, r, c, o, -1);
-      j.mirror = 1;
+      j.mirror = (it.flags & TF_NO_MIRROR) ? 0 : 1;
       return;
     case TINV_SYRK_ADD_T:
       gemm_job(j, V_TN, x, r, 0, x, c, 0, 0, R, w, r, c, o, 1);

@@ -53,6 +53,8 @@ enum TaskFlags : int32_t {
   TF_RENAMED = 1,   // output written to the alternate slot, slots swapped at completion
   TF_EXTERNAL = 2,  // never queued: completed by the inbox poller (RECV, ARRIVE)
   TF_DIAG_FROM_AUX = 4,  // TRTRI / INV: diagonal-block inverses copied from the POTRF aux tile (in1)
+  TF_NO_MIRROR = 8,      // SYRK_SUB whose tile is next factored by POTRF (through SYRK_SUBs only): the
+                         // strict upper part is dead, so the lower blocks reduce-add with no mirror
 };
 
 struct TaskDev {
