@@ -542,7 +542,9 @@ def main():
     # per-step device times (each step on the previous one's
     # output, same store) and pipelined vs barriered full inversion
     steps_breakdown = None
-    if batch == 1 and mg is None and not args.no_steps:
+    # (skipped above n = 32768: three more step plans on the same store would
+    # not fit next to C5's 34 GB matrix and its working tiles)
+    if batch == 1 and mg is None and not args.no_steps and n <= 32768:
         def med_ms(plans, reps=3):
             out = []
             for _ in range(reps):
@@ -675,7 +677,7 @@ def main():
                                         f"{DGEMM_TFLOPS} TF/s for context; MEASURED_PEAKS.json has no FP64 entry"},
             "pct_fp64_peak": 100.0 * value / world / 1e3 / DMMA_PEAK_TFLOPS,  # per GPU
             "kernel_ms": kern_avg, "plan": stats,
-            "store_bytes": None if ctx is None else store_bytes, "share_slots": bool(args.share_slots),
+            "store_bytes": store_bytes, "share_slots": bool(args.share_slots),
             "residual": res, "symmetry_err": sym_err,
             "gpu_launches": (1 if fused else 3) * args.steps,
             "clocks": clk.summary(),
