@@ -383,7 +383,13 @@ def main():
                         ("fused, pipelined: one persistent CTA per SM, several matrices in flight, 64x64 block jobs "
                          "of gen_inversion(1) over a DAG in shared memory (tinv_batch_small_launch, engine pipe)")
                         if feng == "pipe" else "DAG executor (tinv_plan_exec)")
-    ctx = None if fused else _native.Context(n, nb, local, batch=batch)
+    if fused:
+        ctx = None
+    elif world > 1 and batch == 1:  # distributed: each rank's store holds only its own tiles
+        from paper_1002_4057_b200.distributed import default_grid, owned_tiles
+        ctx = _native.Context.owned(n, nb, owned_tiles(t, default_grid(world), rank), local)
+    else:
+        ctx = _native.Context(n, nb, local, batch=batch)
     if ctx is not None:
         ctx.set_stream(stream.cuda_stream)
     s = P.gen_inversion(t, P.VariantConfig(P.Placement(args.placement), args.loops, pipelined))
@@ -479,8 +485,8 @@ def main():
             dist.all_gather(allb, v)
             load["rank_busy_frac"] = [float(x.item()) for x in allb]
     achieved = flops / (world if mg is not None else 1) / (kern_avg * 1e-3) / 1e12
-    if mg is not None:  # gather the owned tiles for the check below
-        x *= owned_mask(n, nb, mg.grid, rank, "cuda")
+    if mg is not None:  # gather the owned tiles for the check below (others' tiles: not written, masked out)
+        x = torch.where(owned_mask(n, nb, mg.grid, rank, "cuda") > 0, x, torch.zeros((), dtype=x.dtype, device=x.device))
         import torch.distributed as tdist
         tdist.all_reduce(x)
         x = torch.tril(x) + torch.tril(x, -1).T

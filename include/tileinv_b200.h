@@ -226,6 +226,28 @@ int tinv_ipc_export(tinv_ctx* ctx, tinv_plan* plan, void* pool_handle, void* inb
 int tinv_ipc_open(tinv_ctx* ctx, int32_t rank, int32_t world, const void* pool_handles,
                   const void* inbox_handles);
 int tinv_ipc_reset(tinv_ctx* ctx);
+/* Several ranks in ONE process on one device (tests / emulation of the
+ * multi-process runtime): after tinv_ipc_export on every rank's context,
+ * tinv_peer_attach maps the peers' pools and inboxes by plain device pointer
+ * (what tinv_ipc_open does with IPC handles across processes). */
+int tinv_peer_attach(tinv_ctx* ctx, int32_t rank, int32_t world, tinv_ctx* const* peers);
+/* A rank's store with slots only for the lower tiles it owns (owned[i * t + j]
+ * != 0, i >= j; e.g. the 2D block-cyclic owner (i mod P) * Q + (j mod Q) ==
+ * rank), their rename shadows, and its receive / working tiles -- instead of
+ * the whole matrix twice. Plans may touch only owned matrix tiles (the
+ * distributed stream of the rank does); not combinable with
+ * TINV_KEEP_ON_FAILURE or TINV_STREAM_IO. put / get_dense skip other ranks'
+ * tiles (get leaves them as they are in the destination). */
+int tinv_create_owned(tinv_ctx** ctx, int64_t n, int64_t b, int device, const int32_t* owned);
+/* receive-slot base of this store (SEND targets in it), and the peers' bases
+ * for a multi-process run whose stores differ (exchange, then set; plain
+ * pointers via tinv_peer_attach set them automatically) */
+int tinv_recv_base(const tinv_ctx* ctx, int32_t* base);
+int tinv_ipc_recv_bases(tinv_ctx* ctx, int32_t world, const int32_t* bases);
+/* executor grid of this context: nsm CTAs (1 <= nsm <= the device's SMs;
+ * default all). Ranks sharing one device each take a disjoint share, so their
+ * persistent executors are co-resident. Set before creating plans. */
+int tinv_set_sms(tinv_ctx* ctx, int32_t nsm);
 /* run the plan on the context's matrix; blocks. ms (optional) = device time
  * of the executor launch measured with CUDA events. */
 int tinv_plan_exec(tinv_plan* plan, tinv_err* err, double* ms);

@@ -25,7 +25,7 @@ EXPORTS = (
     "tinv_abi_version", "tinv_device_count", "tinv_last_error", "tinv_create", "tinv_create_batch", "tinv_destroy",
     "tinv_shape", "tinv_store_bytes", "tinv_set_stream", "tinv_put_dense", "tinv_get_dense", "tinv_put_dense_device", "tinv_get_dense_device",
     "tinv_put_tile", "tinv_get_tile", "tinv_gen_stream", "tinv_dag_edges", "tinv_dag_paths", "tinv_dist_stream", "tinv_plan_create",
-    "tinv_plan_create_xfer", "tinv_plan_create_ranks", "tinv_plan_cta_idle", "tinv_model_run", "tinv_ipc_export", "tinv_ipc_open", "tinv_ipc_reset", "tinv_plan_exec",
+    "tinv_plan_create_xfer", "tinv_plan_create_ranks", "tinv_plan_cta_idle", "tinv_model_run", "tinv_ipc_export", "tinv_ipc_open", "tinv_ipc_reset", "tinv_peer_attach", "tinv_set_sms", "tinv_create_owned", "tinv_recv_base", "tinv_ipc_recv_bases", "tinv_plan_exec",
     "tinv_plan_exec_host", "tinv_plan_destroy", "tinv_plan_stats", "tinv_plan_trace", "tinv_run",
     "tinv_batch_small_launch", "tinv_batch_small_host", "tinv_batch_small_engine",
 )
@@ -98,6 +98,11 @@ def lib():
         "tinv_ipc_export": ([_P, _P, ctypes.c_char_p, ctypes.c_char_p], ctypes.c_int),
         "tinv_ipc_open": ([_P, _I32, _I32, ctypes.c_char_p, ctypes.c_char_p], ctypes.c_int),
         "tinv_ipc_reset": ([_P], ctypes.c_int),
+        "tinv_peer_attach": ([_P, _I32, _I32, ctypes.POINTER(_P)], ctypes.c_int),
+        "tinv_set_sms": ([_P, _I32], ctypes.c_int),
+        "tinv_create_owned": ([ctypes.POINTER(_P), _I64, _I64, ctypes.c_int, _I32P], ctypes.c_int),
+        "tinv_recv_base": ([_P, _I32P], ctypes.c_int),
+        "tinv_ipc_recv_bases": ([_P, _I32, _I32P], ctypes.c_int),
         "tinv_plan_exec": ([_P, ctypes.POINTER(TinvErr), ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
         "tinv_plan_exec_host": ([_P, _P, _I64, _P, _I64, ctypes.c_int, ctypes.POINTER(TinvErr),
                                  ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
@@ -278,6 +283,30 @@ class Context:
         self.n, self.b, self.batch = n, b, batch
         self.t = n // b
 
+    @classmethod
+    def owned(cls, n, b, owned, device=0):
+        """A partitioned store: slots only for the lower tiles with owned[i, j]
+        != 0 (tinv_create_owned), e.g. one rank's 2D block-cyclic share."""
+        self = cls.__new__(cls)
+        own = np.ascontiguousarray(owned, dtype=np.int32)
+        h = _P()
+        rc = lib().tinv_create_owned(ctypes.byref(h), n, b, device, _ip(own))
+        if rc != OK:
+            raise NativeError(rc, last_error(None))
+        self.h = h
+        self.n, self.b, self.batch = n, b, 1
+        self.t = n // b
+        return self
+
+    def recv_base(self):
+        v = ctypes.c_int32()
+        check(lib().tinv_recv_base(self.h, ctypes.byref(v)), self.h)
+        return v.value
+
+    def ipc_recv_bases(self, bases):
+        arr = np.ascontiguousarray(bases, dtype=np.int32)
+        check(lib().tinv_ipc_recv_bases(self.h, len(arr), _ip(arr)), self.h)
+
     def close(self):
         if self.h:
             lib().tinv_destroy(self.h)
@@ -303,6 +332,15 @@ class Context:
 
     def ipc_reset(self):
         check(lib().tinv_ipc_reset(self.h), self.h)
+
+    def peer_attach(self, rank, contexts):
+        """Map the peers' pools / inboxes by device pointer (ranks in one process, tinv_peer_attach)."""
+        arr = (_P * len(contexts))(*[c.h for c in contexts])
+        check(lib().tinv_peer_attach(self.h, rank, len(contexts), arr), self.h)
+
+    def set_sms(self, nsm):
+        """Executor grid of this context (tinv_set_sms)."""
+        check(lib().tinv_set_sms(self.h, nsm), self.h)
 
     def put_dense(self, m):
         m = np.ascontiguousarray(m, dtype=np.float64)

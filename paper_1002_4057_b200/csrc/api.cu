@@ -78,9 +78,9 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-// the other slot of lower tile k's pair (home slot, shadow T + k)
+// the other slot of lower tile k's pair (home slot, shadow: T + k, or compact in a partitioned store)
 static inline int32_t alt_slot_of(const tinv_ctx* c, int64_t k) {
-  return c->a_slot[k] == c->home[k] ? (int32_t)(c->T + k) : c->home[k];
+  return c->a_slot[k] == c->home[k] ? c->shadow[k] : c->home[k];
 }
 
 static int make_maps(tinv_ctx* c) {
@@ -120,7 +120,7 @@ static int ensure_pool(tinv_ctx* c, int64_t slots) {
   double* np = nullptr;
   CK(c, cudaMalloc(&np, (size_t)slots * c->slot_elems * 8));
   if (c->pool) {
-    CK(c, cudaMemcpyAsync(np, c->pool, (size_t)std::min<int64_t>(c->pool_slots, 2 * c->T) * c->slot_elems * 8,
+    CK(c, cudaMemcpyAsync(np, c->pool, (size_t)std::min<int64_t>(c->pool_slots, c->mslots) * c->slot_elems * 8,
                           cudaMemcpyDeviceToDevice, c->st));
     CK(c, cudaStreamSynchronize(c->st));
     CK(c, cudaFree(c->pool));
@@ -153,7 +153,18 @@ int tinv_device_count(void) {
 
 int tinv_create(tinv_ctx** out, int64_t n, int64_t b, int device) { return tinv_create_batch(out, 1, n, b, device); }
 
+static int create_impl(tinv_ctx** out, int64_t batch, int64_t n, int64_t b, int device, const int32_t* owned);
+
 int tinv_create_batch(tinv_ctx** out, int64_t batch, int64_t n, int64_t b, int device) {
+  return create_impl(out, batch, n, b, device, nullptr);
+}
+
+int tinv_create_owned(tinv_ctx** out, int64_t n, int64_t b, int device, const int32_t* owned) {
+  if (!owned) return fail(nullptr, TINV_ERR_BAD_ARG, "null ownership mask");
+  return create_impl(out, 1, n, b, device, owned);
+}
+
+static int create_impl(tinv_ctx** out, int64_t batch, int64_t n, int64_t b, int device, const int32_t* owned) {
   if (!out) return fail(nullptr, TINV_ERR_BAD_ARG, "null ctx pointer");
   *out = nullptr;
   if (n < 1 || b < 1 || n % b) return fail(nullptr, TINV_ERR_BAD_ARG, "matrix order not divisible by tile order");
@@ -190,11 +201,30 @@ int tinv_create_batch(tinv_ctx** out, int64_t batch, int64_t n, int64_t b, int d
   c->own = c->st;
   c->a_slot.resize(c->T);
   c->home.resize(c->T);
-  for (int64_t k = 0; k < c->T; ++k) c->a_slot[k] = c->home[k] = (int32_t)k;
+  c->shadow.resize(c->T);
+  if (!owned) {
+    for (int64_t k = 0; k < c->T; ++k) c->a_slot[k] = c->home[k] = (int32_t)k, c->shadow[k] = (int32_t)(c->T + k);
+    c->mslots = 2 * c->T;
+  } else {  // partitioned: slots only for this rank's tiles (owned[i * t + j], i >= j), homes then shadows
+    c->partitioned = true;
+    int64_t nown = 0;
+    for (int64_t i = 0; i < c->t; ++i)
+      for (int64_t j = 0; j <= i; ++j) nown += owned[i * c->t + j] != 0;
+    int32_t s = 0;
+    for (int64_t i = 0; i < c->t; ++i)
+      for (int64_t j = 0; j <= i; ++j) {
+        const int64_t k = tri_index(i, j);
+        const bool mine = owned[i * c->t + j] != 0;
+        c->a_slot[k] = c->home[k] = mine ? s : -1;
+        c->shadow[k] = mine ? (int32_t)(nown + s) : -1;
+        s += mine;
+      }
+    c->mslots = 2 * nown;
+  }
   if (cudaMalloc(&c->d_a_slot, c->T * sizeof(int32_t)) != cudaSuccess)
     return bail(fail(nullptr, TINV_ERR_CUDA, "cudaMalloc failed"));
   cudaMemcpy(c->d_a_slot, c->a_slot.data(), c->T * sizeof(int32_t), cudaMemcpyHostToDevice);
-  rc = ensure_pool(c, 2 * c->T + c->nsm);
+  rc = ensure_pool(c, c->mslots + c->nsm);
   if (rc != TINV_OK) {
     g_err = c->err;
     return bail(rc);
@@ -209,7 +239,7 @@ int tinv_destroy(tinv_ctx* c) {
   if (c->pool) cudaFree(c->pool);
   if (c->d_a_slot) cudaFree(c->d_a_slot);
   if (c->bstage) cudaFree(c->bstage);
-  for (int r = 0; r < MAX_RANKS; ++r) {
+  for (int r = 0; r < MAX_RANKS && !c->attached; ++r) {
     if (r == c->rank) continue;
     if (c->peer_pool[r]) cudaIpcCloseMemHandle(c->peer_pool[r]);
     if (c->peer_inbox[r]) cudaIpcCloseMemHandle(c->peer_inbox[r]);
@@ -391,6 +421,7 @@ int tinv_put_tile(tinv_ctx* c, int64_t i, int64_t j, const double* host) {
   int rc = sync_slots(c);
   if (rc) return rc;
   const int64_t b = c->b, bp = c->bp, x = tri_index(i, j);
+  if (c->a_slot[x] < 0) return fail(c, TINV_ERR_BAD_ARG, "tile of another rank's store");
   double* slot = c->pool + (int64_t)c->a_slot[x] * c->slot_elems;
   // the b x b tile straight into its slot; a padded slot (bp > b) gets the
   // closure padding (identity on a diagonal tile, 0 elsewhere) around it
@@ -409,6 +440,7 @@ int tinv_get_tile(tinv_ctx* c, int64_t i, int64_t j, double* host) {
   if (!c || !host || i < 0 || j < 0 || j > i || i >= c->t) return fail(c, TINV_ERR_BAD_ARG, "bad tile index");
   CK(c, cudaSetDevice(c->device));
   const int64_t b = c->b;
+  if (c->a_slot[tri_index(i, j)] < 0) return fail(c, TINV_ERR_BAD_ARG, "tile of another rank's store");
   CK(c, cudaMemcpy2D(host, b * 8, c->pool + (int64_t)c->a_slot[tri_index(i, j)] * c->slot_elems, c->bp * 8, b * 8,
                      b, cudaMemcpyDeviceToHost));
   return TINV_OK;
@@ -988,6 +1020,8 @@ int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, c
     return fail(c, TINV_ERR_STREAM, "stream generated for t=" + std::to_string(stream_t) +
                                         " cannot run on a t=" + std::to_string(c->t) + " matrix");
   }
+  if (c->partitioned && (flags & (TINV_KEEP_ON_FAILURE | TINV_STREAM_IO)))
+    return fail(c, TINV_ERR_BAD_ARG, "a partitioned store supports neither TINV_KEEP_ON_FAILURE nor TINV_STREAM_IO");
   const int R = (int)c->R, t = (int)c->t;
   const int64_t T = c->T;
   tinv_plan* p = new tinv_plan();
@@ -1089,6 +1123,9 @@ int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, c
       continue;
     }
     if (!get_logical(f[F_OL], f[F_OR], f[F_OC], false, v, o)) return bad("output tile outside the matrix");
+    if (c->partitioned)
+      for (int32_t tl : {in0, in1, o})
+        if (tl >= 0 && tl < T && c->home[tl] < 0) return bad("tile of another rank's store (partitioned context)");
     if (kind == KIND_RECV) {
       if (ax1 < 0 || ax1 >= nrecv) return bad("receive sequence out of range");
       recv_pin[o] = ax1;
@@ -1353,12 +1390,13 @@ int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, c
   // ---- slots of the non-matrix logical tiles: [2T, 2T + dyn)
   p->cur0.assign(p->nlogical, -1);
   p->alt0.assign(p->nlogical, -1);
-  int64_t next_slot = 2 * T + nrecv;  // receive tiles pinned at 2T + seq (same on every rank)
+  const int64_t mslots = c->mslots;
+  int64_t next_slot = mslots + nrecv;  // receive tiles pinned at mslots + seq
   std::vector<int32_t> group_slot(share_width.size(), -1);
   for (int64_t l = T; l < p->nlogical; ++l) {
     auto pin = recv_pin.find((int32_t)l);
     if (pin != recv_pin.end()) {
-      p->cur0[l] = p->alt0[l] = (int32_t)(2 * T + pin->second);
+      p->cur0[l] = p->alt0[l] = (int32_t)(mslots + pin->second);
       continue;
     }
     const int32_t gr = l - T < (int64_t)share_group.size() ? share_group[l - T] : -1;
@@ -1374,7 +1412,7 @@ int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, c
     p->cur0[l] = (int32_t)next_slot++;
     p->alt0[l] = renamed_tile[l] ? (int32_t)next_slot++ : p->cur0[l];
   }
-  p->dyn_slots = next_slot - 2 * T;
+  p->dyn_slots = next_slot - mslots;
   p->nrecv = nrecv;
   p->recv_task_h.assign(std::max<int64_t>(nrecv, 1), -1);
   for (int64_t u = 0; u < nx; ++u)
@@ -1471,7 +1509,7 @@ int tinv_plan_cta_idle(const tinv_plan* p, int64_t* idle_ns, int32_t* rank, int6
 int tinv_ipc_export(tinv_ctx* c, tinv_plan* p, void* pool_handle, void* inbox_handle) {
   if (!c || !p || !pool_handle || !inbox_handle) return fail(c, TINV_ERR_BAD_ARG, "bad ipc_export arguments");
   CK(c, cudaSetDevice(c->device));
-  const int64_t need = 2 * c->T + p->dyn_slots + c->nsm + ((p->flags & TINV_KEEP_ON_FAILURE) ? c->T : 0);
+  const int64_t need = c->mslots + p->dyn_slots + c->nsm + ((p->flags & TINV_KEEP_ON_FAILURE) ? c->T : 0);
   int rc = ensure_pool(c, need);
   if (rc) return rc;
   if (!c->inbox || c->inbox_len < std::max<int64_t>(p->nrecv, 1)) {
@@ -1512,6 +1550,44 @@ int tinv_ipc_open(tinv_ctx* c, int32_t rank, int32_t world, const void* pool_han
     c->peer_pool[r] = (double*)pp;
     c->peer_inbox[r] = (int32_t*)pi;
   }
+  return TINV_OK;
+}
+
+int tinv_peer_attach(tinv_ctx* c, int32_t rank, int32_t world, tinv_ctx* const* peers) {
+  if (!c || !peers || rank < 0 || world < 1 || world > MAX_RANKS || rank >= world || peers[rank] != c)
+    return fail(c, TINV_ERR_BAD_ARG, "bad peer_attach arguments");
+  for (int r = 0; r < world; ++r)
+    if (!peers[r] || !peers[r]->exported || peers[r]->device != c->device)
+      return fail(c, TINV_ERR_BAD_ARG, "every peer must be exported, on this device");
+  c->rank = rank;
+  c->world = world;
+  c->attached = true;  // plain pointers: nothing to close
+  for (int r = 0; r < world; ++r) {
+    c->peer_pool[r] = peers[r]->pool;
+    c->peer_inbox[r] = peers[r]->inbox;
+    c->peer_rbase[r] = (int32_t)peers[r]->mslots;
+  }
+  return TINV_OK;
+}
+
+int tinv_ipc_recv_bases(tinv_ctx* c, int32_t world, const int32_t* bases) {
+  if (!c || !bases || world < 1 || world > MAX_RANKS) return fail(c, TINV_ERR_BAD_ARG, "bad ipc_recv_bases arguments");
+  for (int r = 0; r < world; ++r) c->peer_rbase[r] = bases[r];
+  return TINV_OK;
+}
+
+int tinv_recv_base(const tinv_ctx* c, int32_t* base) {
+  if (!c || !base) return TINV_ERR_BAD_ARG;
+  *base = (int32_t)c->mslots;
+  return TINV_OK;
+}
+
+int tinv_set_sms(tinv_ctx* c, int32_t nsm) {
+  if (!c) return TINV_ERR_BAD_ARG;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, c->device) != cudaSuccess) return fail(c, TINV_ERR_CUDA, "device query failed");
+  if (nsm < 1 || nsm > prop.multiProcessorCount) return fail(c, TINV_ERR_BAD_ARG, "nsm out of range");
+  c->nsm = nsm;
   return TINV_OK;
 }
 
@@ -1720,7 +1796,7 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
   tinv_ctx* c = p->ctx;
   const int64_t T = c->T, nx = p->nexec;
   CK(c, cudaSetDevice(c->device));
-  const int64_t scratch_base = 2 * T + p->dyn_slots;
+  const int64_t scratch_base = c->mslots + p->dyn_slots;
   const bool keep = (p->flags & TINV_KEEP_ON_FAILURE) != 0;
   const int64_t backup_base = scratch_base + c->nsm;
   const bool staged_out = io && io->mode == TINV_DENSE_SYMMETRIZE;
@@ -1810,7 +1886,9 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
   P.trace_ready = p->d_tr;
   P.t0 = 0;
   P.nrecv = (int32_t)p->nrecv;
-  P.recv_base = (int32_t)(2 * T);
+  P.recv_base = (int32_t)c->mslots;
+  for (int r = 0; r < MAX_RANKS; ++r)  // SEND targets: the receivers' receive bases (peer_attach / ipc_recv_bases)
+    P.peer_recv_base[r] = c->peer_rbase[r] > 0 ? c->peer_rbase[r] : (int32_t)c->mslots;
   P.recv_task = p->d_recv_task;
   P.inbox = p->d_inbox;
   if (c->inbox) {  // multi-process: the exported inbox, zeroed by tinv_ipc_reset before the ranks' barrier

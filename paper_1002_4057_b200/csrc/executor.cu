@@ -1122,7 +1122,8 @@ __device__ __noinline__ void run_special(const Job& jb, const ItemInfo& it, cons
     }
     case SP_SEND: {  // tile version -> receiver's pool (peer memory), then its inbox flag
       const double2* src = reinterpret_cast<const double2*>(P.pool + (int64_t)src_s * P.slot_elems);
-      double2* out = reinterpret_cast<double2*>(P.peer_pool[aux0] + (int64_t)(P.recv_base + aux1) * P.slot_elems);
+      double2* out =
+          reinterpret_cast<double2*>(P.peer_pool[aux0] + (int64_t)(P.peer_recv_base[aux0] + aux1) * P.slot_elems);
       copy_d2(out, src, P.slot_elems / 2);
       __threadfence_system();
       cons_bar();

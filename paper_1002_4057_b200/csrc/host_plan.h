@@ -21,6 +21,7 @@ struct tinv_ctx {
   int32_t* inbox = nullptr;              // exported inbox (multi-process)
   int64_t inbox_len = 0;
   bool exported = false;                 // pool mapped by peers: must not move
+  bool attached = false;                 // peers mapped by plain pointers (tinv_peer_attach), not IPC
   int rank = -1, world = 0;
   int device = 0, nsm = 0;
   cudaStream_t st = nullptr, st2 = nullptr, own = nullptr;
@@ -29,7 +30,12 @@ struct tinv_ctx {
   int64_t pool_slots = 0, slot_elems = 0;
   std::vector<int32_t> a_slot;  // current slot of each lower tile (its home slot or its shadow T+k)
   std::vector<int32_t> home;    // home slot of each lower tile: a permutation of [0, T) (identity, or
-                                // column-major per matrix after a streamed run's reset)
+                                // column-major per matrix after a streamed run's reset); -1: a
+                                // partitioned store's tile owned by another rank
+  std::vector<int32_t> shadow;  // rename shadow slot of each lower tile (T + k; partitioned: compact)
+  int64_t mslots = 0;           // slots of the matrix tiles and their shadows (2T; partitioned: 2 x owned)
+  bool partitioned = false;     // tinv_create_owned: only this rank's tiles have slots
+  int32_t peer_rbase[MAX_RANKS] = {};  // receive-slot base of each peer's store (SEND targets)
   int32_t* d_a_slot = nullptr;
   double* staging[2] = {nullptr, nullptr};
   size_t staging_bytes = 0;

@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(256) k_put(const double* __restrict__ src, int
   const int64_t x = tri_lo + blockIdx.x;
   const int64_t m = x / T1;
   tri_decode(x - m * T1, i, j);
+  if (slot_of[x] < 0) return;  // a partitioned store: another rank's tile
   double* dst = pool + (int64_t)slot_of[x] * slot_elems;
   const int rr = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (rr >= bp) return;
@@ -104,7 +105,9 @@ __global__ void __launch_bounds__(256) k_get(double* __restrict__ dst, int64_t l
     si = sj = I;
     transp = symmetrize && (sr < sc);
   }
-  const double* tile = pool + (int64_t)slot_of[m * T1 + (int64_t)si * (si + 1) / 2 + sj] * slot_elems;
+  const int32_t src_slot = slot_of[m * T1 + (int64_t)si * (si + 1) / 2 + sj];
+  if (src_slot < 0) return;  // a partitioned store: another rank's tile (destination left as is)
+  const double* tile = pool + (int64_t)src_slot * slot_elems;
   const int br = transp ? sc : sr, bc = transp ? sr : sc;  // source sub-block
   if (vec) {
 #pragma unroll
@@ -193,6 +196,7 @@ __global__ void __launch_bounds__(256) k_pad(double* __restrict__ pool, int64_t 
   int i, j;
   const int64_t x = blockIdx.x;
   tri_decode(x % T1, i, j);
+  if (slot_of[x] < 0) return;
   double* dst = pool + (int64_t)slot_of[x] * slot_elems;
   const int rr = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (rr >= bp) return;

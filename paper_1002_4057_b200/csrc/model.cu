@@ -123,6 +123,7 @@ int tinv_model_run(int64_t n, int64_t b, const int32_t* table, int64_t ntasks, i
   c.T1 = c.t * (c.t + 1) / 2;
   c.T = c.T1;
   c.nmat = 1;
+  c.mslots = 2 * c.T;
   c.nsm = sms_per_rank * nranks;
   tinv_plan* p = nullptr;
   tinv_err err;

@@ -117,7 +117,8 @@ struct ExecParams {
   int32_t* inbox;                  // this rank's inbox flags (1 = arrived, 2 = consumed)
   const int32_t* recv_task;        // inbox index -> exec task id (-1: not received here)
   int32_t nrecv;                   // inbox length
-  int32_t recv_base;               // slot of receive sequence number 0 (same on every rank)
+  int32_t recv_base;               // slot of this store's receive sequence number 0
+  int32_t peer_recv_base[MAX_RANKS];  // the same in each peer's store (SEND targets; differs when partitioned)
   const int32_t* recv_gate;        // streamed arrivals: entry -> copy run (null: the entry's own inbox flag)
   const int32_t* gate_flag;        // per copy run: 1 = arrived (stream write-value)
   // streamed host output (DEPART; the copy engines do the device -> host moves)

@@ -181,12 +181,106 @@ def execute_distributed(stream: TaskStream, a, grid=(1, 2), transport="loopback"
     return d
 
 
+def execute_ranks_local(stream: TaskStream, a, grid=(1, 2), sms_per_rank=None, partition=False):
+    """The multi-process runtime with every rank in THIS process on one B200:
+    one tile store (tinv_ctx) and one transfer plan per rank (exactly what
+    `MultiGPU` builds per process), each rank's persistent executor on its own
+    share of the SMs (`tinv_set_sms`) so the ranks run concurrently, peers
+    mapped by device pointer (`tinv_peer_attach`, the in-process form of the
+    CUDA-IPC mapping), SEND work items writing into the receivers' stores and
+    inboxes. `partition`: each rank's store holds only the tiles it owns
+    (tinv_create_owned). Gathers every rank's owned tiles into `a`.
+    -> (DistStream, per-rank device ms, per-rank store bytes)."""
+    import threading
+
+    import torch
+
+    from .scheduler import ExecutionError, InvalidStreamError, _cause
+    from .tile_matrix import _NONE
+    if a.t != stream.t:
+        raise InvalidStreamError(f"stream generated for t={stream.t} cannot run on a t={a.t} matrix")
+    d = distribute(stream, grid, a.label)
+    W = d.world
+    nsm = sms_per_rank or torch.cuda.get_device_properties(0).multi_processor_count // W
+    P, Q = grid
+    a._pull()
+    host = a._host
+    ctxs, plans, srcs = [], [], []
+    try:
+        for r in range(W):
+            if partition:
+                ctx = _native.Context.owned(a.n, a.b, owned_tiles(a.t, grid, r))
+            else:
+                ctx = _native.Context(a.n, a.b)
+            ctx.set_sms(nsm)
+            ctx.put_dense(host)
+            table, aux, nrecv, src = transfer_plan(d, r)
+            plan = _native.Plan.xfer(ctx, table, stream.t, aux, nrecv)
+            if plan.rc != _native.OK:
+                raise _native.NativeError(plan.rc, plan.msg)
+            plan.ipc_export()
+            ctxs.append(ctx)
+            plans.append(plan)
+            srcs.append(src)
+        for r, ctx in enumerate(ctxs):
+            ctx.peer_attach(r, ctxs)
+            ctx.ipc_reset()
+        res = [None] * W
+        start = threading.Barrier(W)
+
+        def run(r):
+            start.wait()
+            res[r] = plans[r].run()
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(W)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        fails = []
+        for r, (rc, err, ms) in enumerate(res):
+            if rc != _native.OK:
+                sid = int(srcs[r][err.task_id]) if 0 <= err.task_id < len(srcs[r]) else -1
+                fails.append((sid if sid >= 0 else 2 ** 62, r, rc, err.code, err.index, plans[r].msg))
+        if fails:
+            a._state = _NONE
+            sid, r, rc, code, index, msg = min(fails)
+            if sid >= 2 ** 62:
+                raise _native.NativeError(rc, msg or f"rank {r} failed")
+            e = _native.TinvErr(int(sid), -1, int(code), int(index))
+            cause = _cause(e, msg)
+            raise ExecutionError(stream.tasks[int(sid)], cause) from cause
+        b = a.b
+        for r, ctx in enumerate(ctxs):
+            out = np.zeros((a.n, a.n))
+            ctx.get_dense(out, _native.DENSE_LOWER)
+            for i in range(a.t):
+                for j in range(i + 1):
+                    if (i % P) * Q + (j % Q) == r:
+                        a._host[i * b:(i + 1) * b, j * b:(j + 1) * b] = out[i * b:(i + 1) * b, j * b:(j + 1) * b]
+        a._state = _NONE
+        return d, [x[2] for x in res], [c.store_bytes() for c in ctxs]
+    finally:
+        for pl in plans:
+            pl.close()
+        for c in ctxs:
+            c.close()
+
+
 def default_grid(world: int):
     """P x Q with P <= Q, as square as possible (1x2, 2x2, 2x4, ...)."""
     p = int(np.sqrt(world))
     while world % p:
         p -= 1
     return (p, world // p)
+
+
+def owned_tiles(t, grid, rank):
+    """(t, t) int32 mask of the lower tiles `rank` owns (2D block-cyclic) --
+    the ownership argument of a partitioned store (`_native.Context.owned`)."""
+    P, Q = grid
+    return np.array([[1 if j <= i and (i % P) * Q + (j % Q) == rank else 0 for j in range(t)] for i in range(t)],
+                    np.int32)
 
 
 def owned_mask(n, b, grid, rank, device):
@@ -224,8 +318,9 @@ class MultiGPU:
             raise _native.NativeError(self.plan.rc, self.plan.msg or "plan failed on a peer rank")
         hp, hi = self.plan.ipc_export()
         hs = [None] * self.world
-        dist.all_gather_object(hs, (hp, hi))
+        dist.all_gather_object(hs, (hp, hi, ctx.recv_base()))
         ctx.ipc_open(self.rank, self.world, [h[0] for h in hs], [h[1] for h in hs])
+        ctx.ipc_recv_bases([h[2] for h in hs])  # partitioned stores: each peer's receive slots start elsewhere
 
     def run(self):
         """Every rank: reset inbox, barrier, execute. -> (rc, err, device ms)."""
@@ -244,10 +339,11 @@ def _agree(flag: bool) -> bool:
     return int(v.item()) == 0
 
 
-def execute_multi_gpu(stream: TaskStream, a, grid=None):
+def execute_multi_gpu(stream: TaskStream, a, grid=None, partition=True):
     """`execute` over all ranks of the default process group (one B200 each):
     every rank passes the same stream and matrix; on return every rank's `a`
-    holds the full result (owned tiles all-reduced over NCCL)."""
+    holds the full result (owned tiles all-reduced over NCCL). partition: each
+    rank's store holds only its own tiles (tinv_create_owned)."""
     import torch
     import torch.distributed as dist
 
@@ -256,7 +352,13 @@ def execute_multi_gpu(stream: TaskStream, a, grid=None):
     if a.t != stream.t:
         raise InvalidStreamError(f"stream generated for t={stream.t} cannot run on a t={a.t} matrix")
     dev = torch.cuda.current_device()
-    ctx = a._device(dev)
+    grid = grid or default_grid(dist.get_world_size())
+    if partition:
+        a._pull()
+        ctx = _native.Context.owned(a.n, a.b, owned_tiles(a.t, grid, dist.get_rank()), dev)
+        ctx.put_dense(a._host)
+    else:
+        ctx = a._device(dev)
     mg = MultiGPU(stream, ctx, grid, a.label)
     rc, err, _ = mg.run()
     src_id = int(mg.src[err.task_id]) if rc != _native.OK and 0 <= err.task_id < len(mg.src) else -1
@@ -277,8 +379,10 @@ def execute_multi_gpu(stream: TaskStream, a, grid=None):
     # the zero fill runs on torch's stream, the gather on the context's own
     # (non-blocking) stream: order them (get_dense_device syncs its stream on return)
     torch.cuda.current_stream().synchronize()
-    ctx.get_dense_device(x.data_ptr(), a.n, _native.DENSE_LOWER)
+    ctx.get_dense_device(x.data_ptr(), a.n, _native.DENSE_LOWER)  # (a partitioned store leaves others' tiles 0)
     x *= owned_mask(a.n, a.b, mg.grid, mg.rank, "cuda")
+    if partition:
+        ctx.close()
     dist.all_reduce(x)
     full = x.cpu().numpy()
     b = a.b

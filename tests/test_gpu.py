@@ -426,6 +426,30 @@ def test_distributed_loopback_bitwise(grid):
         assert d.stats(b)["transfers"] > 0
 
 
+@pytest.mark.parametrize("grid,partition", [((1, 2), False), ((2, 2), False), ((1, 2), True), ((2, 2), True),
+                                            ((2, 4), True)])
+def test_distributed_separate_stores_concurrent_ranks(grid, partition):
+    """The multi-process runtime's data path with every rank in this process:
+    one store and one transfer plan per rank (what MultiGPU builds), the ranks'
+    persistent executors running concurrently on disjoint SM shares, SENDs
+    writing into the OTHER stores and inboxes (tinv_peer_attach). partition:
+    each store holds only its rank's tiles. Bitwise equal to execute()."""
+    from paper_1002_4057_b200.distributed import execute_ranks_local
+    n, b = 1024, 128
+    a = O.spd_matrix(n, 8, 0.5)
+    for cfg in (P.VariantConfig(P.Placement.OUT_OF_PLACE), P.VariantConfig(P.Placement.IN_PLACE, "UUU", False)):
+        s = P.gen_inversion(n // b, cfg)
+        ref = P.from_dense(a, b)
+        P.execute(s, ref)
+        tm = P.from_dense(a, b)
+        d, ms, store = execute_ranks_local(s, tm, grid, partition=partition)
+        assert np.array_equal(P.to_dense(tm), P.to_dense(ref))
+        assert len(ms) == grid[0] * grid[1] and d.stats(b)["transfers"] > 0
+        if partition:
+            full = _native.Context(n, b).store_bytes()
+            assert max(store) < full  # a rank keeps its own tiles, not the whole matrix
+
+
 @pytest.mark.parametrize("grid", [(1, 2), (2, 2), (2, 4)])
 def test_distributed_device_transport_bitwise(grid):
     # SEND (CTA copy into the receiver's pool + system-scope inbox flag) and
