@@ -291,8 +291,8 @@ __device__ __forceinline__ void get_job_phase(const ItemInfo& it, int n, int R, 
     special_job(j, SP_COPY_ROWS, it.item, x, o);
     return;
   }
-  if (kind == KIND_SEND) {
-    special_job(j, SP_SEND, 0, x, -1);
+  if (kind == KIND_SEND) {  // block item of the tile version -> receiver's pool
+    special_job(j, SP_SEND, it.item, x, -1);
     return;
   }
   if (kind == KIND_DEPART) {  // block (item / R, item % R) of the result tile -> host
@@ -1120,14 +1120,21 @@ __device__ __noinline__ void run_special(const Job& jb, const ItemInfo& it, cons
       }
       break;
     }
-    case SP_SEND: {  // tile version -> receiver's pool (peer memory), then its inbox flag
-      const double2* src = reinterpret_cast<const double2*>(P.pool + (int64_t)src_s * P.slot_elems);
-      double2* out =
-          reinterpret_cast<double2*>(P.peer_pool[aux0] + (int64_t)(P.peer_recv_base[aux0] + aux1) * P.slot_elems);
-      copy_d2(out, src, P.slot_elems / 2);
+    case SP_SEND: {  // 128-block d of the tile version -> receiver's pool (peer memory); the inbox flag is
+                     // set by the task's last item (complete_item) once every block is out
+      const int64_t off = (int64_t)(d / R) * BLK * bp + (d % R) * BLK;
+      const double* src = P.pool + (int64_t)src_s * P.slot_elems + off;
+      double* out = P.peer_pool[aux0] + (int64_t)(P.peer_recv_base[aux0] + aux1) * P.slot_elems + off;
+      const int c2 = threadIdx.x & 63;  // 64 double2 per block row, 4 rows per pass, 8 loads in flight
+#pragma unroll 1
+      for (int r0 = threadIdx.x >> 6; r0 < BLK; r0 += 32) {
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(reinterpret_cast<const double2*>(src + (int64_t)(r0 + 4 * u) * bp) + c2);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) reinterpret_cast<double2*>(out + (int64_t)(r0 + 4 * u) * bp)[c2] = v[u];
+      }
       __threadfence_system();
-      cons_bar();
-      if (threadIdx.x == 0) st_release_sys_s32(P.peer_inbox[aux0] + aux1, 1);
       break;
     }
     case SP_BCOPYINV: {  // dst block (d,d) <- aux block (d,d) (lower, zero upper); zero dst blocks (d, c>d)
@@ -1398,6 +1405,10 @@ __device__ void complete_item(const ExecParams& P, const Rec& r) {
           if (P.trace_end) {
             atomicMax(P.trace_end + task, globaltimer() - P.t0);
             P.trace_sm[task] = (int)smid();
+          }
+          if (t.kind == KIND_SEND) {  // every block item fenced its copy (system scope): raise the flag
+            __threadfence_system();
+            st_release_sys_s32(P.peer_inbox[t.aux0] + t.aux1, 1);
           }
           if (t.kind == KIND_DEPART) {  // result tile final (and staged): release its copy-engine group
             P.depart_seq[atomicAdd(P.depart_seq_ctr, 1)] = t.aux0;

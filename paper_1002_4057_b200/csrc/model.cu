@@ -63,7 +63,7 @@ double phase_cost(int kind, int step, int flags, int p, int item, int R, const d
     return products(p - 1, true) + products(0, true);
   }
   if (kind == TINV_COPY) return c[C_BCOPY] * R;
-  if (kind == KIND_SEND) return c[C_SEND] * R * R;
+  if (kind == KIND_SEND) return c[C_SEND];  // one 128-block per item
   int r, cc;
   if (kind == TINV_SYRK_SUB || kind == TINV_SYRK_ADD_T || kind == TINV_LAUUM) {
     r = 0;

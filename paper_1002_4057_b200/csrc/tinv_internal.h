@@ -32,8 +32,9 @@ constexpr int SMEM_BYTES = NSTAGE * STAGE_BYTES + EXTRA_SMEM + 2048;
 // DMMA triangular multiply by the inverse).
 constexpr int KIND_INV = 11;
 // Multi-GPU transfer pseudo-tasks (csrc/api.cu tinv_plan_create_dist):
-// SEND copies a tile version into the receiver's pool (peer memory) and sets
-// the receiver's inbox flag; RECV is completed by the receiver's inbox poller.
+// SEND copies a tile version into the receiver's pool (peer memory; one item
+// per 128-block) and, once every block is out, sets the receiver's inbox flag;
+// RECV is completed by the receiver's inbox poller.
 constexpr int KIND_SEND = 12;
 constexpr int KIND_RECV = 13;
 constexpr int MAX_RANKS = 8;
@@ -177,10 +178,11 @@ TINV_HD int phase_items(int kind, int R, int p) {
       return R * (R + 1) / 2;
     case TINV_COPY:
       return R;
-    case KIND_SEND:
     case KIND_RECV:
     case KIND_ARRIVE:
       return 1;
+    case KIND_SEND:  // one item per 128-block: the tile crosses NVLink from R^2 SMs at once
+      return R * R;
     default:
       return R * R;
   }
