@@ -93,7 +93,7 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 }
 
 // ---------------------------------------------------------------- program
-__device__ int gen_program(BOp* ops, int nb) {
+__host__ __device__ int gen_program(BOp* ops, int nb) {
   int k = 0;
   auto mma = [&](int aa, int ai, int aj, int ba, int bi, int bj, int flags, int kr, int st, int oi, int oj, int sg,
                  int ca = 0, int ci = 0, int cj = 0) {
@@ -146,6 +146,11 @@ __device__ int gen_program(BOp* ops, int nb) {
       }
   return k;
 }
+
+// the block programs for nb = 1..4, generated on the host once per device (a
+// per-CTA gen_program put ~1100 instructions in front of every matrix)
+__constant__ BOp c_prog[NBMAX][MAXOPS];
+__constant__ int c_nops[NBMAX];
 
 // ---------------------------------------------------------------- DMMA quad product
 // acc (16x16 quad at rows 16 qr.., cols 16 qc..; 2x2 m8n8 tiles) +=
@@ -244,7 +249,7 @@ __constant__ int8_t c_map[3][4][4] = {
 __device__ __forceinline__ void load_blk(double* S, const double* G, int n, int bi, int bj) {
   const int r0 = bi * BB, c0 = bj * BB;
   if ((n & 1) == 0) {
-#pragma unroll
+#pragma unroll 4
     for (int u = 0; u < 16; ++u) {
       const int idx = threadIdx.x + NT * u, r = idx >> 5, c = (idx & 31) * 2;
       const bool ok = r0 + r < n && c0 + c < n;
@@ -346,18 +351,15 @@ __global__ void __launch_bounds__(NT, 3)
     k_bsmall(const double* __restrict__ A, double* X, int n, int nb, int64_t mstride, unsigned long long* fail,
               int64_t id0, unsigned long long* prof) {
   extern __shared__ __align__(128) double dsm[];
-  __shared__ BOp ops[MAXOPS];
-  __shared__ int sfail, nops;
+  __shared__ int sfail;
+  const BOp* ops = c_prog[nb - 1];
   const int64_t mat = blockIdx.x;
   const double* const a = A + mat * mstride;
   double* const x = X + mat * mstride;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tg = lane & 3;
-  if (tid == 0) {
-    nops = gen_program(ops, nb);
-    sfail = 1 << 30;
-  }
+  if (tid == 0) sfail = 1 << 30;
   __syncthreads();
-  const int nop = nops;
+  const int nop = c_nops[nb - 1];
   auto buf = [&](int b) { return dsm + b * BUFD; };
   auto base = [&](int arr) -> const double* { return arr ? x : a; };
   int tag0 = 0, tag1 = 0;  // global block held by buffer 0 / 1 (0: none)
@@ -560,6 +562,14 @@ cudaError_t launch_bsmall(const double* dA, double* dX, int64_t batch, int64_t n
   if (r != cudaSuccess) return r;
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
   if (!(attr_set >> dev & 1)) {
+    {
+      static bsm::BOp prog[bsm::NBMAX][bsm::MAXOPS];
+      int nops[bsm::NBMAX];
+      for (int nb = 1; nb <= bsm::NBMAX; ++nb) nops[nb - 1] = bsm::gen_program(prog[nb - 1], nb);
+      r = cudaMemcpyToSymbol(bsm::c_prog, prog, sizeof prog);
+      if (r == cudaSuccess) r = cudaMemcpyToSymbol(bsm::c_nops, nops, sizeof nops);
+      if (r != cudaSuccess) return r;
+    }
     r = cudaFuncSetAttribute(bsm::k_bsmall<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm::SMEM_DYN);
     if (r == cudaSuccess)
       r = cudaFuncSetAttribute(bsm::k_bsmall<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm::SMEM_DYN);
