@@ -640,7 +640,18 @@ double weight_of(int kind) {  // flops in units of b^3 (SURVEY.md §7 hard part 
 // in parallel. The diagonal chains dominate when the DAG is latency-bound
 // (C2: a POTRF of a 256 tile takes ~5x a GEMM of the same tile although it
 // does a sixth of its flops), so bottom levels in flops under-prioritise them.
-double latency_of(int kind, int R) {
+// latency of a mirrored (symmetric-output) block item beyond its block
+// products, in block-product units (TINV_MIRROR_COST). Measured at C2: a
+// mirrored SYRK_ADD_T item takes 69 us against 46 us for a GEMM item of the
+// same K; weighting it 2.5 (GEMM: 0.5) puts step 3's diagonal accumulation
+// chains -- the DAG's tail -- ahead of the off-diagonal ones: 19.14 -> 18.94 ms
+// (0.5 / 1.0 / 1.5 / 2.5: 19.14 / 19.05 / 19.08 / 18.94 ms).
+static double mirror_cost() {
+  static const double v = getenv("TINV_MIRROR_COST") ? atof(getenv("TINV_MIRROR_COST")) : 2.5;
+  return v;
+}
+
+double latency_of(int kind, int R, int flags = 0) {
   const double r = R;
   switch (kind) {
     case KIND_POTRF_INV:  // R factor+inverse blocks, TRSM / update phases, the full inverse
@@ -655,7 +666,12 @@ double latency_of(int kind, int R) {
     case KIND_ARRIVE:
     case KIND_DEPART:
       return 0.0;
-    default:  // GEMM, SYRK, TRSM, TRMM, LAUUM: one phase of K <= R block products
+    case TINV_SYRK_ADD_T:  // symmetric outputs: the generic epilogue with the mirror (C2: 69 us an item
+    case TINV_LAUUM:       // against 46 us for a GEMM of the same K)
+      return r + mirror_cost();
+    case TINV_SYRK_SUB:
+      return r + ((flags & TF_NO_MIRROR) ? 0.5 : mirror_cost());
+    default:  // GEMM, TRSM, TRMM: one phase of K <= R block products
       return r + 0.5;
   }
 }
@@ -1316,13 +1332,15 @@ int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, c
   for (int64_t u = nx - 1; u >= 0; --u) {
     double m = 0.0;
     for (int32_t k = p->tasks[u].succ_begin; k < p->tasks[u].succ_end; ++k) m = std::max(m, bl[p->succ[k]]);
-    bl[u] = (xs[u].kind == KIND_DEPART ? dw : lat ? latency_of(xs[u].kind, R) : weight_of(xs[u].kind)) + m;
+    bl[u] = (xs[u].kind == KIND_DEPART ? dw : lat ? latency_of(xs[u].kind, R, xs[u].flags) : weight_of(xs[u].kind)) + m;
     blmax = std::max(blmax, bl[u]);
   }
   std::vector<char> renamed_tile(p->nlogical, 0);
   if (sio) p->rename_parity.assign(T, 0);
   const int NQ = nranks * NLEV;  // queue sets: one per rank
   std::vector<int64_t> lev_items(NQ, 0);
+
+  FILE* dump = getenv("TINV_DUMP_LEVELS") ? fopen(getenv("TINV_DUMP_LEVELS"), "w") : nullptr;  // debug
   p->exec_ref.resize(nx);
   for (int64_t u = 0; u < nx; ++u) {
     TaskDev& d = p->tasks[u];
@@ -1352,11 +1370,13 @@ int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, c
     int lev = blmax > 0 ? (int)std::floor(NLEV * (1.0 - std::pow(bl[u] / blmax, prio_exp))) : 0;
     lev = std::min(NLEV - 1, std::max(0, lev));
     if (x.kind == KIND_DEPART) lev = 0;  // cheap, and the copy engines wait on it
+    if (dump) fprintf(dump, "%lld %d %d %d %.3f %d\n", (long long)u, x.kind, x.ref, x.out, bl[u], lev);
     d.level = (int8_t)lev;
     lev_items[d.rank * NLEV + lev] += d.nitems;
     p->items += d.nitems;
     p->exec_ref[u] = x.ref;
   }
+  if (dump) fclose(dump);
   if (sio) {  // departures in predicted completion order: the last writer's top level (earliest finish on
               // unbounded workers); after a run the observed order replaces it (tinv_plan_exec_host)
     std::vector<double> tl(nx, 0.0);
@@ -1438,7 +1458,7 @@ int plan_build(tinv_ctx* c, const int32_t* table, int64_t n, int32_t stream_t, c
   }
   if (flags & TINV_TRACE) {
     if (ckm((void**)&p->d_ts, nx * 8) || ckm((void**)&p->d_te, nx * 8) || ckm((void**)&p->d_tsm, nx * 4) ||
-        ckm((void**)&p->d_tr, nx * 8)) {
+        ckm((void**)&p->d_tr, 2 * nx * 8)) {
       tinv_plan_destroy(p);
       return fail(c, TINV_ERR_CUDA, "trace allocation failed");
     }
@@ -1842,6 +1862,7 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
     CK(c, cudaMemsetAsync(p->d_te, 0, nx * 8, st));
     CK(c, cudaMemsetAsync(p->d_tsm, 0xff, nx * 4, st));
     CK(c, cudaMemsetAsync(p->d_tr, 0, nx * 8, st));
+    CK(c, cudaMemsetAsync(p->d_tr + nx, 0xff, nx * 8, st));  // first claim of each task (atomicMin)
   }
   std::vector<int32_t> from(T), to(T);
   if (keep) {
@@ -1997,8 +2018,8 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
     CK(c, cudaMemcpy(p->h_te.data(), p->d_te, nx * 8, cudaMemcpyDeviceToHost));
     CK(c, cudaMemcpy(p->h_tsm.data(), p->d_tsm, nx * 4, cudaMemcpyDeviceToHost));
     if (getenv("TINV_READY_PROFILE")) {  // dispatch delay: ready (in-degree 0) -> first item start
-      std::vector<unsigned long long> tr(nx);
-      CK(c, cudaMemcpy(tr.data(), p->d_tr, nx * 8, cudaMemcpyDeviceToHost));
+      std::vector<unsigned long long> tr(2 * nx);
+      CK(c, cudaMemcpy(tr.data(), p->d_tr, 2 * nx * 8, cudaMemcpyDeviceToHost));
       static const char* kn[] = {"COPY", "POTRF", "TRSM", "SYRK_SUB", "SYRK_ADD_T", "GEMM", "TRTRI", "TRMM_L",
                                  "TRMM_RN", "TRMM_LT", "LAUUM", "INV", "SEND", "RECV", "ARRIVE", "DEPART", "POTRF_INV"};
       double sum[17] = {0}, mx[17] = {0};
@@ -2014,6 +2035,19 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
       fprintf(stderr, "[tinv ready] dispatch delay per kind (tasks, mean us, max us):");
       for (int k = 0; k < 17; ++k)
         if (cnt[k]) fprintf(stderr, " %s %d %.1f %.1f |", kn[k], cnt[k], sum[k] / cnt[k], mx[k]);
+      fprintf(stderr, "\n");
+      // split: ready -> first claim by a producer (queueing) and claim -> first item start (the
+      // claiming CTA's consumers still busy / operands streaming)
+      double q[17] = {0}, w[17] = {0}, qm[17] = {0}, wm[17] = {0};
+      for (int64_t u = 0; u < nx; ++u) {
+        const int k = p->tasks[u].kind;
+        if (k < 0 || k > 16 || p->h_ts[u] == ~0ull || !tr[u] || tr[nx + u] == ~0ull) continue;
+        const double a = ((double)tr[nx + u] - (double)tr[u]) * 1e-3, b = ((double)p->h_ts[u] - (double)tr[nx + u]) * 1e-3;
+        q[k] += a, w[k] += b, qm[k] = std::max(qm[k], a), wm[k] = std::max(wm[k], b);
+      }
+      fprintf(stderr, "[tinv ready] ready->claim / claim->start per kind (mean us, max us):");
+      for (int k = 0; k < 17; ++k)
+        if (cnt[k]) fprintf(stderr, " %s %.1f/%.1f %.1f/%.1f |", kn[k], q[k] / cnt[k], qm[k], w[k] / cnt[k], wm[k]);
       fprintf(stderr, "\n");
     }
   }

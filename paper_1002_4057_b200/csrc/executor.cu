@@ -1718,6 +1718,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(&ctl.item_empty[slot], ((itn >> 1) & 1) ^ 1);
       ptick(0);
       const unsigned long long e = next ? next : pop_item(P, own);  // all 32 lanes
+      if (P.trace_ready && lane == 0 && e && e != POP_EXIT)  // TINV_READY_PROFILE: first claim of the task
+        atomicMin(P.trace_ready + P.ntasks + (int)(e >> 32) - 1, globaltimer() - P.t0);
       ptick(1);
       next = produce_item(e, slot, P, ctl, ring, tmK, tmM, R, ks, issued);
       ptick(2);

@@ -77,3 +77,9 @@ print("  tasks with an empty trace span:", dict(zero))
 u0, v0 = worst[0]
 print(f"  preds of {names[table[v0, 0]]}({v0}) start {st[v0] / 1e3:.1f} us:",
       [(names[table[q, 0]], int(q), round(en[q] / 1e3, 1)) for q in pred[v0]])
+# optional: the critical path's task ids and times, for joining with TINV_DUMP_LEVELS
+if len(sys.argv) > 4:
+    import json
+    with open(sys.argv[4], "w") as fh:
+        json.dump({"path": [int(v) for v in path], "st": [int(st[v]) for v in path], "en": [int(en[v]) for v in path],
+                   "running_at_ready": [running_at(en[u] + 1) for u in path]}, fh)
