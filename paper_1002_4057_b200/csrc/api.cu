@@ -325,9 +325,44 @@ static int ensure_bstage(tinv_ctx* c) {
   return TINV_OK;
 }
 
+// partitioned store (tinv_create_owned): only this rank's tiles cross PCIe,
+// one 2D copy per owned tile straight into its slot (+ the closure padding)
+static int put_owned_tiles(tinv_ctx* c, const double* host, int64_t lda) {
+  int rc = sync_slots(c);
+  if (rc) return rc;
+  const int64_t b = c->b, bp = c->bp;
+  for (int64_t i = 0; i < c->t; ++i)
+    for (int64_t j = 0; j <= i; ++j) {
+      const int32_t sl = c->a_slot[tri_index(i, j)];
+      if (sl < 0) continue;
+      CK(c, cudaMemcpy2DAsync(c->pool + (int64_t)sl * c->slot_elems, bp * 8, host + i * b * lda + j * b, lda * 8,
+                              b * 8, b, cudaMemcpyHostToDevice, c->st));
+    }
+  if (bp != b) CK(c, launch_pad(c->pool, c->slot_elems, c->d_a_slot, (int)b, (int)bp, c->T, c->T1, c->st));
+  CK(c, cudaStreamSynchronize(c->st));
+  return TINV_OK;
+}
+
+static int get_owned_tiles(tinv_ctx* c, double* host, int64_t lda, int mode) {
+  if (mode != TINV_DENSE_LOWER_TILES) return fail(c, TINV_ERR_BAD_ARG, "a partitioned store returns its own lower tiles only");
+  int rc = sync_slots(c);
+  if (rc) return rc;
+  const int64_t b = c->b, bp = c->bp;
+  for (int64_t i = 0; i < c->t; ++i)
+    for (int64_t j = 0; j <= i; ++j) {
+      const int32_t sl = c->a_slot[tri_index(i, j)];
+      if (sl < 0) continue;
+      CK(c, cudaMemcpy2DAsync(host + i * b * lda + j * b, lda * 8, c->pool + (int64_t)sl * c->slot_elems, bp * 8,
+                              b * 8, b, cudaMemcpyDeviceToHost, c->st));
+    }
+  CK(c, cudaStreamSynchronize(c->st));
+  return TINV_OK;
+}
+
 int tinv_put_dense(tinv_ctx* c, const double* host, int64_t lda) {
   if (!c || !host || lda < c->n) return fail(c, TINV_ERR_BAD_ARG, "bad put_dense arguments");
   CK(c, cudaSetDevice(c->device));
+  if (c->partitioned) return put_owned_tiles(c, host, lda);
   if (c->nmat > 1) {  // batch: one bulk copy of all matrices, then one conversion
     int rc = ensure_bstage(c);
     if (rc) return rc;
@@ -369,6 +404,7 @@ int tinv_put_dense(tinv_ctx* c, const double* host, int64_t lda) {
 int tinv_get_dense(tinv_ctx* c, double* host, int64_t lda, int mode) {
   if (!c || !host || lda < c->n) return fail(c, TINV_ERR_BAD_ARG, "bad get_dense arguments");
   CK(c, cudaSetDevice(c->device));
+  if (c->partitioned) return get_owned_tiles(c, host, lda, mode);
   if (c->nmat > 1) {
     int rc = ensure_bstage(c);
     if (rc) return rc;

@@ -450,6 +450,36 @@ def test_distributed_separate_stores_concurrent_ranks(grid, partition):
             assert max(store) < full  # a rank keeps its own tiles, not the whole matrix
 
 
+def test_partitioned_store_transfers_only_owned_tiles():
+    """tinv_create_owned: put_dense / get_dense move this rank's tiles only (one
+    2D copy per tile); other ranks' tiles of the host buffer stay untouched,
+    and plans touching them are rejected."""
+    from paper_1002_4057_b200.distributed import owned_tiles
+    n, b, grid = 640, 128, (2, 2)
+    t = n // b
+    a = O.spd_matrix(n, 3, 0.5)
+    for r in range(4):
+        own = owned_tiles(t, grid, r)
+        ctx = _native.Context.owned(n, b, own)
+        assert ctx.store_bytes() < _native.Context(n, b).store_bytes()
+        ctx.put_dense(a)
+        out = np.full((n, n), 7.0)
+        ctx.get_dense(out, _native.DENSE_LOWER)
+        for i in range(t):
+            for j in range(t):
+                blk = out[i * b:(i + 1) * b, j * b:(j + 1) * b]
+                if j <= i and own[i, j]:
+                    assert np.array_equal(blk, a[i * b:(i + 1) * b, j * b:(j + 1) * b])
+                else:
+                    assert (blk == 7.0).all()
+        with pytest.raises(_native.NativeError):
+            ctx.get_dense(out, _native.DENSE_SYMMETRIZE)
+        s = P.gen_inversion(t, P.VariantConfig())  # the whole stream touches every tile
+        plan = _native.Plan(ctx, s.table(), t, np.zeros(0, np.int64))
+        assert plan.rc != _native.OK and "another rank" in plan.msg
+        ctx.close()
+
+
 @pytest.mark.parametrize("grid", [(1, 2), (2, 2), (2, 4)])
 def test_distributed_device_transport_bitwise(grid):
     # SEND (CTA copy into the receiver's pool + system-scope inbox flag) and
