@@ -83,3 +83,14 @@ if len(sys.argv) > 4:
     with open(sys.argv[4], "w") as fh:
         json.dump({"path": [int(v) for v in path], "st": [int(st[v]) for v in path], "en": [int(en[v]) for v in path],
                    "running_at_ready": [running_at(en[u] + 1) for u in path]}, fh)
+# optional: what ran during the worst gaps (kind histogram of the tasks running at the successor's ready time)
+if len(sys.argv) > 5:
+    for u, v in worst[:4]:
+        tr_ = en[u] + 1
+        run_ = [q for q in range(len(en)) if st[q] <= tr_ < en[q]]
+        started_ = [q for q in range(len(en)) if tr_ <= st[q] < st[v]]
+        kinds = defaultdict(int)
+        for q in started_:
+            kinds[names[table[q, 0]]] += 1
+        print(f"  gap before {names[table[v, 0]]}({v}): {len(run_)} running at ready, tasks started inside the gap "
+              f"{len(started_)}: {dict(kinds)}; their ids {sorted(started_)[:12]}")
