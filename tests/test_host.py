@@ -226,6 +226,34 @@ def test_fused_batched_engine_selection_and_abi_validation():
     _native.batch_engine(prev)
 
 
+def test_multi_rank_abi_validation_host_only():
+    """The multi-rank entry points reject bad arguments without a device:
+    tinv_peer_attach / tinv_set_sms / tinv_create_owned / tinv_recv_base /
+    tinv_ipc_recv_bases (include/tileinv_b200.h)."""
+    import ctypes
+    L = _native.lib()
+    assert L.tinv_set_sms(None, 4) == _native.ERR_BAD_ARG
+    assert L.tinv_peer_attach(None, 0, 1, None) == _native.ERR_BAD_ARG
+    assert L.tinv_ipc_recv_bases(None, 1, None) == _native.ERR_BAD_ARG
+    assert L.tinv_recv_base(None, None) == _native.ERR_BAD_ARG
+    h = ctypes.c_void_p()
+    assert L.tinv_create_owned(ctypes.byref(h), 256, 128, 0, None) == _native.ERR_BAD_ARG  # null mask
+    # with a mask but no device: no store is created
+    own = np.ones((2, 2), np.int32)
+    rc = L.tinv_create_owned(ctypes.byref(h), 256, 128, 0, own.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+    assert rc == _native.ERR_NO_DEVICE and not h.value
+
+
+def test_owned_tiles_partition_the_lower_tiles():
+    """distributed.owned_tiles: the 2D block-cyclic ownership masks of the
+    ranks of a grid cover every lower tile exactly once."""
+    from paper_1002_4057_b200.distributed import owned_tiles
+    for grid in ((1, 1), (1, 2), (2, 2), (2, 4)):
+        t = 9
+        tot = sum(owned_tiles(t, grid, r) for r in range(grid[0] * grid[1]))
+        assert np.array_equal(tot, np.tril(np.ones((t, t), np.int32)))
+
+
 def test_schedule_model_host_only():
     """csrc/model.cu: the executor's schedule simulated on the host (no GPU):
     deadlock-free on single-GPU and transfer plans, busy SM-time independent of
