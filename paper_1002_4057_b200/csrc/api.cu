@@ -2116,14 +2116,17 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
             "completion %.0f | items %.0f jobs %.0f | special totals: load %.0f factor %.0f inverse %.0f store %.0f\n",
             tot[0] / items, tot[1] / items, tot[2] / items, tot[3] / items, tot[4] / items, tot[5] / items, tot[6],
             tot[7], tot[8], tot[9], tot[10], tot[11]);
-    fprintf(stderr, "[tinv phase] potrf factor %.0f subst %.0f trailing %.0f | trtri base %.0f l16 %.0f l32 %.0f l64 %.0f\n",
-            tot[12], tot[13], tot[14], tot[15], tot[16], tot[17], tot[18]);
+    fprintf(stderr, "[tinv phase] trtri base %.0f l16 %.0f l32 %.0f l64 %.0f\n", tot[15], tot[16], tot[17], tot[18]);
     const double pops = tot[23] > 0 ? tot[23] : 1;
     fprintf(stderr,
             "[tinv phase] producer per pop: slot-wait %.0f pop %.0f produce %.0f (pops %.0f) | storer per item: "
             "quarters %.0f job-end %.0f item-end %.0f idle %.0f\n",
             tot[20] / pops, tot[21] / pops, tot[22] / pops, tot[23], tot[24] / items, tot[25] / items,
             tot[26] / items, tot[27] / items);
+    fprintf(stderr, "[tinv phase] consumer idle (item-wait) share of the SMs per ~1 ms bin:");
+    for (int k = 0; k < PHASE_NBIN; ++k)
+      if (tot[PHASE_BIN0 + k] > 0) fprintf(stderr, " %d:%.3f", k, tot[PHASE_BIN0 + k] / (c->nsm * 1048576.0 * 1.965));
+    fprintf(stderr, "\n");
   }
   if (ekey != ~0ull || ctr_out[0] != 0) {
     if (keep) {

@@ -385,6 +385,11 @@ struct Rec {
 constexpr int NREC = 16;
 constexpr int MAXJ = 8;
 
+struct PotrfFlags {
+  int fac;      // panels whose L_PP (+ 1 / l_kk) is published
+  int rowdone;  // panels whose row block P + 1 warp 0 has solved
+  int ready;    // rounds P whose blocks (P + 2, P + 1) and (P + 2, P + 2) are updated by panel P
+};
 struct SmemCtl {
   uint64_t full[NSTAGE];
   uint64_t empty[NSTAGE];
@@ -403,6 +408,7 @@ struct SmemCtl {
   int scan_min;
   unsigned long long dbg[4];
   unsigned long long dbg2[8];
+  PotrfFlags pf;  // block_potrf's warp-0 / helper counters
 };
 
 // ---------------------------------------------------------------- consumers: DMMA chunk
@@ -667,8 +673,8 @@ __device__ __forceinline__ void run_gemm(const Job& jb, const ExecParams& P, Sme
 // ---------------------------------------------------------------- consumers: diagonal phases
 // A 128x128 diagonal block in shared memory uses row stride SLD = 132 doubles.
 constexpr int SLD = BLK + 4;  // = 4 mod 16 doubles: m8n8k4 fragment loads (rows g, cols tg) hit distinct banks
-// after the 128x128 block (row stride SLD): [0, 64) block_potrf's staging of
-// the factored 8x8 block, [XD_OFF, XD_OFF + 1024) the 8x8 diagonal inverses,
+// after the 128x128 block (row stride SLD): [0, 16) block_potrf's 1 / l_kk of
+// the last two panels, [XD_OFF, XD_OFF + 1024) the 8x8 diagonal inverses,
 // then 8 x 64 doubles of level-8 products (all inside block_trtri_dmma's T area)
 constexpr int XD_OFF = 64;
 constexpr int XT_OFF = XD_OFF + 16 * 64;
@@ -747,10 +753,33 @@ __device__ __forceinline__ void inv8(const double (&l)[8][8], double (&x)[8][8])
   }
 }
 
-// Cholesky of the lower 8x8 block at (p0, p0) of S in registers
-// (right-looking; kernels.py:68-71 failure test: not d > 0, or d non-finite):
-// l = the factor, x = l^-1. Returns the first failing pivot or -1.
-__device__ __forceinline__ int chol8_inv(const double* S, int p0, double (&l)[8][8], double (&x)[8][8]) {
+// ---- dataflow 128x128 block Cholesky (tools/micro/potrf_flow.cu times it and
+// checks it against the look-ahead version it replaced: 66K -> 42K cycles).
+//
+// Warp 0 runs the pivot chain alone: per 8-wide panel P it factors the 8x8
+// diagonal block in registers (chol8), publishes L_PP, solves row block P + 1
+// of the panel (lanes 0-7, one row each, by substitution) and applies panel P
+// to the diagonal block (P + 1, P + 1) itself -- the only work between two
+// chol8's. Warps 1-7 (the helpers) solve the rest of the panel and apply it
+// to the trailing blocks, the blocks warp 0 needs next first, synchronised
+// with warp 0 through three shared counters (no CTA-wide barrier per panel).
+// Every block (i, j) still receives panels 0, 1, ... in order, each as two
+// m8n8k4 DMMAs (k 0-3, then 4-7).
+__device__ __forceinline__ int ld_acq_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void helper_bar() { asm volatile("bar.sync 4, 224;" ::: "memory"); }
+
+// Cholesky of the lower 8x8 block at (p0, p0) of S in registers (kernels.py:68-71
+// failure test: not d > 0, or d non-finite; the pivot is then taken as 1 so the
+// chain completes): l = the factor, il[k] = 1 / l[k][k]. Returns the first
+// failing pivot or -1.
+__device__ __forceinline__ int chol8(const double* S, int p0, double (&l)[8][8], double (&il)[8]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -761,118 +790,173 @@ __device__ __forceinline__ int chol8_inv(const double* S, int p0, double (&l)[8]
     const double d = l[k][k];
     const bool b = !(d > 0.0) || !isfinite(d);
     bad = (b && bad < 0) ? k : bad;
-    const double il = b ? 1.0 : rsqrt(d);
-    l[k][k] = b ? 1.0 : d * il;
+    il[k] = b ? 1.0 : rsqrt(d);
+    l[k][k] = b ? 1.0 : d * il[k];
 #pragma unroll
-    for (int i = k + 1; i < 8; ++i) l[i][k] *= il;
+    for (int i = k + 1; i < 8; ++i) l[i][k] *= il[k];
 #pragma unroll
     for (int j = k + 1; j < 8; ++j)
 #pragma unroll
       for (int i = j; i < 8; ++i) l[i][j] = fma(-l[i][k], l[j][k], l[i][j]);
   }
-  inv8(l, x);
   return bad;
 }
 
-// Trailing update by panel p0 (8 columns, K = 8) of the lower 8x8 tiles in
-// tile columns [c_lo, c_hi] (rows >= the column): S -= L_p L_p^T. Warp wl of
-// nw takes tile rows c_lo + wl, c_lo + wl + nw, ...: the row's panel fragments
-// are loaded once, its tiles go two at a time.
-__device__ __forceinline__ void upd8(double* S, int p0, int c_lo, int c_hi, int wl, int nw) {
-  constexpr int T8 = BLK / 8;
-  const int lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3;
-  for (int ti = c_lo + wl; ti < T8; ti += nw) {
-    const int r = 8 * ti + g;
-    const double a0 = -S[r * SLD + p0 + tg], a1 = -S[r * SLD + p0 + 4 + tg];
-    const int jmax = min(c_hi, ti);
-    for (int tj = c_lo; tj <= jmax; tj += 2) {
-      const bool two = tj + 1 <= jmax;
-      const int c0 = 8 * tj, c1 = two ? c0 + 8 : c0;
-      double x0[2] = {S[r * SLD + c0 + 2 * tg], S[r * SLD + c0 + 2 * tg + 1]};
-      double x1[2] = {S[r * SLD + c1 + 2 * tg], S[r * SLD + c1 + 2 * tg + 1]};
-      const double b00 = S[(c0 + g) * SLD + p0 + tg], b01 = S[(c0 + g) * SLD + p0 + 4 + tg];
-      const double b10 = S[(c1 + g) * SLD + p0 + tg], b11 = S[(c1 + g) * SLD + p0 + 4 + tg];
-      dmma(x0, a0, b00);
-      dmma(x1, a0, b10);
-      dmma(x0, a1, b01);
-      dmma(x1, a1, b11);
-      S[r * SLD + c0 + 2 * tg] = x0[0];
-      S[r * SLD + c0 + 2 * tg + 1] = x0[1];
-      if (two) {
-        S[r * SLD + c1 + 2 * tg] = x1[0];
-        S[r * SLD + c1 + 2 * tg + 1] = x1[1];
-      }
-    }
+// Row q of panel p0: v = a L_PP^-T by substitution, L_PP from S (broadcast
+// reads), 1 / l_kk at il.
+__device__ __forceinline__ void panel_row(double* S, int q, int p0, const double* il) {
+  double v[8];
+#pragma unroll
+  for (int c = 0; c < 8; c += 2) {
+    const double2 t2 = *reinterpret_cast<const double2*>(S + q * SLD + p0 + c);
+    v[c] = t2.x;
+    v[c + 1] = t2.y;
   }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    double t = v[c];
+#pragma unroll
+    for (int k = 0; k < c; ++k) t = fma(-v[k], S[(p0 + c) * SLD + p0 + k], t);
+    v[c] = t * il[c];
+  }
+#pragma unroll
+  for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2*>(S + q * SLD + p0 + c) = make_double2(v[c], v[c + 1]);
 }
 
-// In-place Cholesky of the lower 128x128 block in S over 8-wide panels with
-// look-ahead. Iteration P starts with column block P updated by panels < P
-// and columns > P by panels < P - 1:
-//   A: warps 0-3 factor the 8x8 diagonal block of panel P redundantly in
-//      registers (chol8_inv: no shuffles or smem round trips on the column
-//      chain) and each solves one panel row below it by the block inverse,
-//      while warps 4-7 apply panel P - 1 to the columns > P (DMMA);
-//   B: all warps apply panel P to column block P + 1.
-// Returns the first failing pivot (kernels.py:68-71) or -1.
-__device__ int block_potrf(double* S, SmemCtl& ctl) {
+// One warp: 8x8 block (ti, tj) -= L_i L_j^T over panel p0 (two DMMAs).
+__device__ __forceinline__ void upd_blk(double* S, int p0, int ti, int tj) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3;
+  const int r = 8 * ti + g, c0 = 8 * tj;
+  double2* cp = reinterpret_cast<double2*>(S + r * SLD + c0 + 2 * tg);
+  const double2 c2 = *cp;
+  double x[2] = {c2.x, c2.y};
+  const double a0 = -S[r * SLD + p0 + tg], a1 = -S[r * SLD + p0 + 4 + tg];
+  const double b0 = S[(c0 + g) * SLD + p0 + tg], b1 = S[(c0 + g) * SLD + p0 + 4 + tg];
+  dmma(x, a0, b0);
+  dmma(x, a1, b1);
+  *cp = make_double2(x[0], x[1]);
+}
+
+// In-place Cholesky of the lower 128x128 block in S (all 256 consumer
+// threads; lp: 16 doubles of shared scratch; fl zeroed and scan_min set by
+// the caller before a barrier). Returns the first failing pivot or -1.
+__device__ int block_potrf(double* S, double* lp, PotrfFlags& fl, int& scan_min) {
   constexpr int T8 = BLK / 8;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  if (tid == 0) ctl.scan_min = 1 << 30;
-  long long tq = clock64();
-  auto probe = [&](int k) {
-    const long long now = clock64();
-    if (tid == 0) ctl.dbg2[k] += now - tq;
-    tq = now;
-  };
-  // the factored 8x8 diagonal block until every reader is past the barrier;
-  // stage + XD_OFF: the inverses of the 16 diagonal 8x8 blocks (block_trtri_dmma's base)
-  double* stage = S + BLK * SLD;
-  for (int P = 0; P < T8; ++P) {
-    const int p0 = 8 * P;
-    if (warp < 4) {
-      double l[8][8], x[8][8];
-      const int bad = chol8_inv(S, p0, l, x);
-      if (tid == 0 && bad >= 0) atomicMin(&ctl.scan_min, p0 + bad);
-      if (tid < 8) {  // thread i stages row i of L_PP and of its inverse (rows picked by select chains)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    for (int P = 0; P < T8; ++P) {
+      const int p0 = 8 * P;
+      double l[8][8], il[8];
+      double* lpP = lp + 8 * (P & 1);  // double-buffered: helpers may still read panel P - 1's
+      const int bad = chol8(S, p0, l, il);
+      if (lane == 0 && bad >= 0) atomicMin(&scan_min, p0 + bad);
+      if (lane < 8) {  // lane r publishes row r of L_PP to S and 1 / l_rr to lp (register selects)
+        double row[8], ilr = 0.0;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          double v = 0.0, w = 0.0;
+          row[j] = 0.0;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            v = (tid == i && j <= i) ? l[i][j] : v;
-            w = (tid == i && j <= i) ? x[i][j] : w;
-          }
-          stage[8 * tid + j] = v;
-          stage[XD_OFF + 64 * P + 8 * tid + j] = w;
+          for (int i = j; i < 8; ++i) row[j] = lane == i ? l[i][j] : row[j];
         }
-      }
-      const int q = p0 + 8 + tid;  // panel row: v = a L^-T = a x^T
-      if (q < BLK) {
-        double av[8], v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) av[k] = S[q * SLD + p0 + k];
+        for (int i = 0; i < 8; ++i) ilr = lane == i ? il[i] : ilr;
+#pragma unroll
+        for (int j = 0; j < 8; j += 2)
+          *reinterpret_cast<double2*>(S + (p0 + lane) * SLD + p0 + j) = make_double2(row[j], row[j + 1]);
+        lpP[lane] = ilr;
+      }
+      __syncwarp();
+      if (lane == 0) st_rel_cta(&fl.fac, P + 1);
+      if (P + 1 == T8) break;
+      // row block P + 1 needs panels < P applied to block (P + 1, P): helpers' round P - 1
+      if (P >= 1)
+        while (ld_acq_cta(&fl.ready) < P) {
+        }
+      __syncwarp();
+      if (lane < 8) {  // row r of block (P + 1, P) by substitution with the factor in registers
+        const int q = p0 + 8 + lane;
+        double v[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          double t = 0.0;
+          double t = S[q * SLD + p0 + c];
 #pragma unroll
-          for (int k = 0; k <= c; ++k) t = fma(av[k], x[c][k], t);
-          v[c] = t;
+          for (int k = 0; k < c; ++k) t = fma(-v[k], l[c][k], t);
+          v[c] = t * il[c];
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) S[q * SLD + p0 + k] = v[k];
+        for (int c = 0; c < 8; c += 2)
+          *reinterpret_cast<double2*>(S + q * SLD + p0 + c) = make_double2(v[c], v[c + 1]);
       }
-    } else if (P >= 1 && P + 1 < T8) {
-      upd8(S, p0 - 8, P + 1, T8 - 1, warp - 4, 4);  // look-ahead: panel P - 1 on the columns > P
+      __syncwarp();
+      if (lane == 0) st_rel_cta(&fl.rowdone, P + 1);
+      upd_blk(S, p0, P + 1, P + 1);  // block (P + 1, P + 1) had panels < P applied in round P - 1
+      __syncwarp();
     }
-    cons_bar();
-    probe(0);
-    if (tid < 64) S[(p0 + (tid >> 3)) * SLD + p0 + (tid & 7)] = stage[tid];
-    if (P + 1 < T8) upd8(S, p0, P + 1, P + 1, warp, NCONS_WARPS);  // panel P on column block P + 1
-    cons_bar();
-    probe(1);
+  } else {
+    const int hw = warp - 1;  // helper warp 0..6
+    for (int P = 0; P + 1 < T8; ++P) {
+      const int p0 = 8 * P;
+      while (ld_acq_cta(&fl.fac) < P + 1) {
+      }
+      const int q = p0 + 16 + (tid - 32);  // rows of blocks P + 2 ..
+      if (q < BLK) panel_row(S, q, p0, lp + 8 * (P & 1));
+      while (ld_acq_cta(&fl.rowdone) < P + 1) {
+      }
+      helper_bar();  // every L_iP of the panel is in S
+      // warp 0's next needs first: blocks (P + 2, P + 1), (P + 2, P + 2)
+      if (P + 2 < T8 && hw == 0) {
+        upd_blk(S, p0, P + 2, P + 1);
+        upd_blk(S, p0, P + 2, P + 2);
+        __syncwarp();
+        if (lane == 0) st_rel_cta(&fl.ready, P + 1);
+      }
+      // the rest of the trailing blocks, rows P + 3 .. in units of four blocks of one row
+      // (one A fragment pair per unit, every load before the first DMMA). Units run
+      // chunk-major -- chunk q = block columns P + 1 + 4q .., rows max(P + 3, P + 1 + 4q) .. 15
+      // -- and unit c goes to helper warp c mod 7 (decoded directly, no scan)
+      {
+        const int g = lane >> 2, tg = lane & 3;
+        // warp 4 shares warp 0's SM sub-partition (FP64 pipe): it takes no update units
+        const int uw = hw < 3 ? hw : hw - 1;  // updater index 0..5 (hw 3 = warp 4: none)
+        for (int c = uw; hw != 3; c += 6) {
+          int q = 0, rem = c, i = -1;
+          for (; q < 4; ++q) {
+            const int r0 = max(P + 3, P + 1 + 4 * q), n = T8 - r0;
+            if (n <= 0) break;
+            if (rem < n) {
+              i = r0 + rem;
+              break;
+            }
+            rem -= n;
+          }
+          if (i < 0) break;
+          const int j0 = P + 1 + 4 * q, r = 8 * i + g;
+          const double a0 = -S[r * SLD + p0 + tg], a1 = -S[r * SLD + p0 + 4 + tg];
+          double x[4][2], b[4][2];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c0 = 8 * min(j0 + u, i);
+            const double2 c2 = *reinterpret_cast<const double2*>(S + r * SLD + c0 + 2 * tg);
+            x[u][0] = c2.x;
+            x[u][1] = c2.y;
+            b[u][0] = S[(c0 + g) * SLD + p0 + tg];
+            b[u][1] = S[(c0 + g) * SLD + p0 + 4 + tg];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dmma(x[u], a0, b[u][0]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dmma(x[u], a1, b[u][1]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (j0 + u <= i)
+              *reinterpret_cast<double2*>(S + r * SLD + 8 * (j0 + u) + 2 * tg) = make_double2(x[u][0], x[u][1]);
+        }
+      }
+      helper_bar();  // round P done: column P + 1 (and every block) has panels <= P applied
+    }
   }
-  const int f = ctl.scan_min;
+  cons_bar();
+  const int f = scan_min;
   return f < (1 << 30) ? f : -1;
 }
 
@@ -940,13 +1024,13 @@ __device__ __forceinline__ void dmma_group16x32(const double* L, int lld, int lr
 }
 
 // In-place inverse of the lower-triangular 128x128 block in S by recursive
-// doubling: the sixteen 8x8 diagonal inverses (inv8; from8: already left at
-// XD by block_potrf), then for s = 8, 16, 32, 64 every pair [[A,0],[B,C]] ->
+// doubling: the sixteen 8x8 diagonal inverses (inv8, from the stored factor),
+// then for s = 8, 16, 32, 64 every pair [[A,0],[B,C]] ->
 // [[A^-1,0],[-C^-1 B A^-1, C^-1]] with the products on DMMA. Strict upper
 // part of S must be zero on entry. Per level s and pair c, T = B A^-1 (A^-1
 // lower: k >= first output column) into scratch, then X21 = -C^-1 T (C^-1
 // lower: k < last output row), 16x16 groups per warp.
-__device__ void block_trtri_dmma(double* S, unsigned long long* ctl_dbg, bool from8 = false) {
+__device__ void block_trtri_dmma(double* S, unsigned long long* ctl_dbg) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int TLD = 68;
   double* Tb = S + BLK * SLD;  // T of every pair of a level: pair c at Tb + c * s * TLD
@@ -958,7 +1042,7 @@ __device__ void block_trtri_dmma(double* S, unsigned long long* ctl_dbg, bool fr
     tq = now;
     ++pk;
   };
-  if (!from8) {  // the 16 diagonal 8x8 inverses (block_potrf leaves them at XD when it ran just before)
+  {  // the 16 diagonal 8x8 inverses
     if (tid < BLK / 8) {
       double l[8][8], x[8][8];
       const int p0 = 8 * tid;
@@ -1058,10 +1142,14 @@ __device__ __noinline__ void run_special(const Job& jb, const ItemInfo& it, cons
     case SP_BPOTRF: {  // factor block (d,d) of dst in place; inverse -> aux block (d,d)
       long long t0 = clock64();
       double* blk = dst + (int64_t)d * BLK * bp + d * BLK;
+      if (threadIdx.x == 0) {
+        ctl.scan_min = 1 << 30;
+        ctl.pf.fac = ctl.pf.rowdone = ctl.pf.ready = 0;
+      }
       load_block_lower(S, blk, bp);
       cons_bar();
       long long t1 = clock64();
-      const int f = block_potrf(S, ctl);
+      const int f = block_potrf(S, S + BLK * SLD, ctl.pf, ctl.scan_min);
       long long t2 = clock64();
       if (threadIdx.x == 0) {
         ctl.dbg[0] += t1 - t0;
@@ -1080,7 +1168,7 @@ __device__ __noinline__ void run_special(const Job& jb, const ItemInfo& it, cons
       zero_upper_row(dst, d, R, bp);
       cons_bar();
       t1 = clock64();
-      block_trtri_dmma(S, ctl.dbg2, true);  // seeded by block_potrf's 8x8 inverses
+      block_trtri_dmma(S, ctl.dbg2);  // the 8x8 diagonal inverses from the stored factor, as TRTRI forms them
       t2 = clock64();
       double* aux = P.pool + (int64_t)src_s * P.slot_elems;
       store_block_lower(S, aux + (int64_t)d * BLK * bp + d * BLK, bp);
@@ -1737,7 +1825,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONS_REGS));
   unsigned ks = 0;
   EpiState es = {0u, 0u, 0u, 0};
-  unsigned long long ph[NPHASE] = {};
+  unsigned long long ph[PHASE_BIN0] = {};
+  const unsigned long long g_start = globaltimer();
   long long tc = clock64();
   auto tick = [&](int k) {
     if constexpr (PROF) {
@@ -1749,6 +1838,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   for (unsigned itn = 0;; ++itn) {
     const int slot = itn & 1;
     mbar_wait(&ctl.item_full[slot], (itn >> 1) & 1);
+    if constexpr (PROF) {
+      if (tid == 0 && P.phase) {  // item-wait by time bin
+        const int bin = (int)min((globaltimer() - g_start) >> 20, (unsigned long long)(PHASE_NBIN - 1));
+        P.phase[blockIdx.x * NPHASE + PHASE_BIN0 + bin] += (unsigned long long)(clock64() - tc);
+      }
+    }
     tick(0);
     const ItemInfo& it = ctl.items[slot];  // stays in smem: the slot is released at item end
     if (it.task < 0) {

@@ -130,9 +130,11 @@ struct ExecParams {
   int32_t* depart_seq;             // observed departure order (matrix tile ids)
   int32_t* depart_seq_ctr;
 };
-constexpr int NPHASE = 28;  // item-wait, mainloop, epilogue, job-end, item-end, completion, items, jobs,
+constexpr int NPHASE = 60;  // item-wait, mainloop, epilogue, job-end, item-end, completion, items, jobs,
                             // special: load, factor, inverse, store; potrf/trtri sub-steps;
-                            // producer: slot-wait, pop, produce, pops; storer: quarters, job-end, item-end, idle
+                            // producer: slot-wait, pop, produce, pops; storer: quarters, job-end, item-end, idle;
+                            // 28..59: consumer item-wait cycles in 2^20 ns (~1 ms) bins from the CTA's start
+constexpr int PHASE_BIN0 = 28, PHASE_NBIN = 32;
 
 inline int64_t tri_index(int64_t i, int64_t j) { return i * (i + 1) / 2 + j; }
 

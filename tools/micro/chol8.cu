@@ -38,6 +38,25 @@ __device__ __forceinline__ int chol8_inv(const double* S, int ld, int p0, double
   return bad;
 }
 
+// the executor's inv8: x[i][i] = 1 / l[i][i] (IEEE division), so an inverse
+// formed from a stored factor is bitwise the one formed inside the factor
+__device__ __forceinline__ void inv8_div(const double (&l)[8][8], double (&x)[8][8]) {
+  double d[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) d[i] = 1.0 / l[i][i];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    x[c][c] = d[c];
+#pragma unroll
+    for (int i = c + 1; i < 8; ++i) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = c; k < i; ++k) t = fma(l[i][k], x[k][c], t);
+      x[i][c] = -t * d[i];
+    }
+  }
+}
+
 template <int MODE>
 __global__ void k(double* out, long long* cyc) {
   __shared__ double S[40 * 129];
@@ -49,7 +68,8 @@ __global__ void k(double* out, long long* cyc) {
     double l[8][8], x[8][8];
     const int p0 = (it & 3) * 8;
     int bad = chol8_inv(S, 129, p0, l, x);
-    if (MODE == 1) {
+    if (MODE == 2) inv8_div(l, x);
+    if (MODE == 1 || MODE == 2) {
       const int q = (p0 + 8 + threadIdx.x) % 40;
       double av[8], v[8];
 #pragma unroll
@@ -78,5 +98,7 @@ int main() {
   printf("chol8_inv (+ barrier): %lld cycles\n", *cyc);
   k<1><<<1, 128>>>(out, cyc); cudaDeviceSynchronize(); k<1><<<1, 128>>>(out, cyc); cudaDeviceSynchronize();
   printf("chol8_inv + row solve (+ barrier): %lld cycles\n", *cyc);
+  k<2><<<1, 128>>>(out, cyc); cudaDeviceSynchronize(); k<2><<<1, 128>>>(out, cyc); cudaDeviceSynchronize();
+  printf("chol8_inv + inverse by division + row solve (+ barrier): %lld cycles\n", *cyc);
   return 0;
 }
