@@ -732,27 +732,6 @@ __device__ void zero_upper_row(double* tile, int d, int R, int64_t bp) {
 // register factor / inverse blocks, DMMA for every product.
 constexpr unsigned FULL = 0xffffffffu;
 
-// x = l^-1 for a lower 8x8 l in registers (x[i][i] = 1 / l[i][i], column-wise
-// forward substitution). The one routine behind every 8x8 diagonal inverse, so
-// an inverse formed inside POTRF and one formed later from the stored factor
-// (TRTRI / INV of a received or reused tile) are bitwise equal.
-__device__ __forceinline__ void inv8(const double (&l)[8][8], double (&x)[8][8]) {
-  double d[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) d[i] = 1.0 / l[i][i];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    x[c][c] = d[c];
-#pragma unroll
-    for (int i = c + 1; i < 8; ++i) {
-      double t = 0.0;
-#pragma unroll
-      for (int k = c; k < i; ++k) t = fma(l[i][k], x[k][c], t);
-      x[i][c] = -t * d[i];
-    }
-  }
-}
-
 // ---- dataflow 128x128 block Cholesky (tools/micro/potrf_flow.cu times it and
 // checks it against the look-ahead version it replaced: 66K -> 42K cycles).
 //
@@ -835,6 +814,31 @@ __device__ __forceinline__ void upd_blk(double* S, int p0, int ti, int tj) {
   dmma(x, a0, b0);
   dmma(x, a1, b1);
   *cp = make_double2(x[0], x[1]);
+}
+
+// Column c of x = l^-1 for the stored lower 8x8 block l at (p0, p0) of S, by
+// one thread (eight threads form one block's inverse): x_cc = 1 / l_cc,
+// x_ic = -(sum_{k<i} l_ik x_kc, fma in ascending k from 0.0) * x_ii with x_kc = 0
+// for k < c. The one routine behind every 8x8 diagonal inverse (TRTRI, INV of a
+// received tile, the inverse half of POTRF_INV), so they are bitwise equal.
+// out: the full 8x8 (zero upper).
+__device__ __forceinline__ void diag_inv8_col(const double* S, int p0, int c, double* out) {
+  double l[8][8], d[8], x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) l[i][j] = S[(p0 + i) * SLD + p0 + j];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) d[i] = 1.0 / l[i][i];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) t = fma(l[i][k], x[k], t);
+    x[i] = i < c ? 0.0 : (i == c ? d[i] : -t * d[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) out[8 * i + c] = x[i];
 }
 
 // In-place Cholesky of the lower 128x128 block in S (all 256 consumer
@@ -1024,8 +1028,7 @@ __device__ __forceinline__ void dmma_group16x32(const double* L, int lld, int lr
 }
 
 // In-place inverse of the lower-triangular 128x128 block in S by recursive
-// doubling: the sixteen 8x8 diagonal inverses (inv8, from the stored factor),
-// then for s = 8, 16, 32, 64 every pair [[A,0],[B,C]] ->
+// doubling: the sixteen 8x8 diagonal inverses (diag_inv8_col), then for s = 8, 16, 32, 64 every pair [[A,0],[B,C]] ->
 // [[A^-1,0],[-C^-1 B A^-1, C^-1]] with the products on DMMA. Strict upper
 // part of S must be zero on entry. Per level s and pair c, T = B A^-1 (A^-1
 // lower: k >= first output column) into scratch, then X21 = -C^-1 T (C^-1
@@ -1042,22 +1045,8 @@ __device__ void block_trtri_dmma(double* S, unsigned long long* ctl_dbg) {
     tq = now;
     ++pk;
   };
-  {  // the 16 diagonal 8x8 inverses
-    if (tid < BLK / 8) {
-      double l[8][8], x[8][8];
-      const int p0 = 8 * tid;
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) l[i][j] = j <= i ? S[(p0 + i) * SLD + p0 + j] : 0.0;
-      inv8(l, x);
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) S[BLK * SLD + XD_OFF + 64 * tid + 8 * i + j] = j <= i ? x[i][j] : 0.0;
-    }
-    cons_bar();
-  }
+  if (tid < BLK) diag_inv8_col(S, 8 * (tid >> 3), tid & 7, S + BLK * SLD + XD_OFF + 64 * (tid >> 3));
+  cons_bar();  // the 16 diagonal 8x8 inverses, one column per thread
   {
     // 16x16 diagonal inverses from the 8x8 ones (warp w = pair of 8x8 blocks
     // 2w, 2w + 1): X21 = -C^-1 (B A^-1), two 8x8 DMMA tiles
@@ -1168,7 +1157,7 @@ __device__ __noinline__ void run_special(const Job& jb, const ItemInfo& it, cons
       zero_upper_row(dst, d, R, bp);
       cons_bar();
       t1 = clock64();
-      block_trtri_dmma(S, ctl.dbg2);  // the 8x8 diagonal inverses from the stored factor, as TRTRI forms them
+      block_trtri_dmma(S, ctl.dbg2);
       t2 = clock64();
       double* aux = P.pool + (int64_t)src_s * P.slot_elems;
       store_block_lower(S, aux + (int64_t)d * BLK * bp + d * BLK, bp);
