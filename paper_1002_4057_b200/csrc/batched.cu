@@ -555,6 +555,9 @@ cudaError_t launch_bsmall(const double* dA, double* dX, int64_t batch, int64_t n
   // TINV_BSMALL_PROF=1: per-phase clock64 spans of thread 0, printed per launch
   // (process-wide state: like a context, this entry point is not thread-safe)
   static const int prof_mode = getenv("TINV_BSMALL_PROF") && atoi(getenv("TINV_BSMALL_PROF")) ? 1 : 0;
+  // TINV_BSMALL_PAD_KB: extra dynamic shared memory per CTA (a profiling knob:
+  // 32 -> 2 CTAs per SM, 64 -> 1, so the phase profile shows uncontended spans)
+  static const int pad_smem = getenv("TINV_BSMALL_PAD_KB") ? atoi(getenv("TINV_BSMALL_PAD_KB")) * 1024 : 0;
   static unsigned long long* dprof[64] = {};
   static uint64_t attr_set = 0;  // devices whose kernel attributes are set
   int dev = 0;
@@ -570,9 +573,11 @@ cudaError_t launch_bsmall(const double* dA, double* dX, int64_t batch, int64_t n
       if (r == cudaSuccess) r = cudaMemcpyToSymbol(bsm::c_nops, nops, sizeof nops);
       if (r != cudaSuccess) return r;
     }
-    r = cudaFuncSetAttribute(bsm::k_bsmall<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm::SMEM_DYN);
+    r = cudaFuncSetAttribute(bsm::k_bsmall<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             bsm::SMEM_DYN + pad_smem);
     if (r == cudaSuccess)
-      r = cudaFuncSetAttribute(bsm::k_bsmall<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bsm::SMEM_DYN);
+      r = cudaFuncSetAttribute(bsm::k_bsmall<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               bsm::SMEM_DYN + pad_smem);
     if (r == cudaSuccess && prof_mode) r = cudaMalloc(&dprof[dev], 4 * sizeof(unsigned long long));
     if (r != cudaSuccess) return r;
     attr_set |= 1ull << dev;
@@ -582,10 +587,10 @@ cudaError_t launch_bsmall(const double* dA, double* dX, int64_t batch, int64_t n
   for (int64_t b0 = 0; b0 < batch; b0 += 0x7fffffff) {
     const int64_t cnt = batch - b0 < 0x7fffffff ? batch - b0 : 0x7fffffff;
     if (prof_mode)
-      bsm::k_bsmall<true><<<(unsigned)cnt, bsm::NT, bsm::SMEM_DYN, st>>>(dA + b0 * stride, dX + b0 * stride, (int)n,
+      bsm::k_bsmall<true><<<(unsigned)cnt, bsm::NT, bsm::SMEM_DYN + pad_smem, st>>>(dA + b0 * stride, dX + b0 * stride, (int)n,
                                                                          nb, stride, dfail, id0 + b0, dprof[dev]);
     else
-      bsm::k_bsmall<false><<<(unsigned)cnt, bsm::NT, bsm::SMEM_DYN, st>>>(dA + b0 * stride, dX + b0 * stride, (int)n,
+      bsm::k_bsmall<false><<<(unsigned)cnt, bsm::NT, bsm::SMEM_DYN + pad_smem, st>>>(dA + b0 * stride, dX + b0 * stride, (int)n,
                                                                           nb, stride, dfail, id0 + b0, nullptr);
   }
   if (prof_mode) {
