@@ -362,8 +362,9 @@ def execute_multi_gpu(stream: TaskStream, a, grid=None, partition=True):
     mg = MultiGPU(stream, ctx, grid, a.label)
     rc, err, _ = mg.run()
     src_id = int(mg.src[err.task_id]) if rc != _native.OK and 0 <= err.task_id < len(mg.src) else -1
+    # control-plane tensors live where the backend can gather them (gloo: host)
     info = torch.tensor([src_id if src_id >= 0 else 2 ** 62, err.code, err.index, rc], dtype=torch.int64,
-                        device="cuda")
+                        device="cuda" if dist.get_backend() == "nccl" else "cpu")
     allinfo = [torch.zeros_like(info) for _ in range(mg.world)]
     dist.all_gather(allinfo, info)
     fails = [x.tolist() for x in allinfo if x[3] != 0]

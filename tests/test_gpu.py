@@ -659,3 +659,19 @@ def test_share_slots_bitwise_and_smaller(n, b, placement, loops):
     if placement == "out":
         assert sizes[1] < sizes[0]
     assert np.array_equal(P.invert(a, b, cfg, share_slots=True), outs[0])
+
+
+@pytest.mark.parametrize("grid", [(1, 2), (2, 2)])
+def test_multi_process_ipc_path_on_one_gpu(grid):
+    """The multi-PROCESS data path (`execute_multi_gpu`: CUDA-IPC mapped
+    partitioned stores, receive bases, system-scope inbox flags, owned-tile
+    gather), two / four ranks as separate processes and CUDA contexts sharing
+    cuda:0 (gloo control plane; the driver time-slices the executors), bitwise
+    against one process running scheduler.py:261-351's `execute`."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "two_proc_one_gpu.py"), "512", "128",
+                        str(grid[0]), str(grid[1])], capture_output=True, text=True, timeout=400)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "bitwise equal to one process: True" in r.stdout

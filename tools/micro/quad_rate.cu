@@ -116,6 +116,13 @@ __global__ void __launch_bounds__(128, 3) k(double* out, long long* cyc, int rep
     } else if (V == 2) {
 #pragma unroll
       for (int sl = 0; sl < 4; ++sl) mma_quad_pipe<false, true>(SA, SB, warp, sl, k0, k1, acc[sl]);
+    } else if (V == 3) {  // register operands only: 256 DMMAs per warp per rep
+      const double a = 1.0 + tid * 1e-9, b = 1.0 - tid * 1e-9;
+      for (int i = 0; i < 16; ++i)
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"((&acc[0][0][0][0])[2 * q]), "+d"((&acc[0][0][0][0])[2 * q + 1]) : "d"(a), "d"(b));
     } else {
       mma_w32<false, true>(SA, SB, warp >> 1, warp & 1, k0, k1, *reinterpret_cast<double(*)[4][4][2]>(&acc));
     }
@@ -129,14 +136,22 @@ __global__ void __launch_bounds__(128, 3) k(double* out, long long* cyc, int rep
 
 template <int V>
 void run(int per_sm, int sms, double* out, long long* cyc) {
-  const int reps = 200;
+  const int reps = 2000;
   const int smem = per_sm == 1 ? 128 * 1024 : per_sm == 2 ? 96 * 1024 : 64 * 1024;
   cudaFuncSetAttribute(k<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int grid = sms * per_sm;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float ms = 0;
   for (int it = 0; it < 2; ++it) {
+    cudaEventRecord(e0);
     k<V><<<grid, 128, smem>>>(out, cyc, reps, 0, 64);
+    cudaEventRecord(e1);
     cudaDeviceSynchronize();
+    cudaEventElapsedTime(&ms, e0, e1);
   }
+  printf("  kernel %.3f ms -> %.2f TFLOP/s by events\n", ms, 512.0 * 1024 * reps * grid / ms / 1e9);
   double mean = 0;
   for (int i = 0; i < grid; ++i) mean += (double)cyc[i];
   mean /= grid;
@@ -154,5 +169,6 @@ int main() {
   for (int c = 1; c <= 3; ++c) run<0>(c, p.multiProcessorCount, out, cyc);
   for (int c = 1; c <= 3; ++c) run<2>(c, p.multiProcessorCount, out, cyc);
   for (int c = 1; c <= 3; ++c) run<1>(c, p.multiProcessorCount, out, cyc);
+  for (int c = 1; c <= 3; ++c) run<3>(c, p.multiProcessorCount, out, cyc);
   return 0;
 }
