@@ -249,6 +249,13 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TINV_BENCH_ONE_GPU=1: functional check of the N > 1 code path on a box
+    # with one GPU -- every rank is its own process and CUDA context on cuda:0,
+    # gloo instead of NCCL (which refuses two ranks on one device); the driver
+    # time-slices the ranks' executors, so the printed numbers mean nothing
+    one_gpu = world > 1 and os.environ.get("TINV_BENCH_ONE_GPU", "0") == "1"
+    if one_gpu:
+        local = 0
     wl = {"c1": (1024, 128, 1), "c2": (8192, 256, 1), "c3": (32768, 512, 1), "c4": (256, 256, 8192),
           "c5": (65536, 1024, 1)}[args.workload]
     shift = 1e-3 if args.workload == "c5" else 1.0  # BASELINE config 5: harder conditioning (cond ~4e3)
@@ -331,7 +338,11 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctl_dev = "cpu" if one_gpu else "cuda"  # where small control-plane tensors live
 
     def barrier():
         if dist is not None:
@@ -341,7 +352,7 @@ def main():
     def max_over_ranks(x):
         if dist is None:
             return x
-        v = torch.tensor([x], dtype=torch.float64, device="cuda")
+        v = torch.tensor([x], dtype=torch.float64, device=ctl_dev)
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         return float(v.item())
 
@@ -480,7 +491,7 @@ def main():
                 "sm_busy_frac": {"min": float(busy.min()), "mean": float(busy.mean()), "max": float(busy.max())},
                 "source": "per-CTA idle ns of the executor's scheduler warp (tinv_plan_cta_idle), last timed step"}
         if dist is not None:
-            v = torch.tensor([float(busy.mean())], dtype=torch.float64, device="cuda")
+            v = torch.tensor([float(busy.mean())], dtype=torch.float64, device=ctl_dev)
             allb = [torch.zeros_like(v) for _ in range(world)]
             dist.all_gather(allb, v)
             load["rank_busy_frac"] = [float(x.item()) for x in allb]

@@ -675,3 +675,23 @@ def test_multi_process_ipc_path_on_one_gpu(grid):
                         str(grid[0]), str(grid[1])], capture_output=True, text=True, timeout=400)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "bitwise equal to one process: True" in r.stdout
+
+
+def test_bench_multi_rank_path_on_one_gpu():
+    """bench.py's N > 1 path under the driver's torchrun launch line, two ranks
+    as separate processes on cuda:0 (TINV_BENCH_ONE_GPU=1: gloo control plane,
+    time-sliced executors -- a functional check, the numbers mean nothing)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TINV_BENCH_ONE_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 400),
+                        os.path.join(root, "bench.py"), "--gpus", "2", "--workload", "c1", "--steps", "2",
+                        "--warmup", "3", "--no-cpu"], capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stdout[-1500:] + r.stderr[-1500:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["config"]["transfers"] > 0 and d["residual"] < 10 and d["symmetry_err"] == 0.0
+    assert d["e2e"]["value"] > 0
