@@ -1916,6 +1916,9 @@ static int plan_exec_impl(tinv_plan* p, tinv_err* err, double* ms, const HostIO*
   P.slot_elems = c->slot_elems;
   P.bp = (int32_t)c->bp;
   P.R = (int32_t)c->R;
+  // TINV_NO_KTRIM=1 (A/B switch): treat the padding as data, as before round 2
+  static const bool no_ktrim = getenv("TINV_NO_KTRIM") && atoi(getenv("TINV_NO_KTRIM"));
+  P.b = no_ktrim ? (int32_t)c->bp : (int32_t)c->b;
   P.ntasks = (int32_t)nx;
   P.scratch_base = (int32_t)scratch_base;
   P.tasks = p->d_tasks;

@@ -566,13 +566,18 @@ __device__ __forceinline__ void run_gemm(const Job& jb, const ExecParams& P, Sme
 
   for (int kb = jb.k0; kb < jb.k1; ++kb) {
     const bool ma = (kb == jb.a_mask), mb = (kb == jb.b_mask);
+    // a tile order b that is not a multiple of 128 is padded to bp: K chunks
+    // that lie wholly in the padding contribute zero (or, on a diagonal tile's
+    // unit padding, only to the output's own padding): skip their DMMAs
+    const int kreal = P.b - kb * BLK;
     for (int ch = 0; ch < BLK / KCH; ++ch, ++ks) {
       const int st = ks % NSTAGE;
       mbar_wait(&ctl.full[st], (ks / NSTAGE) & 1);
       const char* sA = ring + st * STAGE_BYTES;
       const char* sB = sA + STAGE_BYTES / 2;
       const int kb16 = ch * KCH;
-      if (!ma && !mb) {
+      if (kb16 >= kreal) {
+      } else if (!ma && !mb) {
         chunk_mma<V, false, false>(sA, sB, acc, wm, wn, g, tg, kb16);
       } else {
         // on a triangular operand's diagonal block, a chunk whose masked part

@@ -82,6 +82,7 @@ struct ExecParams {
   int64_t slot_elems;      // bp * bp
   int32_t bp;              // padded tile order (multiple of BLK)
   int32_t R;               // bp / BLK
+  int32_t b;               // the tile order itself (rows / columns >= b of a slot are padding)
   int32_t ntasks;
   int32_t scratch_base;    // slot of CTA 0's scratch tile; CTA c uses scratch_base + c
   const TaskDev* tasks;
