@@ -129,9 +129,13 @@ __global__ void __launch_bounds__(256) k_get(double* __restrict__ dst, int64_t l
   const bool diag_mix = symmetrize && I == J && sr == sc;
   if (mirror && !diag_mix) {  // the transposed copy into tile (J, I), sub-block (sc, sr)
     if (vec) {
+      // a warp covers two destination rows (k) x 16 column pairs: its column
+      // reads sm[c2][k], sm[c2 + 1][k] (row stride 65) then hit 16 distinct
+      // 8-byte banks per half warp (32 pairs of one row: 2-way conflicts)
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int idx = tid + 256 * u, k = idx >> 5, c2 = 2 * (idx & 31);
+        const int idx = tid + 256 * u, w = idx >> 5, l = idx & 31;
+        const int k = 2 * (w >> 1) + (l & 1), c2 = 2 * ((l >> 1) + 16 * (w & 1));
         const int r = sc * GSB + k, c = sr * GSB + c2;
         if (r >= b || c >= b) continue;
         *reinterpret_cast<double2*>(dst + ((int64_t)J * b + r - row0) * ldd + (int64_t)I * b + c) =
