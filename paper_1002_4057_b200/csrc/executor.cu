@@ -411,6 +411,7 @@ struct SmemCtl {
   PotrfFlags pf;  // block_potrf's warp-0 / helper counters
 };
 
+constexpr unsigned FULL_MASK = 0xffffffffu;
 // ---------------------------------------------------------------- consumers: DMMA chunk
 // Warp w: rows [64*(w&1), +64), cols [32*(w>>1), +32) of the 128x128 block.
 // A/B stage layouts: K-major = TMA box {16 k, 128 rows}; MN-major = 8 boxes
@@ -614,18 +615,42 @@ __device__ __forceinline__ void run_gemm(const Job& jb, const ExecParams& P, Sme
         const unsigned use = 2 * es.tjobs + (k >> 1);
         mbar_wait(&ctl.stg_free[buf], (use & 1) ^ 1);
         char* sb = stg + buf * 32768;
+        // 16-byte stores, conflict-free per quarter warp (two rows g, g + 1 x
+        // four lanes tg must hit eight distinct 16-byte chunks of the swizzled
+        // 128-byte rows): NT exchanges one value with lane tg ^ 1 so each lane
+        // holds two adjacent columns; NN / TN hold adjacent columns in
+        // acc[p][2 qq][e], acc[p][2 qq + 1][e] and odd rows store e = 1 first.
+        // (8-byte stores here were 2- to 4-way conflicts: 3.7e9 excess
+        // wavefronts a C3 launch, profiles/r02/final/ncu_exec_c3_full_metrics.csv)
+        auto st2 = [&](int r, int c, double v0, double v1) {
+          *reinterpret_cast<double2*>(sb + (c >> 4) * 4096 + r * 128 + ((((c & 15) >> 1) ^ (r & 7)) << 4)) =
+              make_double2(sg * v0, sg * v1);
+        };
 #pragma unroll
         for (int pp = 0; pp < 4; ++pp) {
           const int p = 4 * (k & 1) + pp;
           const int r = out_row<V>(wm, p, g) - 32 * k;
+          if constexpr (V == V_NT) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int c = out_col<V>(wn, q, 2 * tg + e);
-              *reinterpret_cast<double*>(sb + (c >> 4) * 4096 + r * 128 + ((((c & 15) >> 1) ^ (r & 7)) << 4) +
-                                         (c & 1) * 8) = sg * acc[p][q][e];
+            for (int q = 0; q < 4; ++q) {  // columns 32 wn + 8 q + tg (e = 0), + 4 (e = 1)
+              const double mine0 = acc[p][q][0], mine1 = acc[p][q][1];
+              const double got = __shfl_xor_sync(FULL_MASK, (tg & 1) ? mine0 : mine1, 1);
+              const int c = 32 * wn + 8 * q + ((tg & 1) ? tg + 3 : tg);
+              st2(r, c, (tg & 1) ? got : mine0, (tg & 1) ? mine1 : got);
             }
+          } else {
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const bool flip = g & 1;  // this lane's e for this instruction: e ^ (g & 1)
+                const double v0 = flip ? acc[p][2 * qq][e ^ 1] : acc[p][2 * qq][e];
+                const double v1 = flip ? acc[p][2 * qq + 1][e ^ 1] : acc[p][2 * qq + 1][e];
+                const int el = e ^ (int)flip;
+                const int c = out_col<V>(wn, 2 * qq, 2 * tg + el);
+                st2(r, c, v0, v1);
+              }
+          }
         }
         fence_proxy_async_smem();
         asm volatile("bar.sync %0, 128;" ::"r"(2 + wm) : "memory");
