@@ -61,13 +61,16 @@ __global__ void __launch_bounds__(256) k_put(const double* __restrict__ src, int
 // row I is fixed (`panel_i` >= 0) and J = blockIdx.x; otherwise (I, J)
 // enumerates the lower tiles (LOWER) or the full t x t grid (SYMMETRIZE).
 // grid.y: sub-block index. `vec`: b, bp and ldd even (16-byte alignment).
-constexpr int GSB = 64;
-__global__ void __launch_bounds__(256) k_get(double* __restrict__ dst, int64_t ldd, int64_t row0,
+template <int GSB, int NT>
+__global__ void __launch_bounds__(NT) k_get(double* __restrict__ dst, int64_t ldd, int64_t row0,
                                             const double* __restrict__ pool, int64_t slot_elems,
                                             const int32_t* __restrict__ slot_of, int b, int bp, int t,
                                             int panel_i, int64_t tile_lo, int symmetrize, int64_t T1,
                                             int64_t mstride, int vec) {
-  __shared__ double sm[GSB][GSB + 1];
+  extern __shared__ double sm_raw[];
+  double (*sm)[GSB + 1] = reinterpret_cast<double (*)[GSB + 1]>(sm_raw);
+  constexpr int HP = GSB / 2;             // column pairs per row
+  constexpr int NIT = GSB * HP / NT;      // pairs per thread
   int I, J;
   int64_t m = 0;
   if (panel_i >= 0) {
@@ -110,9 +113,9 @@ __global__ void __launch_bounds__(256) k_get(double* __restrict__ dst, int64_t l
   const double* tile = pool + (int64_t)src_slot * slot_elems;
   const int br = transp ? sc : sr, bc = transp ? sr : sc;  // source sub-block
   if (vec) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int idx = tid + 256 * u, k = idx >> 5, c2 = 2 * (idx & 31);
+#pragma unroll 8
+    for (int u = 0; u < NIT; ++u) {
+      const int idx = tid + NT * u, k = idx / HP, c2 = 2 * (idx % HP);
       const int r = br * GSB + k, c = bc * GSB + c2;
       double2 v = make_double2(0.0, 0.0);
       if (r < b && c < b) v = __ldcs(reinterpret_cast<const double2*>(tile + (int64_t)r * bp + c));
@@ -120,8 +123,8 @@ __global__ void __launch_bounds__(256) k_get(double* __restrict__ dst, int64_t l
       sm[k][c2 + 1] = v.y;
     }
   } else {
-    for (int idx = tid; idx < GSB * GSB; idx += 256) {
-      const int k = idx >> 6, cc = idx & 63, r = br * GSB + k, c = bc * GSB + cc;
+    for (int idx = tid; idx < GSB * GSB; idx += NT) {
+      const int k = idx / GSB, cc = idx % GSB, r = br * GSB + k, c = bc * GSB + cc;
       sm[k][cc] = (r < b && c < b) ? tile[(int64_t)r * bp + c] : 0.0;
     }
   }
@@ -132,18 +135,19 @@ __global__ void __launch_bounds__(256) k_get(double* __restrict__ dst, int64_t l
       // a warp covers two destination rows (k) x 16 column pairs: its column
       // reads sm[c2][k], sm[c2 + 1][k] (row stride 65) then hit 16 distinct
       // 8-byte banks per half warp (32 pairs of one row: 2-way conflicts)
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = tid + 256 * u, w = idx >> 5, l = idx & 31;
-        const int k = 2 * (w >> 1) + (l & 1), c2 = 2 * ((l >> 1) + 16 * (w & 1));
+#pragma unroll 8
+      for (int u = 0; u < NIT; ++u) {
+        constexpr int WPR = HP / 16;  // warps per pair of destination rows
+        const int idx = tid + NT * u, w = idx >> 5, l = idx & 31;
+        const int k = 2 * (w / WPR) + (l & 1), c2 = 2 * ((l >> 1) + 16 * (w % WPR));
         const int r = sc * GSB + k, c = sr * GSB + c2;
         if (r >= b || c >= b) continue;
         *reinterpret_cast<double2*>(dst + ((int64_t)J * b + r - row0) * ldd + (int64_t)I * b + c) =
             make_double2(sm[c2][k], sm[c2 + 1][k]);
       }
     } else {
-      for (int idx = tid; idx < GSB * GSB; idx += 256) {
-        const int k = idx >> 6, cc = idx & 63, r = sc * GSB + k, c = sr * GSB + cc;
+      for (int idx = tid; idx < GSB * GSB; idx += NT) {
+        const int k = idx / GSB, cc = idx % GSB, r = sc * GSB + k, c = sr * GSB + cc;
         if (r >= b || c >= b) continue;
         dst[((int64_t)J * b + r - row0) * ldd + (int64_t)I * b + c] = sm[cc][k];
       }
@@ -154,17 +158,17 @@ __global__ void __launch_bounds__(256) k_get(double* __restrict__ dst, int64_t l
     return transp ? sm[cc][k] : sm[k][cc];
   };
   if (vec) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int idx = tid + 256 * u, k = idx >> 5, c2 = 2 * (idx & 31);
+#pragma unroll 8
+    for (int u = 0; u < NIT; ++u) {
+      const int idx = tid + NT * u, k = idx / HP, c2 = 2 * (idx % HP);
       const int r = sr * GSB + k, c = sc * GSB + c2;  // destination element within tile (I, J)
       if (r >= b || c >= b) continue;
       *reinterpret_cast<double2*>(dst + ((int64_t)I * b + r - row0) * ldd + (int64_t)J * b + c) =
           make_double2(val(k, c2), val(k, c2 + 1));
     }
   } else {
-    for (int idx = tid; idx < GSB * GSB; idx += 256) {
-      const int k = idx >> 6, cc = idx & 63, r = sr * GSB + k, c = sc * GSB + cc;
+    for (int idx = tid; idx < GSB * GSB; idx += NT) {
+      const int k = idx / GSB, cc = idx % GSB, r = sr * GSB + k, c = sc * GSB + cc;
       if (r >= b || c >= b) continue;
       dst[((int64_t)I * b + r - row0) * ldd + (int64_t)J * b + c] = val(k, cc);
     }
@@ -184,12 +188,15 @@ cudaError_t launch_get(double* dst, int64_t ldd, int64_t row0, const double* poo
                        const int32_t* slot_of, int b, int bp, int t, int panel_i, int64_t tile_lo,
                        int64_t ntiles, int symmetrize, cudaStream_t st, int64_t T1, int64_t mstride) {
   if (ntiles <= 0) return cudaSuccess;
-  const int nsb = (b + GSB - 1) / GSB;
   const int vec = ((ldd | b | bp | row0) & 1) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0 &&
                   ((mstride & 1) == 0);
+  // (128x128 sub-blocks -- 1 KB row segments, 132 KB of shared memory, one CTA per SM -- measured
+  // 2.37 ms against 2.30 ms for 64x64 at C3)
+  constexpr int G = 64, NT = 256;
+  const int nsb = (b + G - 1) / G;
   dim3 grid((unsigned)ntiles, (unsigned)(nsb * nsb));
-  k_get<<<grid, 256, 0, st>>>(dst, ldd, row0, pool, slot_elems, slot_of, b, bp, t, panel_i, tile_lo, symmetrize, T1,
-                              mstride, vec);
+  k_get<G, NT><<<grid, NT, G * (G + 1) * 8, st>>>(dst, ldd, row0, pool, slot_elems, slot_of, b, bp, t, panel_i, tile_lo,
+                                                  symmetrize, T1, mstride, vec);
   return cudaGetLastError();
 }
 
