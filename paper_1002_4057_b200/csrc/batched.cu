@@ -713,7 +713,27 @@ int tinv_batch_small_host(const double* hA, double* hX, int64_t batch, int64_t n
     const int64_t m0 = c * chunk, cnt = std::min(chunk, batch - m0);
     const size_t bytes = (size_t)(cnt * mat_bytes);
     if (c >= BsHost::NS) BCK(cudaStreamWaitEvent(H.sh, H.d2h[s], 0));
-    BCK(cudaMemcpyAsync(H.slot[s], hA + m0 * n * n, bytes, cudaMemcpyHostToDevice, H.sh));
+    // The engine reads only A's lower 64x64 blocks (diagonal blocks whole): for
+    // nb >= 2 block rows copy block row i as one 3D transfer of its first
+    // 64 (i + 1) columns (n = 256: 62.5 % of the bytes; the slot's other blocks
+    // keep stale data the kernel never reads). TINV_BSMALL_H2D_FULL=1: whole matrices.
+    static const bool h2d_full = getenv("TINV_BSMALL_H2D_FULL") && atoi(getenv("TINV_BSMALL_H2D_FULL"));
+    const int nbr = (int)((n + bsm::BB - 1) / bsm::BB);
+    if (h2d_full || nbr < 2) {
+      BCK(cudaMemcpyAsync(H.slot[s], hA + m0 * n * n, bytes, cudaMemcpyHostToDevice, H.sh));
+    } else {
+      for (int i = 0; i < nbr; ++i) {
+        cudaMemcpy3DParms cp = {};
+        cp.srcPtr = make_cudaPitchedPtr((void*)(hA + m0 * n * n), (size_t)n * 8, (size_t)n, (size_t)n);
+        cp.dstPtr = make_cudaPitchedPtr((void*)H.slot[s], (size_t)n * 8, (size_t)n, (size_t)n);
+        cp.srcPos = make_cudaPos(0, (size_t)i * bsm::BB, 0);
+        cp.dstPos = cp.srcPos;
+        cp.extent = make_cudaExtent((size_t)std::min<int64_t>((int64_t)(i + 1) * bsm::BB, n) * 8,
+                                    (size_t)std::min<int64_t>(bsm::BB, n - (int64_t)i * bsm::BB), (size_t)cnt);
+        cp.kind = cudaMemcpyHostToDevice;
+        BCK(cudaMemcpy3DAsync(&cp, H.sh));
+      }
+    }
     BCK(cudaEventRecord(H.h2d[s], H.sh));
     BCK(cudaStreamWaitEvent(H.sc, H.h2d[s], 0));
     BCK(launch_bsmall(H.slot[s], H.slot[s], cnt, n, n * n, H.sc, H.dfail, m0));  // failure ids absolute
