@@ -688,9 +688,13 @@ def test_bench_multi_rank_path_on_one_gpu():
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, TINV_BENCH_ONE_GPU="1")
+    import socket
+    with socket.socket() as sk:  # a free rendezvous port
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
     try:
         r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                            "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 400),
+                            "--master-addr", "127.0.0.1", "--master-port", str(port),
                             os.path.join(root, "bench.py"), "--gpus", "2", "--workload", "c1", "--steps", "2",
                             "--warmup", "3", "--no-cpu"], capture_output=True, text=True, timeout=600, env=env,
                            cwd=root)

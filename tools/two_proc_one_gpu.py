@@ -49,7 +49,11 @@ if __name__ == "__main__":
     world = grid[0] * grid[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=worker, args=(r, world, n, nb, grid, 29611 + os.getpid() % 997, q)) for r in range(world)]
+    import socket
+    with socket.socket() as sk:  # a free rendezvous port
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ps = [ctx.Process(target=worker, args=(r, world, n, nb, grid, port, q)) for r in range(world)]
     for p in ps:
         p.start()
     for p in ps:
